@@ -1,0 +1,193 @@
+/*
+ * shockhash_b200.h - C-ABI of the B200-native ShockHash hot path.
+ *
+ * The reference's drop-in seam for this path is the kernel module object
+ * `shockhash._kernels.kernels` (/root/reference/pkg/src/shockhash/_kernels/
+ * __init__.py:23), whose functions are defined in _core.pyx / _pure.py.  Every
+ * batched entry point below replaces one of them (cited per function); the
+ * orchestration entry points replace the per-bucket Python loop of
+ * recsplit._build_hashed (recsplit.py:474-550) and MphfDescriptor.query_*
+ * (recsplit.py:251-285).  Plain pointers and sizes only, no torch types.
+ *
+ * Conventions
+ *   - Return value: SHK_OK (0) or an SHK_* code below; negative = CUDA error,
+ *     text via shk_last_error().
+ *   - flags & SHK_DEVICE: every array argument is a device pointer and the
+ *     call is stream-ordered on the context's stream (no host sync).  Without
+ *     it, arrays are host memory; the library copies them and returns when
+ *     the outputs are written.
+ *   - Keys are 128-bit master hash codes (hi, lo) as two uint64 arrays.
+ *   - A context is single-owner and not thread-safe (one per host thread).
+ *   - There is no CPU fallback: without a usable B200 every compute call
+ *     fails with a negative code.
+ */
+#ifndef SHOCKHASH_B200_H
+#define SHOCKHASH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SHK_OK = 0,
+  SHK_EXHAUSTED = 1,  /* seed search hit max_seed -> ConstructionFailureError */
+  SHK_FORMAT = 2,     /* bit-stream overrun -> FormatError */
+  SHK_INVALID = 3,    /* bad parameter -> InvalidParameterError */
+  SHK_UNSOLVABLE = 4, /* ribbon inconsistent for every tried seed */
+  SHK_DUPLICATE = 5   /* equal 128-bit codes in a build */
+};
+#define SHK_DEVICE 1
+
+typedef struct shk_ctx shk_ctx;
+typedef struct shk_build shk_build;
+typedef struct shk_qdesc shk_qdesc;
+
+const char* shk_last_error(void);
+int shk_version(void);
+int shk_device_count(int* n);
+int shk_ctx_create(int device, shk_ctx** out);
+int shk_ctx_destroy(shk_ctx* ctx);
+int shk_ctx_sync(shk_ctx* ctx);
+/* cudaStream_t of the context; shk_ctx_set_stream(ctx, NULL) restores the
+ * context's own stream. */
+void* shk_ctx_stream(shk_ctx* ctx);
+int shk_ctx_set_stream(shk_ctx* ctx, void* stream);
+int shk_ctx_num_sms(shk_ctx* ctx);
+/* Device memory from the context's caching pool (bench / zero-copy users). */
+int shk_dev_alloc(shk_ctx* ctx, size_t bytes, void** out);
+int shk_dev_free(shk_ctx* ctx, void* p);
+int shk_memcpy(shk_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /*0 H2D 1 D2H 2 D2D*/);
+/* Events on the context stream: elapsed milliseconds between two records. */
+int shk_timer_start(shk_ctx* ctx);
+int shk_timer_stop(shk_ctx* ctx, float* ms);
+/* Number of kernels this library launched since context creation. */
+int64_t shk_launch_count(shk_ctx* ctx);
+
+/* ---- scalar hash family (__host__ __device__ source shared with kernels):
+ * mix64 _core.pyx:45-48, seed_mixer :51-52, remix :55-56, hash_range :59-60,
+ * leaf_pair :79-98, split_bit :101-102, leaf_cell :751-771 */
+uint64_t shk_mix64(uint64_t z);
+uint64_t shk_seed_mixer(uint64_t seed, uint64_t tag);
+uint64_t shk_remix(uint64_t hi, uint64_t lo, uint64_t seed, uint64_t tag);
+uint64_t shk_hash_range(uint64_t v, uint64_t m);
+void shk_leaf_pair(uint64_t hi, uint64_t lo, uint64_t seed, int n, int* h0, int* h1);
+int shk_split_bit(uint64_t hi, uint64_t lo, uint64_t seed);
+int shk_leaf_cell(uint64_t hi, uint64_t lo, int64_t q, int mleaf, int mode, int64_t cache_k, int choice);
+
+/* ---- leaf seed search, batched over L leaves in CSR form (leaf i = keys
+ * [leaf_off[i], leaf_off[i+1]), 1..64 keys).  Replaces search_plain
+ * (_core.pyx:186-229) for mode 0 and search_rotate(hi, lo, n, cache_k, ...)
+ * (_core.pyx:238-334) for mode 1, plus the orientation of the found seed
+ * (shockhash._finish -> pseudoforest.orient, pseudoforest.py:149-201).
+ * cache_k applies to leaves with more than cache_min_leaf keys (0 = always,
+ * matching the raw kernel; 32 = recsplit's rule, recsplit.py:577).
+ * seed_out[L]: minimum seed / encoded rotate seed, -1 if none < max_seed.
+ * fbits_out[L] (nullable): bit i = choice of key i.  stats_out[L*4]
+ * (nullable): (hash_evals, filter_passes, exact_checks, a_evals).
+ * team_warps: warps cooperating on one leaf (0 = heuristic, else 1/2/4/8). */
+int shk_leaf_search(shk_ctx* ctx, int mode, int cache_k, int cache_min_leaf, const uint64_t* hi, const uint64_t* lo,
+                    const int64_t* leaf_off, int64_t L, uint64_t max_seed, int team_warps, int64_t* seed_out,
+                    uint64_t* fbits_out, int64_t* stats_out, int flags);
+
+/* ---- canonical 1-orientation of L edge lists (pseudoforest.orient,
+ * pseudoforest.py:149-201).  eu/ev: cells per edge, CSR leaf_off (n <= 64
+ * edges on n cells).  ok_out[i] = 0 if list i is not a pseudoforest. */
+int shk_orient(shk_ctx* ctx, const uint8_t* eu, const uint8_t* ev, const int64_t* leaf_off, int64_t L,
+               uint64_t* fbits_out, int32_t* ok_out, int flags);
+
+/* ---- split-seed search on one node (split_seed_search, _core.pyx:385-428)
+ * and part indices (split_parts, _core.pyx:378-382).  fanout <= 4. */
+int shk_split_search(shk_ctx* ctx, const uint64_t* hi, const uint64_t* lo, int64_t m, const int64_t* sizes,
+                     int fanout, uint64_t max_seed, int64_t* seed_out, int64_t* evals_out);
+int shk_split_parts(shk_ctx* ctx, const uint64_t* hi, const uint64_t* lo, int64_t m, uint64_t seed,
+                    const int64_t* sizes, int fanout, int64_t* parts_out);
+
+/* ---- ribbon retrieval.  rows: ribbon_rows (_core.pyx:435-439); solve:
+ * ribbon_solve (_core.pyx:442-524) -> *consistent = 0 when the system is
+ * inconsistent (reference returns None); query: ribbon_query_many
+ * (_core.pyx:548-568); build: the seed loop of retrieval_build_arrays
+ * (retrieval.py:93-106) over seeds [0, max_tries). */
+int shk_ribbon_rows(shk_ctx* ctx, const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t m, uint64_t seed,
+                    int64_t* starts, uint64_t* pat0, uint64_t* pat1, int flags);
+int shk_ribbon_solve(shk_ctx* ctx, const int64_t* starts, const uint64_t* pat0, const uint64_t* pat1,
+                     const uint8_t* rhs, int64_t N, int64_t m, uint64_t* words_out, int* consistent, int flags);
+int shk_ribbon_query(shk_ctx* ctx, const int64_t* starts, const uint64_t* pat0, const uint64_t* pat1, int64_t N,
+                     const uint64_t* words, int64_t nwords, uint8_t* out, int flags);
+int shk_ribbon_build(shk_ctx* ctx, const uint64_t* hi, const uint64_t* lo, const uint8_t* rhs, int64_t N, int64_t m,
+                     int max_tries, uint64_t* seed_out, uint64_t* words_out, int flags);
+
+/* ---- Rice stream decode of `count` consecutive codes starting at bit pos
+ * (rice_decode_stream, _core.pyx:626-635, applied repeatedly). */
+int shk_rice_decode(shk_ctx* ctx, const uint64_t* words, int64_t nwords, int64_t bit_len, int64_t pos,
+                    const int32_t* g, int64_t count, int64_t* values_out, int64_t* pos_out);
+
+/* ---- master hash: blake2b-128 with salt (keys.master_hash_many,
+ * keys.py:46-58).  Keys are a byte blob with CSR offsets off[N+1]. */
+int shk_blake2b128(shk_ctx* ctx, const uint8_t* blob, int64_t blob_len, const int64_t* off, int64_t N, uint64_t salt,
+                   uint64_t* hi, uint64_t* lo, int flags);
+
+/* ---- plan tables (recsplit.flatten_plan, recsplit.py:95-119), one per
+ * distinct bucket size, concatenated: plan p covers nodes
+ * [plan_off[p], plan_off[p+1]); node fields are the reference's arrays
+ * (kind 0 split / 1 leaf, g, fanout, sizes_off into sizes_flat, subtree,
+ * m_node).  sizes_off is plan-local (as flatten_plan returns it); each plan's
+ * sizes start at sizes_base[p] in sizes_flat. */
+typedef struct shk_plans {
+  int64_t nplans;
+  const int64_t* plan_m;     /* bucket size of each plan */
+  const int64_t* plan_off;   /* [nplans+1] */
+  const int64_t* sizes_base; /* [nplans] */
+  const int64_t* kind;
+  const int64_t* g;
+  const int64_t* fanout;
+  const int64_t* sizes_off;
+  const int64_t* subtree;
+  const int64_t* m_node;
+  const int64_t* sizes_flat;
+} shk_plans;
+
+/* ---- MPHF construction (recsplit._build_hashed, recsplit.py:474-550).
+ * create: bucket hash, sort by (bucket, hi, lo), key_prefix, duplicate flag
+ *   (recsplit.py:475-483, :433-440).  *dup != 0 means equal 128-bit codes.
+ * run: split-seed searches + stable partitions, leaf searches, orientation
+ *   and the Rice stream for buckets [b0, b1) (recsplit.py:499-521).
+ * ribbon: retrieval over ALL keys with the choice bits (recsplit.py:523);
+ *   choice (nullable, host or device per flags) overrides the build's own.
+ * stats_out[7] of run: hash_evals, filter_passes, exact_checks, a_evals,
+ *   leaf_seed_bits, split_seed_bits, leaf_count (recsplit.py:539-547). */
+int shk_build_create(shk_ctx* ctx, const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nbuckets, int flags,
+                     shk_build** out, int* dup, int64_t* max_bucket);
+int shk_build_key_prefix(shk_build* b, uint64_t* key_prefix /* [nb+1] host */);
+int shk_build_sorted_keys(shk_build* b, uint64_t* hi, uint64_t* lo /* [N] host */);
+int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, int cache_min_leaf, int64_t b0,
+                  int64_t b1, uint64_t max_seed, int64_t* stats_out);
+int shk_build_stream_size(shk_build* b, int64_t* bit_len, int64_t* nwords);
+int shk_build_stream(shk_build* b, uint64_t* words /* [nwords] */, uint64_t* bit_offsets /* [b1-b0+1] */);
+int shk_build_choice(shk_build* b, uint8_t* choice /* [N] host, sorted key order */);
+/* record_placements (recsplit.py:493, :592-594): global slot of every sorted
+ * key as placed at construction time; enable before shk_build_run. */
+int shk_build_set_record_placements(shk_build* b, int on);
+int shk_build_placements(shk_build* b, int64_t* out /* [N] host */);
+int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int64_t m, int max_tries,
+                     uint64_t* seed_out, uint64_t* words_out /* [ceil(m/64)] host */);
+int shk_build_destroy(shk_build* b);
+
+/* ---- MPHF evaluation (MphfDescriptor.query_hashed_many ->
+ * query_stream, _core.pyx:642-742).  create uploads the descriptor and builds
+ * the per-node bit-position index; query returns SHK_FORMAT where the
+ * reference raises FormatError.  clamp=1 applies min(out, N-1)
+ * (recsplit.py:275). */
+int shk_qdesc_create(shk_ctx* ctx, int64_t n_keys, int64_t nbuckets, int mode, int64_t cache_k,
+                     const uint64_t* key_prefix, const uint64_t* bit_offsets, const uint64_t* stream_words,
+                     int64_t stream_nwords, int64_t stream_bit_len, const shk_plans* plans, uint64_t rib_seed,
+                     int64_t rib_m, const uint64_t* rib_words, int64_t rib_nwords, shk_qdesc** out);
+int shk_query(shk_qdesc* d, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out, int clamp, int flags);
+int shk_qdesc_destroy(shk_qdesc* d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHOCKHASH_B200_H */

@@ -1,0 +1,1227 @@
+// C-ABI of the B200 ShockHash hot path (declared in include/shockhash_b200.h)
+// plus the native build/query runtime: device memory pool, stream, plan
+// tables, level-by-level split scheduling, leaf batches, Rice stream
+// assembly and the ribbon seed loop.  Replaces the Python orchestration of
+// recsplit._build_hashed (recsplit.py:474-594) and query_hashed_many
+// (recsplit.py:251-275).
+#include <atomic>
+#include <cstdarg>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/shockhash_b200.h"
+#include "shk_common.cuh"
+#include "shk_kernels.h"
+
+// ---------------------------------------------------------------------------
+// errors / launch counting
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void shk_set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+void shk_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+#define RC(x)            \
+  do {                   \
+    int rc_ = (x);       \
+    if (rc_) return rc_; \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// context + caching device pool
+
+struct shk_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::multimap<size_t, void*> free_blocks;
+  std::unordered_map<void*, size_t> live;
+  int* d_counter = nullptr;  // scratch ints: [0] counter [1] flag [2] flag
+  ShkRibbon* rib = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+static size_t round_up(size_t b) {
+  if (b < 256) return 256;
+  if (b < (1u << 20)) return (b + 255) & ~(size_t)255;
+  return (b + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);
+}
+
+static int pool_alloc(shk_ctx* c, size_t bytes, void** out) {
+  size_t b = round_up(bytes);
+  auto it = c->free_blocks.lower_bound(b);
+  if (it != c->free_blocks.end() && it->first <= b * 2) {
+    *out = it->second;
+    c->live[it->second] = it->first;
+    c->free_blocks.erase(it);
+    return 0;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, b);
+  if (e != cudaSuccess) {
+    // release cached blocks and retry once
+    cudaGetLastError();
+    for (auto& kv : c->free_blocks) cudaFree(kv.second);
+    c->free_blocks.clear();
+    SHK_CUDA(cudaMalloc(&p, b));
+  }
+  c->live[p] = b;
+  *out = p;
+  return 0;
+}
+
+static void pool_free(shk_ctx* c, void* p) {
+  if (!p) return;
+  auto it = c->live.find(p);
+  if (it == c->live.end()) return;
+  c->free_blocks.emplace(it->second, p);
+  c->live.erase(it);
+}
+
+// RAII device buffer from the pool.
+struct DBuf {
+  shk_ctx* c = nullptr;
+  void* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(shk_ctx* ctx) : c(ctx) {}
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (c && p) pool_free(c, p);
+    p = nullptr;
+    n = 0;
+  }
+  int alloc(size_t bytes) {
+    release();
+    n = bytes;
+    return pool_alloc(c, bytes ? bytes : 1, &p);
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+static int h2d(shk_ctx* c, void* d, const void* h, size_t n) {
+  if (n) SHK_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, c->stream));
+  return 0;
+}
+static int d2h(shk_ctx* c, void* h, const void* d, size_t n) {
+  if (n) SHK_CUDA(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, c->stream));
+  return 0;
+}
+static int csync(shk_ctx* c) {
+  SHK_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+// Stage a possibly-host input array into device memory.
+static int stage_in(shk_ctx* c, int flags, const void* src, size_t bytes, DBuf& tmp, const void** dev) {
+  if (flags & SHK_DEVICE) {
+    *dev = src;
+    return 0;
+  }
+  RC(tmp.alloc(bytes));
+  RC(h2d(c, tmp.p, src, bytes));
+  *dev = tmp.p;
+  return 0;
+}
+// Output: device pointer to write to (either the caller's or a temp).
+static int stage_out(shk_ctx* c, int flags, void* dst, size_t bytes, DBuf& tmp, void** dev) {
+  if (!dst) {
+    *dev = nullptr;
+    return 0;
+  }
+  if (flags & SHK_DEVICE) {
+    *dev = dst;
+    return 0;
+  }
+  RC(tmp.alloc(bytes));
+  *dev = tmp.p;
+  return 0;
+}
+static int finish_out(shk_ctx* c, int flags, void* dst, const DBuf& tmp, size_t bytes) {
+  if (!dst || (flags & SHK_DEVICE)) return 0;
+  return d2h(c, dst, tmp.p, bytes);
+}
+
+extern "C" {
+
+const char* shk_last_error(void) { return g_err.c_str(); }
+int shk_version(void) { return 10000; }
+int64_t shk_launch_count(shk_ctx*) { return g_launches.load(); }
+
+int shk_device_count(int* n) {
+  int k = 0;
+  cudaError_t e = cudaGetDeviceCount(&k);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    k = 0;
+  }
+  *n = k;
+  return 0;
+}
+
+int shk_ctx_create(int device, shk_ctx** out) {
+  int n = 0;
+  shk_device_count(&n);
+  if (n <= 0) {
+    shk_set_error("no CUDA device available: the B200 path has no CPU fallback");
+    return -1;
+  }
+  SHK_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  SHK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    shk_set_error("device %d is sm_%d%d; this library is built for sm_100a (B200)", device, prop.major, prop.minor);
+    return -2;
+  }
+  shk_ctx* c = new shk_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  SHK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  c->stream = c->own;
+  SHK_CUDA(cudaMalloc(&c->d_counter, 256));
+  SHK_CUDA(cudaEventCreate(&c->t0));
+  SHK_CUDA(cudaEventCreate(&c->t1));
+  shk_ribbon_create(&c->rib);
+  *out = c;
+  return 0;
+}
+
+int shk_ctx_destroy(shk_ctx* c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->free_blocks) cudaFree(kv.second);
+  for (auto& kv : c->live) cudaFree(kv.first);
+  shk_ribbon_destroy(c->rib);
+  cudaFree(c->d_counter);
+  cudaEventDestroy(c->t0);
+  cudaEventDestroy(c->t1);
+  cudaStreamDestroy(c->own);
+  delete c;
+  return 0;
+}
+
+int shk_ctx_sync(shk_ctx* c) { return csync(c); }
+void* shk_ctx_stream(shk_ctx* c) { return (void*)c->stream; }
+int shk_ctx_set_stream(shk_ctx* c, void* s) {
+  c->stream = s ? (cudaStream_t)s : c->own;
+  return 0;
+}
+int shk_ctx_num_sms(shk_ctx* c) { return c->num_sms; }
+
+int shk_dev_alloc(shk_ctx* c, size_t bytes, void** out) { return pool_alloc(c, bytes, out); }
+int shk_dev_free(shk_ctx* c, void* p) {
+  pool_free(c, p);
+  return 0;
+}
+int shk_memcpy(shk_ctx* c, void* dst, const void* src, size_t bytes, int kind) {
+  cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  SHK_CUDA(cudaMemcpyAsync(dst, src, bytes, k, c->stream));
+  return csync(c);
+}
+int shk_timer_start(shk_ctx* c) {
+  SHK_CUDA(cudaEventRecord(c->t0, c->stream));
+  return 0;
+}
+int shk_timer_stop(shk_ctx* c, float* ms) {
+  SHK_CUDA(cudaEventRecord(c->t1, c->stream));
+  SHK_CUDA(cudaEventSynchronize(c->t1));
+  SHK_CUDA(cudaEventElapsedTime(ms, c->t0, c->t1));
+  return 0;
+}
+
+// ---- scalar API --------------------------------------------------------------
+uint64_t shk_mix64(uint64_t z) { return shk::mix64(z); }
+uint64_t shk_seed_mixer(uint64_t seed, uint64_t tag) { return shk::seed_mixer(seed, tag); }
+uint64_t shk_remix(uint64_t hi, uint64_t lo, uint64_t seed, uint64_t tag) { return shk::remix(hi, lo, seed, tag); }
+uint64_t shk_hash_range(uint64_t v, uint64_t m) { return shk::hash_range(v, m); }
+void shk_leaf_pair(uint64_t hi, uint64_t lo, uint64_t seed, int n, int* h0, int* h1) {
+  shk::leaf_pair(hi, lo, seed, n, *h0, *h1);
+}
+int shk_split_bit(uint64_t hi, uint64_t lo, uint64_t seed) { return shk::split_bit(hi, lo, seed); }
+int shk_leaf_cell(uint64_t hi, uint64_t lo, int64_t q, int mleaf, int mode, int64_t cache_k, int choice) {
+  return shk::leaf_cell(hi, lo, q, mleaf, mode, cache_k, choice);
+}
+
+// ---- leaf search -------------------------------------------------------------
+int shk_leaf_search(shk_ctx* c, int mode, int cache_k, int cache_min_leaf, const uint64_t* hi, const uint64_t* lo,
+                    const int64_t* leaf_off, int64_t L, uint64_t max_seed, int team_warps, int64_t* seed_out,
+                    uint64_t* fbits_out, int64_t* stats_out, int flags) {
+  if (L < 0 || (mode != 0 && mode != 1) || cache_k < 0) {
+    shk_set_error("invalid leaf search parameters");
+    return SHK_INVALID;
+  }
+  if (L == 0) return 0;
+  // Validate leaf sizes (host copy of the offsets).
+  std::vector<int64_t> hoff((size_t)L + 1);
+  if (flags & SHK_DEVICE) {
+    RC(d2h(c, hoff.data(), leaf_off, (L + 1) * 8));
+    RC(csync(c));
+  } else {
+    memcpy(hoff.data(), leaf_off, (L + 1) * 8);
+  }
+  int max_n = 0;
+  for (int64_t i = 0; i < L; ++i) {
+    int64_t n = hoff[i + 1] - hoff[i];
+    if (n < 1 || n > 64) {
+      shk_set_error("leaf %lld has %lld keys; leaves hold 1..64 keys", (long long)i, (long long)n);
+      return SHK_INVALID;
+    }
+    if (n > max_n) max_n = (int)n;
+  }
+  const int64_t N = hoff[L] - hoff[0];
+  DBuf thi(c), tlo(c), toff(c), tseed(c), tfb(c), tst(c);
+  const void *dhi, *dlo, *doff;
+  void *dseed, *dfb, *dst;
+  RC(stage_in(c, flags, hi, (size_t)(hoff[L]) * 8, thi, &dhi));
+  RC(stage_in(c, flags, lo, (size_t)(hoff[L]) * 8, tlo, &dlo));
+  RC(stage_in(c, flags, leaf_off, (size_t)(L + 1) * 8, toff, &doff));
+  RC(stage_out(c, flags, seed_out, (size_t)L * 8, tseed, &dseed));
+  RC(stage_out(c, flags, fbits_out, (size_t)L * 8, tfb, &dfb));
+  RC(stage_out(c, flags, stats_out, (size_t)L * 32, tst, &dst));
+  (void)N;
+  ShkLeafLaunch p{};
+  p.hi = (const uint64_t*)dhi;
+  p.lo = (const uint64_t*)dlo;
+  p.off = (const int64_t*)doff;
+  p.L = L;
+  p.max_n = max_n;
+  p.max_seed = max_seed;
+  p.mode = mode;
+  p.cache_k = cache_k;
+  p.cache_min_leaf = cache_min_leaf;
+  p.seed_out = (int64_t*)dseed;
+  p.fbits_out = (uint64_t*)dfb;
+  p.choice_out = nullptr;
+  p.stats_out = (int64_t*)dst;
+  p.counter = c->d_counter;
+  p.error = c->d_counter + 1;
+  p.team_warps = team_warps;
+  p.num_sms = c->num_sms;
+  p.stride = 1;
+  RC(shk_launch_leaf_search(p, c->stream));
+  RC(finish_out(c, flags, seed_out, tseed, (size_t)L * 8));
+  RC(finish_out(c, flags, fbits_out, tfb, (size_t)L * 8));
+  RC(finish_out(c, flags, stats_out, tst, (size_t)L * 32));
+  if (!(flags & SHK_DEVICE)) RC(csync(c));
+  return 0;
+}
+
+int shk_orient(shk_ctx* c, const uint8_t* eu, const uint8_t* ev, const int64_t* leaf_off, int64_t L,
+               uint64_t* fbits_out, int32_t* ok_out, int flags) {
+  if (L <= 0) return 0;
+  std::vector<int64_t> hoff((size_t)L + 1);
+  if (flags & SHK_DEVICE) {
+    RC(d2h(c, hoff.data(), leaf_off, (L + 1) * 8));
+    RC(csync(c));
+  } else {
+    memcpy(hoff.data(), leaf_off, (L + 1) * 8);
+  }
+  for (int64_t i = 0; i < L; ++i) {
+    int64_t n = hoff[i + 1] - hoff[i];
+    if (n < 1 || n > 64) {
+      shk_set_error("edge list %lld has %lld edges; 1..64 supported", (long long)i, (long long)n);
+      return SHK_INVALID;
+    }
+  }
+  DBuf tu(c), tv(c), to(c), tf(c), tk(c);
+  const void *du, *dv, *doff;
+  void *df, *dk;
+  RC(stage_in(c, flags, eu, (size_t)hoff[L], tu, &du));
+  RC(stage_in(c, flags, ev, (size_t)hoff[L], tv, &dv));
+  RC(stage_in(c, flags, leaf_off, (size_t)(L + 1) * 8, to, &doff));
+  RC(stage_out(c, flags, fbits_out, (size_t)L * 8, tf, &df));
+  RC(stage_out(c, flags, ok_out, (size_t)L * 4, tk, &dk));
+  RC(shk_launch_orient((const uint8_t*)du, (const uint8_t*)dv, (const int64_t*)doff, L, (uint64_t*)df, (int*)dk,
+                       c->stream));
+  RC(finish_out(c, flags, fbits_out, tf, (size_t)L * 8));
+  RC(finish_out(c, flags, ok_out, tk, (size_t)L * 4));
+  if (!(flags & SHK_DEVICE)) RC(csync(c));
+  return 0;
+}
+
+// ---- split search (single node, seam parity) -----------------------------------
+int shk_split_search(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t m, const int64_t* sizes, int fanout,
+                     uint64_t max_seed, int64_t* seed_out, int64_t* evals_out) {
+  if (fanout < 1 || fanout > 4 || m < 1 || m >= 32768) {
+    shk_set_error("split search supports fanout 1..4 and 1 <= m < 32768 (got fanout %d, m %lld)", fanout,
+                  (long long)m);
+    return SHK_INVALID;
+  }
+  int64_t tot = 0;
+  for (int j = 0; j < fanout; ++j) {
+    if (sizes[j] < 0) {
+      shk_set_error("negative part size");
+      return SHK_INVALID;
+    }
+    tot += sizes[j];
+  }
+  if (tot != m) {
+    shk_set_error("part sizes must sum to m");
+    return SHK_INVALID;
+  }
+  DBuf keys(c), tmp(c), task(c), seeds(c), ev(c);
+  RC(keys.alloc((size_t)m * 16));
+  RC(tmp.alloc((size_t)m * 16));
+  {
+    DBuf th(c), tl(c);
+    RC(th.alloc((size_t)m * 8));
+    RC(tl.alloc((size_t)m * 8));
+    RC(h2d(c, th.p, hi, (size_t)m * 8));
+    RC(h2d(c, tl.p, lo, (size_t)m * 8));
+    RC(shk_launch_interleave(th.as<uint64_t>(), tl.as<uint64_t>(), m, keys.as<uint64_t>(), c->stream));
+    RC(csync(c));
+  }
+  ShkSplitTask t{};
+  t.start = 0;
+  t.m = (int32_t)m;
+  t.fanout = fanout;
+  for (int j = 0; j < 4; ++j) t.sizes[j] = j < fanout ? (int32_t)sizes[j] : 0;
+  t.seed_slot = 0;
+  RC(task.alloc(sizeof t));
+  RC(h2d(c, task.p, &t, sizeof t));
+  RC(seeds.alloc(8));
+  RC(ev.alloc(8));
+  ShkSplitLaunch p{};
+  p.hi = keys.as<uint64_t>();
+  p.tmp_hi = tmp.as<uint64_t>();
+  p.tasks = task.as<ShkSplitTask>();
+  p.ntasks = 1;
+  p.max_seed = max_seed;
+  p.seeds = seeds.as<int64_t>();
+  p.evals_out = ev.as<int64_t>();
+  p.counter = c->d_counter;
+  p.num_sms = c->num_sms;
+  p.partition = 0;
+  RC(shk_launch_split(p, c->stream));
+  RC(d2h(c, seed_out, seeds.p, 8));
+  RC(d2h(c, evals_out, ev.p, 8));
+  return csync(c);
+}
+
+int shk_split_parts(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t m, uint64_t seed, const int64_t* sizes,
+                    int fanout, int64_t* parts_out) {
+  if (m <= 0) return 0;
+  if (fanout < 1) {
+    shk_set_error("fanout must be >= 1");
+    return SHK_INVALID;
+  }
+  DBuf th(c), tl(c), ts(c), tp(c);
+  RC(th.alloc((size_t)m * 8));
+  RC(tl.alloc((size_t)m * 8));
+  RC(ts.alloc((size_t)fanout * 8));
+  RC(tp.alloc((size_t)m * 8));
+  RC(h2d(c, th.p, hi, (size_t)m * 8));
+  RC(h2d(c, tl.p, lo, (size_t)m * 8));
+  RC(h2d(c, ts.p, sizes, (size_t)fanout * 8));
+  RC(shk_launch_split_parts(th.as<uint64_t>(), tl.as<uint64_t>(), m, seed, ts.as<int64_t>(), fanout,
+                            tp.as<int64_t>(), c->stream));
+  RC(d2h(c, parts_out, tp.p, (size_t)m * 8));
+  return csync(c);
+}
+
+// ---- ribbon ----------------------------------------------------------------------
+int shk_ribbon_rows(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t m, uint64_t seed,
+                    int64_t* starts, uint64_t* pat0, uint64_t* pat1, int flags) {
+  if (m < 128) {
+    shk_set_error("ribbon needs m >= 128");
+    return SHK_INVALID;
+  }
+  if (N <= 0) return 0;
+  DBuf th(c), tl(c), ts(c), t0(c), t1(c);
+  const void *dh, *dl;
+  void *ds, *d0, *d1;
+  RC(stage_in(c, flags, hi, (size_t)N * 8, th, &dh));
+  RC(stage_in(c, flags, lo, (size_t)N * 8, tl, &dl));
+  RC(stage_out(c, flags, starts, (size_t)N * 8, ts, &ds));
+  RC(stage_out(c, flags, pat0, (size_t)N * 8, t0, &d0));
+  RC(stage_out(c, flags, pat1, (size_t)N * 8, t1, &d1));
+  RC(shk_launch_ribbon_rows((const uint64_t*)dh, (const uint64_t*)dl, 1, N, m, seed, (int64_t*)ds, (uint64_t*)d0,
+                            (uint64_t*)d1, c->stream));
+  RC(finish_out(c, flags, starts, ts, (size_t)N * 8));
+  RC(finish_out(c, flags, pat0, t0, (size_t)N * 8));
+  RC(finish_out(c, flags, pat1, t1, (size_t)N * 8));
+  if (!(flags & SHK_DEVICE)) RC(csync(c));
+  return 0;
+}
+
+int shk_ribbon_solve(shk_ctx* c, const int64_t* starts, const uint64_t* pat0, const uint64_t* pat1,
+                     const uint8_t* rhs, int64_t N, int64_t m, uint64_t* words_out, int* consistent, int flags) {
+  if (m < 128) {
+    shk_set_error("ribbon needs m >= 128");
+    return SHK_INVALID;
+  }
+  const int64_t nw = (m + 63) / 64;
+  DBuf ts(c), t0(c), t1(c), tr(c), tw(c);
+  const void *ds, *d0, *d1, *dr;
+  void* dw;
+  RC(stage_in(c, flags, starts, (size_t)N * 8, ts, &ds));
+  RC(stage_in(c, flags, pat0, (size_t)N * 8, t0, &d0));
+  RC(stage_in(c, flags, pat1, (size_t)N * 8, t1, &d1));
+  RC(stage_in(c, flags, rhs, (size_t)N, tr, &dr));
+  RC(stage_out(c, flags, words_out, (size_t)nw * 8, tw, &dw));
+  // validate starts on the host side when given host arrays
+  if (!(flags & SHK_DEVICE)) {
+    for (int64_t i = 0; i < N; ++i)
+      if (starts[i] < 0 || starts[i] > m - 128) {
+        shk_set_error("row %lld start %lld outside [0, m-128]", (long long)i, (long long)starts[i]);
+        return SHK_INVALID;
+      }
+  }
+  RC(shk_ribbon_solve_rows(c->rib, (const int64_t*)ds, (const uint64_t*)d0, (const uint64_t*)d1, (const uint8_t*)dr,
+                           N, m, (uint64_t*)dw, consistent, c->stream));
+  if (*consistent) RC(finish_out(c, flags, words_out, tw, (size_t)nw * 8));
+  return csync(c);
+}
+
+int shk_ribbon_query(shk_ctx* c, const int64_t* starts, const uint64_t* pat0, const uint64_t* pat1, int64_t N,
+                     const uint64_t* words, int64_t nwords, uint8_t* out, int flags) {
+  if (N <= 0) return 0;
+  DBuf ts(c), t0(c), t1(c), tw(c), to(c);
+  const void *ds, *d0, *d1, *dw;
+  void* dout;
+  RC(stage_in(c, flags, starts, (size_t)N * 8, ts, &ds));
+  RC(stage_in(c, flags, pat0, (size_t)N * 8, t0, &d0));
+  RC(stage_in(c, flags, pat1, (size_t)N * 8, t1, &d1));
+  RC(stage_in(c, flags, words, (size_t)(nwords > 0 ? nwords : 1) * 8, tw, &dw));
+  RC(stage_out(c, flags, out, (size_t)N, to, &dout));
+  RC(shk_launch_ribbon_query((const int64_t*)ds, (const uint64_t*)d0, (const uint64_t*)d1, N, (const uint64_t*)dw,
+                             nwords, (uint8_t*)dout, c->stream));
+  RC(finish_out(c, flags, out, to, (size_t)N));
+  if (!(flags & SHK_DEVICE)) RC(csync(c));
+  return 0;
+}
+
+static int ribbon_seed_loop(shk_ctx* c, const uint64_t* dkeys, const uint8_t* drhs, int64_t N, int64_t m,
+                            int max_tries, uint64_t* seed_out, uint64_t* dwords) {
+  for (int seed = 0; seed < max_tries; ++seed) {
+    int ok = 0;
+    RC(shk_ribbon_solve_keys(c->rib, dkeys, drhs, N, m, (uint64_t)seed, dwords, &ok, c->stream));
+    if (ok) {
+      *seed_out = (uint64_t)seed;
+      return 0;
+    }
+  }
+  shk_set_error("retrieval system unsolvable after %d seeds (n=%lld, m=%lld)", max_tries, (long long)N,
+                (long long)m);
+  return SHK_UNSOLVABLE;
+}
+
+int shk_ribbon_build(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, const uint8_t* rhs, int64_t N, int64_t m,
+                     int max_tries, uint64_t* seed_out, uint64_t* words_out, int flags) {
+  if (m < 128) {
+    shk_set_error("ribbon needs m >= 128");
+    return SHK_INVALID;
+  }
+  const int64_t nw = (m + 63) / 64;
+  DBuf th(c), tl(c), tr(c), keys(c), tw(c);
+  const void *dh, *dl, *dr;
+  void* dw;
+  RC(stage_in(c, flags, hi, (size_t)N * 8, th, &dh));
+  RC(stage_in(c, flags, lo, (size_t)N * 8, tl, &dl));
+  RC(stage_in(c, flags, rhs, (size_t)N, tr, &dr));
+  RC(stage_out(c, flags, words_out, (size_t)nw * 8, tw, &dw));
+  RC(keys.alloc((size_t)N * 16 + 16));
+  RC(shk_launch_interleave((const uint64_t*)dh, (const uint64_t*)dl, N, keys.as<uint64_t>(), c->stream));
+  RC(ribbon_seed_loop(c, keys.as<uint64_t>(), (const uint8_t*)dr, N, m, max_tries, seed_out, (uint64_t*)dw));
+  RC(finish_out(c, flags, words_out, tw, (size_t)nw * 8));
+  return csync(c);
+}
+
+int shk_rice_decode(shk_ctx* c, const uint64_t* words, int64_t nwords, int64_t bit_len, int64_t pos,
+                    const int32_t* g, int64_t count, int64_t* values_out, int64_t* pos_out) {
+  if (count <= 0) return 0;
+  if (nwords * 64 < bit_len) {
+    shk_set_error("bit_len exceeds the word array");
+    return SHK_INVALID;
+  }
+  DBuf tw(c), tg(c), tv(c), tp(c);
+  RC(tw.alloc((size_t)(nwords + 1) * 8));
+  RC(tg.alloc((size_t)count * 4));
+  RC(tv.alloc((size_t)count * 8));
+  RC(tp.alloc((size_t)count * 8));
+  RC(h2d(c, tw.p, words, (size_t)nwords * 8));
+  RC(h2d(c, tg.p, g, (size_t)count * 4));
+  int* err = c->d_counter + 2;
+  SHK_CUDA(cudaMemsetAsync(err, 0, 4, c->stream));
+  RC(shk_launch_rice_decode(tw.as<uint64_t>(), bit_len, pos, tg.as<int32_t>(), count, tv.as<int64_t>(),
+                            tp.as<int64_t>(), err, c->stream));
+  int herr = 0;
+  RC(d2h(c, &herr, err, 4));
+  RC(d2h(c, values_out, tv.p, (size_t)count * 8));
+  RC(d2h(c, pos_out, tp.p, (size_t)count * 8));
+  RC(csync(c));
+  if (herr) {
+    shk_set_error("bit stream overrun");
+    return SHK_FORMAT;
+  }
+  return 0;
+}
+
+int shk_blake2b128(shk_ctx* c, const uint8_t* blob, int64_t blob_len, const int64_t* off, int64_t N, uint64_t salt,
+                   uint64_t* hi, uint64_t* lo, int flags) {
+  if (N <= 0) return 0;
+  DBuf tb(c), to(c), th(c), tl(c);
+  const void *db, *doff;
+  void *dh, *dl;
+  RC(stage_in(c, flags, blob, (size_t)(blob_len > 0 ? blob_len : 1), tb, &db));
+  RC(stage_in(c, flags, off, (size_t)(N + 1) * 8, to, &doff));
+  RC(stage_out(c, flags, hi, (size_t)N * 8, th, &dh));
+  RC(stage_out(c, flags, lo, (size_t)N * 8, tl, &dl));
+  // Fixed-length fast path when every key has the same length (host offsets).
+  int fixed = 0;
+  if (!(flags & SHK_DEVICE) && off[0] == 0 && blob_len == off[N] && N > 0) {
+    int64_t L0 = off[1] - off[0];
+    if (L0 >= 1 && L0 <= 128 && L0 * N == blob_len) {
+      fixed = 1;
+      for (int64_t i = 0; i < N && fixed; ++i)
+        if (off[i + 1] - off[i] != L0) fixed = 0;
+      if (fixed)
+        RC(shk_launch_blake2b_fixed((const uint8_t*)db, (int)L0, N, salt, (uint64_t*)dh, (uint64_t*)dl, c->stream));
+    }
+  }
+  if (!fixed)
+    RC(shk_launch_blake2b((const uint8_t*)db, (const int64_t*)doff, N, salt, (uint64_t*)dh, (uint64_t*)dl,
+                          c->stream));
+  RC(finish_out(c, flags, hi, th, (size_t)N * 8));
+  RC(finish_out(c, flags, lo, tl, (size_t)N * 8));
+  if (!(flags & SHK_DEVICE)) RC(csync(c));
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Plans: host tables derived from the reference's flattened plan arrays.
+
+struct PlanNode {
+  int32_t kind, g, m, fanout;
+  int32_t sizes[4];
+  int32_t child[4];
+  int32_t off;    // key offset inside the bucket
+  int32_t depth;
+};
+struct PlanSet {
+  std::vector<int64_t> plan_m;
+  std::vector<int64_t> plan_off;  // nplans+1
+  std::vector<PlanNode> nodes;
+  std::unordered_map<int64_t, int32_t> by_size;
+  int max_depth = 0;
+};
+
+static int load_plans(const shk_plans* P, PlanSet& S) {
+  if (!P || P->nplans < 0) {
+    shk_set_error("missing plan tables");
+    return SHK_INVALID;
+  }
+  S.plan_m.assign(P->plan_m, P->plan_m + P->nplans);
+  S.plan_off.assign(P->plan_off, P->plan_off + P->nplans + 1);
+  const int64_t total = S.plan_off.empty() ? 0 : S.plan_off.back();
+  S.nodes.resize((size_t)total);
+  for (int64_t p = 0; p < P->nplans; ++p) {
+    const int64_t a = S.plan_off[p], b = S.plan_off[p + 1];
+    if (b <= a) {
+      shk_set_error("empty plan %lld", (long long)p);
+      return SHK_INVALID;
+    }
+    S.by_size[S.plan_m[p]] = (int32_t)p;
+    for (int64_t j = a; j < b; ++j) {
+      PlanNode& nd = S.nodes[j];
+      nd.kind = (int32_t)P->kind[j];
+      nd.g = (int32_t)P->g[j];
+      nd.m = (int32_t)P->m_node[j];
+      nd.fanout = nd.kind == 0 ? (int32_t)P->fanout[j] : 0;
+      if (nd.g < 0 || nd.g > 63) {
+        shk_set_error("Rice parameter out of range");
+        return SHK_INVALID;
+      }
+      if (nd.kind == 0 && (nd.fanout < 1 || nd.fanout > 4)) {
+        shk_set_error("split fanout %d unsupported (1..4)", nd.fanout);
+        return SHK_INVALID;
+      }
+      for (int k = 0; k < 4; ++k) {
+        nd.sizes[k] = (k < nd.fanout) ? (int32_t)P->sizes_flat[P->sizes_base[p] + P->sizes_off[j] + k] : 0;
+        nd.child[k] = 0;
+      }
+    }
+    // children (preorder: first child follows, next child after its subtree)
+    for (int64_t j = a; j < b; ++j) {
+      PlanNode& nd = S.nodes[j];
+      if (nd.kind != 0) continue;
+      int64_t cidx = j + 1;
+      for (int k = 0; k < nd.fanout; ++k) {
+        if (cidx >= b) {
+          shk_set_error("malformed plan subtree counts");
+          return SHK_INVALID;
+        }
+        nd.child[k] = (int32_t)(cidx - a);
+        cidx += P->subtree[cidx];
+      }
+    }
+    // offsets and depths (walk in preorder)
+    S.nodes[a].off = 0;
+    S.nodes[a].depth = 0;
+    for (int64_t j = a; j < b; ++j) {
+      PlanNode& nd = S.nodes[j];
+      if (nd.kind != 0) continue;
+      int32_t o = nd.off;
+      for (int k = 0; k < nd.fanout; ++k) {
+        PlanNode& ch = S.nodes[a + nd.child[k]];
+        ch.off = o;
+        ch.depth = nd.depth + 1;
+        if (ch.depth > S.max_depth) S.max_depth = ch.depth;
+        o += nd.sizes[k];
+      }
+    }
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Build object.
+
+struct shk_build {
+  shk_ctx* c = nullptr;
+  int64_t N = 0, nb = 0, max_bucket = 0;
+  DBuf keys, tmp, prefix, choice;
+  std::vector<uint64_t> h_prefix;
+  // results of run()
+  int64_t b0 = 0, b1 = 0;
+  int64_t nnodes = 0;
+  DBuf words;
+  int64_t bit_len = 0, nwords = 0;
+  std::vector<uint64_t> bit_off;  // [b1-b0+1] relative to the range start
+  bool ran = false;
+  bool record = false;
+  DBuf place;
+  explicit shk_build(shk_ctx* ctx)
+      : c(ctx), keys(ctx), tmp(ctx), prefix(ctx), choice(ctx), words(ctx), place(ctx) {}
+};
+
+__global__ void gather_bitoff_kernel(const int64_t* pos, const int64_t* node_base, int64_t nb, uint64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nb; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint64_t)pos[node_base[i]];
+}
+
+__global__ void seed_bits_kernel(const int64_t* len, const uint8_t* kind, int64_t nn, unsigned long long* acc) {
+  unsigned long long a = 0, b = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+    if (kind[i])
+      a += (unsigned long long)len[i];
+    else
+      b += (unsigned long long)len[i];
+  }
+  a = shk::warp_sum(a);
+  b = shk::warp_sum(b);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&acc[0], a);
+    atomicAdd(&acc[1], b);
+  }
+}
+
+extern "C" {
+
+int shk_build_create(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nbuckets, int flags,
+                     shk_build** out, int* dup, int64_t* max_bucket) {
+  if (N < 1 || nbuckets < 1) {
+    shk_set_error("build needs N >= 1 and nbuckets >= 1");
+    return SHK_INVALID;
+  }
+  shk_build* b = new shk_build(c);
+  b->N = N;
+  b->nb = nbuckets;
+  DBuf th(c), tl(c), scratch(c);
+  const void *dh, *dl;
+  int rc = 0;
+  do {
+    if ((rc = stage_in(c, flags, hi, (size_t)N * 8, th, &dh))) break;
+    if ((rc = stage_in(c, flags, lo, (size_t)N * 8, tl, &dl))) break;
+    if ((rc = b->keys.alloc((size_t)N * 16))) break;
+    if ((rc = b->tmp.alloc((size_t)N * 16))) break;
+    if ((rc = b->prefix.alloc((size_t)(nbuckets + 1) * 8))) break;
+    if ((rc = b->choice.alloc((size_t)N))) break;
+    size_t ss = shk_bucketize_scratch(N, nbuckets);
+    if ((rc = scratch.alloc(ss))) break;
+    int* ddup = c->d_counter + 3;
+    if ((rc = shk_bucketize((const uint64_t*)dh, (const uint64_t*)dl, N, nbuckets, b->keys.as<uint64_t>(),
+                            b->prefix.as<uint64_t>(), ddup, scratch.p, ss, &b->max_bucket, c->stream)))
+      break;
+    b->h_prefix.resize((size_t)nbuckets + 1);
+    if ((rc = d2h(c, b->h_prefix.data(), b->prefix.p, (size_t)(nbuckets + 1) * 8))) break;
+    int hd = 0;
+    if ((rc = d2h(c, &hd, ddup, 4))) break;
+    if ((rc = csync(c))) break;
+    *dup = hd;
+    if (max_bucket) *max_bucket = b->max_bucket;
+  } while (0);
+  if (rc) {
+    delete b;
+    return rc;
+  }
+  *out = b;
+  return 0;
+}
+
+int shk_build_key_prefix(shk_build* b, uint64_t* out) {
+  memcpy(out, b->h_prefix.data(), (size_t)(b->nb + 1) * 8);
+  return 0;
+}
+
+int shk_build_sorted_keys(shk_build* b, uint64_t* hi, uint64_t* lo) {
+  shk_ctx* c = b->c;
+  DBuf th(c), tl(c);
+  RC(th.alloc((size_t)b->N * 8));
+  RC(tl.alloc((size_t)b->N * 8));
+  RC(shk_launch_deinterleave(b->keys.as<uint64_t>(), b->N, th.as<uint64_t>(), tl.as<uint64_t>(), c->stream));
+  RC(d2h(c, hi, th.p, (size_t)b->N * 8));
+  RC(d2h(c, lo, tl.p, (size_t)b->N * 8));
+  return csync(c);
+}
+
+int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, int cache_min_leaf, int64_t b0,
+                  int64_t b1, uint64_t max_seed, int64_t* stats_out) {
+  shk_ctx* c = b->c;
+  if (b0 < 0 || b1 > b->nb || b0 > b1 || (mode != 0 && mode != 1)) {
+    shk_set_error("invalid bucket range or mode");
+    return SHK_INVALID;
+  }
+  PlanSet S;
+  RC(load_plans(plans, S));
+  const int64_t nbr = b1 - b0;
+  // ---- per-bucket plan ids and global node numbering
+  std::vector<int64_t> node_base((size_t)nbr + 1);
+  std::vector<int32_t> bplan((size_t)nbr);
+  int64_t nn = 0;
+  for (int64_t i = 0; i < nbr; ++i) {
+    const int64_t bu = b0 + i;
+    const int64_t m = (int64_t)(b->h_prefix[bu + 1] - b->h_prefix[bu]);
+    node_base[i] = nn;
+    if (m == 0) {
+      bplan[i] = -1;
+      continue;
+    }
+    auto it = S.by_size.find(m);
+    if (it == S.by_size.end()) {
+      shk_set_error("no plan for bucket size %lld", (long long)m);
+      return SHK_INVALID;
+    }
+    bplan[i] = it->second;
+    nn += S.plan_off[it->second + 1] - S.plan_off[it->second];
+  }
+  node_base[nbr] = nn;
+  b->nnodes = nn;
+  // ---- node tables, split tasks per depth, leaf CSR
+  std::vector<int32_t> ng((size_t)nn);
+  std::vector<uint8_t> nkind((size_t)nn);
+  std::vector<std::vector<ShkSplitTask>> tasks((size_t)S.max_depth + 1);
+  std::vector<int64_t> leaf_off, leaf_slot;
+  leaf_off.reserve((size_t)(b->N / 8 + 16));
+  int max_leaf = 0;
+  for (int64_t i = 0; i < nbr; ++i) {
+    if (bplan[i] < 0) continue;
+    const int64_t bu = b0 + i;
+    const int64_t kstart = (int64_t)b->h_prefix[bu];
+    const int64_t pa = S.plan_off[bplan[i]], pb = S.plan_off[bplan[i] + 1];
+    for (int64_t j = pa; j < pb; ++j) {
+      const PlanNode& nd = S.nodes[j];
+      const int64_t slot = node_base[i] + (j - pa);
+      ng[slot] = nd.g;
+      nkind[slot] = (uint8_t)(nd.kind != 0);
+      if (nd.kind == 0) {
+        if (nd.m >= 32768) {
+          shk_set_error("split node of %d keys exceeds the 32767-key split kernel limit", nd.m);
+          return SHK_INVALID;
+        }
+        ShkSplitTask t{};
+        t.start = kstart + nd.off;
+        t.m = nd.m;
+        t.fanout = nd.fanout;
+        for (int k = 0; k < 4; ++k) t.sizes[k] = nd.sizes[k];
+        t.seed_slot = slot;
+        tasks[nd.depth].push_back(t);
+      } else {
+        if (nd.m < 1 || nd.m > 64) {
+          shk_set_error("leaf of %d keys outside 1..64", nd.m);
+          return SHK_INVALID;
+        }
+        leaf_off.push_back(kstart + nd.off);
+        leaf_slot.push_back(slot);
+        if (nd.m > max_leaf) max_leaf = nd.m;
+      }
+    }
+  }
+  const int64_t L = (int64_t)leaf_off.size();
+  // leaves are contiguous in key order: CSR end = range end
+  leaf_off.push_back((int64_t)b->h_prefix[b1]);
+  // ---- device tables
+  DBuf dseeds(c), dg(c), dkind(c), dtasks(c), dloff(c), dlslot(c), dlen(c), dpos(c), dnb(c), dbo(c), dacc(c),
+      dscan(c);
+  RC(dseeds.alloc((size_t)(nn + 1) * 8));
+  RC(dg.alloc((size_t)(nn + 1) * 4));
+  RC(dkind.alloc((size_t)(nn + 1)));
+  RC(h2d(c, dg.p, ng.data(), (size_t)nn * 4));
+  RC(h2d(c, dkind.p, nkind.data(), (size_t)nn));
+  size_t ntask_total = 0;
+  for (auto& v : tasks) ntask_total += v.size();
+  RC(dtasks.alloc((ntask_total + 1) * sizeof(ShkSplitTask)));
+  {
+    size_t o = 0;
+    for (auto& v : tasks) {
+      RC(h2d(c, dtasks.as<char>() + o * sizeof(ShkSplitTask), v.data(), v.size() * sizeof(ShkSplitTask)));
+      o += v.size();
+    }
+  }
+  RC(dloff.alloc((size_t)(L + 1) * 8));
+  RC(dlslot.alloc((size_t)(L + 1) * 8));
+  RC(h2d(c, dloff.p, leaf_off.data(), (size_t)(L + 1) * 8));
+  RC(h2d(c, dlslot.p, leaf_slot.data(), (size_t)L * 8));
+  RC(dacc.alloc(64));
+  SHK_CUDA(cudaMemsetAsync(dacc.p, 0, 64, c->stream));
+  int* exh = c->d_counter + 4;
+  SHK_CUDA(cudaMemsetAsync(exh, 0, 4, c->stream));
+  // ---- splits, level by level (every node of one depth in one launch)
+  {
+    size_t o = 0;
+    for (auto& v : tasks) {
+      if (!v.empty()) {
+        ShkSplitLaunch p{};
+        p.hi = b->keys.as<uint64_t>();
+        p.tmp_hi = b->tmp.as<uint64_t>();
+        p.tasks = dtasks.as<ShkSplitTask>() + o;
+        p.ntasks = (int64_t)v.size();
+        p.max_seed = max_seed;
+        p.seeds = dseeds.as<int64_t>();
+        p.evals_out = nullptr;
+        p.counter = c->d_counter;
+        p.num_sms = c->num_sms;
+        p.partition = 1;
+        p.exhausted = exh;
+        RC(shk_launch_split(p, c->stream));
+      }
+      o += v.size();
+    }
+  }
+  // ---- leaves
+  if (L > 0) {
+    ShkLeafLaunch p{};
+    p.hi = b->keys.as<uint64_t>();
+    p.lo = b->keys.as<uint64_t>() + 1;
+    p.stride = 2;
+    p.off = dloff.as<int64_t>();
+    p.L = L;
+    p.max_n = max_leaf;
+    p.max_seed = max_seed;
+    p.mode = mode;
+    p.cache_k = cache_k;
+    p.cache_min_leaf = cache_min_leaf;
+    p.seed_out = dseeds.as<int64_t>();
+    p.seed_slot = dlslot.as<int64_t>();
+    p.fbits_out = nullptr;
+    p.choice_out = b->choice.as<uint8_t>();
+    p.stats_out = nullptr;
+    p.stats_acc = dacc.as<unsigned long long>();
+    p.counter = c->d_counter;
+    p.error = c->d_counter + 1;
+    p.exhausted = exh;
+    p.num_sms = c->num_sms;
+    if (b->record) {
+      RC(b->place.alloc((size_t)b->N * 8));
+      p.place_out = b->place.as<int64_t>();
+    }
+    RC(shk_launch_leaf_search(p, c->stream));
+  }
+  int hex = 0;
+  RC(d2h(c, &hex, exh, 4));
+  RC(csync(c));
+  if (hex) {
+    shk_set_error("seed search exhausted (max_seed %llu)", (unsigned long long)max_seed);
+    return SHK_EXHAUSTED;
+  }
+  // ---- Rice stream: lengths -> scan -> scatter
+  RC(dlen.alloc((size_t)(nn + 1) * 8));
+  RC(dpos.alloc((size_t)(nn + 2) * 8));
+  RC(shk_rice_lengths(dseeds.as<int64_t>(), dg.as<int32_t>(), nn, dlen.as<int64_t>(), c->stream));
+  size_t ss = shk_scan_scratch(nn);
+  RC(dscan.alloc(ss));
+  RC(shk_exclusive_scan_i64(dlen.as<int64_t>(), dpos.as<int64_t>(), nn, dscan.p, ss, c->stream));
+  seed_bits_kernel<<<64, 256, 0, c->stream>>>(dlen.as<int64_t>(), dkind.as<uint8_t>(), nn,
+                                               dacc.as<unsigned long long>() + 4);
+  SHK_LAUNCHED();
+  int64_t total_bits = 0;
+  RC(d2h(c, &total_bits, dpos.as<int64_t>() + nn, 8));
+  RC(csync(c));
+  b->bit_len = total_bits;
+  b->nwords = (total_bits + 63) / 64;
+  RC(b->words.alloc((size_t)(b->nwords + 1) * 8));
+  SHK_CUDA(cudaMemsetAsync(b->words.p, 0, (size_t)(b->nwords + 1) * 8, c->stream));
+  RC(shk_rice_scatter(dseeds.as<int64_t>(), dg.as<int32_t>(), dpos.as<int64_t>(), nn, b->words.as<uint64_t>(),
+                      c->stream));
+  // per-bucket bit offsets: pos[node_base[i]]
+  RC(dnb.alloc((size_t)(nbr + 1) * 8));
+  RC(dbo.alloc((size_t)(nbr + 1) * 8));
+  RC(h2d(c, dnb.p, node_base.data(), (size_t)(nbr + 1) * 8));
+  gather_bitoff_kernel<<<(unsigned)((nbr + 256) / 256), 256, 0, c->stream>>>(dpos.as<int64_t>(), dnb.as<int64_t>(),
+                                                                              nbr, dbo.as<uint64_t>());
+  SHK_LAUNCHED();
+  b->bit_off.resize((size_t)nbr + 1);
+  RC(d2h(c, b->bit_off.data(), dbo.p, (size_t)(nbr + 1) * 8));
+  unsigned long long acc[8];
+  RC(d2h(c, acc, dacc.p, 64));
+  RC(csync(c));
+  if (stats_out) {
+    stats_out[0] = (int64_t)acc[0];
+    stats_out[1] = (int64_t)acc[1];
+    stats_out[2] = (int64_t)acc[2];
+    stats_out[3] = (int64_t)acc[3];
+    stats_out[4] = (int64_t)acc[4];  // leaf seed bits
+    stats_out[5] = (int64_t)acc[5];  // split seed bits
+    stats_out[6] = L;
+  }
+  b->b0 = b0;
+  b->b1 = b1;
+  b->ran = true;
+  return 0;
+}
+
+int shk_build_stream_size(shk_build* b, int64_t* bit_len, int64_t* nwords) {
+  if (!b->ran) {
+    shk_set_error("shk_build_run first");
+    return SHK_INVALID;
+  }
+  *bit_len = b->bit_len;
+  *nwords = b->nwords;
+  return 0;
+}
+
+int shk_build_stream(shk_build* b, uint64_t* words, uint64_t* bit_offsets) {
+  if (!b->ran) {
+    shk_set_error("shk_build_run first");
+    return SHK_INVALID;
+  }
+  if (words) RC(d2h(b->c, words, b->words.p, (size_t)b->nwords * 8));
+  if (bit_offsets) memcpy(bit_offsets, b->bit_off.data(), b->bit_off.size() * 8);
+  return csync(b->c);
+}
+
+int shk_build_set_record_placements(shk_build* b, int on) {
+  b->record = on != 0;
+  return 0;
+}
+
+int shk_build_placements(shk_build* b, int64_t* out) {
+  if (!b->ran || !b->record) {
+    shk_set_error("placements were not recorded");
+    return SHK_INVALID;
+  }
+  RC(d2h(b->c, out, b->place.p, (size_t)b->N * 8));
+  return csync(b->c);
+}
+
+int shk_build_choice(shk_build* b, uint8_t* choice) {
+  RC(d2h(b->c, choice, b->choice.p, (size_t)b->N));
+  return csync(b->c);
+}
+
+int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int64_t m, int max_tries,
+                     uint64_t* seed_out, uint64_t* words_out) {
+  shk_ctx* c = b->c;
+  if (m < 128) {
+    shk_set_error("ribbon needs m >= 128");
+    return SHK_INVALID;
+  }
+  const uint8_t* drhs = b->choice.as<uint8_t>();
+  DBuf tr(c);
+  if (choice) {
+    const void* d;
+    RC(stage_in(c, choice_flags, choice, (size_t)b->N, tr, &d));
+    drhs = (const uint8_t*)d;
+  }
+  const int64_t nw = (m + 63) / 64;
+  DBuf tw(c);
+  RC(tw.alloc((size_t)nw * 8));
+  RC(ribbon_seed_loop(c, b->keys.as<uint64_t>(), drhs, b->N, m, max_tries, seed_out, tw.as<uint64_t>()));
+  RC(d2h(c, words_out, tw.p, (size_t)nw * 8));
+  return csync(c);
+}
+
+int shk_build_destroy(shk_build* b) {
+  delete b;
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Query descriptor.
+
+struct shk_qdesc {
+  shk_ctx* c;
+  ShkQueryDesc d{};
+  DBuf kp, bo, sw, rw, bplan, nbase, npos, bbad, kind, g, mm, child, sizes, fan, poff;
+  int64_t nnodes = 0;
+  explicit shk_qdesc(shk_ctx* ctx)
+      : c(ctx), kp(ctx), bo(ctx), sw(ctx), rw(ctx), bplan(ctx), nbase(ctx), npos(ctx), bbad(ctx), kind(ctx), g(ctx),
+        mm(ctx), child(ctx), sizes(ctx), fan(ctx), poff(ctx) {}
+};
+
+extern "C" {
+
+int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int64_t cache_k,
+                     const uint64_t* key_prefix, const uint64_t* bit_offsets, const uint64_t* stream_words,
+                     int64_t stream_nwords, int64_t stream_bit_len, const shk_plans* plans, uint64_t rib_seed,
+                     int64_t rib_m, const uint64_t* rib_words, int64_t rib_nwords, shk_qdesc** out) {
+  if (nbuckets < 1 || nbuckets > 0xFFFFFFFFll) {
+    shk_set_error("invalid bucket count");
+    return SHK_INVALID;
+  }
+  if (stream_nwords * 64 < stream_bit_len) {
+    shk_set_error("stream bit length exceeds the word array");
+    return SHK_INVALID;
+  }
+  PlanSet S;
+  RC(load_plans(plans, S));
+  shk_qdesc* q = new shk_qdesc(c);
+  std::unique_ptr<shk_qdesc> guard(q);
+  std::vector<int32_t> bplan((size_t)nbuckets);
+  std::vector<int64_t> nbase((size_t)nbuckets + 1);
+  int64_t nn = 0;
+  for (int64_t bu = 0; bu < nbuckets; ++bu) {
+    const int64_t m = (int64_t)(key_prefix[bu + 1] - key_prefix[bu]);
+    nbase[bu] = nn;
+    if (m <= 0) {
+      bplan[bu] = -1;
+      continue;
+    }
+    auto it = S.by_size.find(m);
+    if (it == S.by_size.end()) {
+      shk_set_error("no plan for bucket size %lld", (long long)m);
+      return SHK_INVALID;
+    }
+    bplan[bu] = it->second;
+    nn += S.plan_off[it->second + 1] - S.plan_off[it->second];
+  }
+  nbase[nbuckets] = nn;
+  q->nnodes = nn;
+  const size_t np = S.nodes.size();
+  std::vector<int32_t> kind(np), g(np), mm(np), child(np * 4), sizes(np * 4), fan(np);
+  for (size_t j = 0; j < np; ++j) {
+    kind[j] = S.nodes[j].kind;
+    g[j] = S.nodes[j].g;
+    mm[j] = S.nodes[j].m;
+    fan[j] = S.nodes[j].fanout;
+    for (int k = 0; k < 4; ++k) {
+      child[4 * j + k] = S.nodes[j].child[k];
+      sizes[4 * j + k] = S.nodes[j].sizes[k];
+    }
+  }
+  const int64_t rnw = rib_nwords > 0 ? rib_nwords : 0;
+  RC(q->kp.alloc((size_t)(nbuckets + 1) * 8));
+  RC(q->bo.alloc((size_t)(nbuckets + 1) * 8));
+  RC(q->sw.alloc((size_t)(stream_nwords + 1) * 8));
+  RC(q->rw.alloc((size_t)(rnw + 1) * 8));
+  RC(q->bplan.alloc((size_t)nbuckets * 4));
+  RC(q->nbase.alloc((size_t)(nbuckets + 1) * 8));
+  RC(q->npos.alloc((size_t)(nn + 1) * 8));
+  RC(q->bbad.alloc((size_t)nbuckets * 4));
+  RC(q->kind.alloc(np * 4 + 4));
+  RC(q->g.alloc(np * 4 + 4));
+  RC(q->mm.alloc(np * 4 + 4));
+  RC(q->child.alloc(np * 16 + 16));
+  RC(q->sizes.alloc(np * 16 + 16));
+  RC(q->fan.alloc(np * 4 + 4));
+  RC(q->poff.alloc(S.plan_off.size() * 8 + 8));
+  RC(h2d(c, q->kp.p, key_prefix, (size_t)(nbuckets + 1) * 8));
+  RC(h2d(c, q->bo.p, bit_offsets, (size_t)(nbuckets + 1) * 8));
+  SHK_CUDA(cudaMemsetAsync(q->sw.p, 0, (size_t)(stream_nwords + 1) * 8, c->stream));
+  RC(h2d(c, q->sw.p, stream_words, (size_t)stream_nwords * 8));
+  SHK_CUDA(cudaMemsetAsync(q->rw.p, 0, (size_t)(rnw + 1) * 8, c->stream));
+  if (rnw) RC(h2d(c, q->rw.p, rib_words, (size_t)rnw * 8));
+  RC(h2d(c, q->bplan.p, bplan.data(), (size_t)nbuckets * 4));
+  RC(h2d(c, q->nbase.p, nbase.data(), (size_t)(nbuckets + 1) * 8));
+  RC(h2d(c, q->kind.p, kind.data(), np * 4));
+  RC(h2d(c, q->g.p, g.data(), np * 4));
+  RC(h2d(c, q->mm.p, mm.data(), np * 4));
+  RC(h2d(c, q->child.p, child.data(), np * 16));
+  RC(h2d(c, q->sizes.p, sizes.data(), np * 16));
+  RC(h2d(c, q->fan.p, fan.data(), np * 4));
+  RC(h2d(c, q->poff.p, S.plan_off.data(), S.plan_off.size() * 8));
+  ShkQueryDesc& d = q->d;
+  d.nbuckets = nbuckets;
+  d.n_keys = n_keys;
+  d.mode = mode;
+  d.cache_k = cache_k;
+  d.key_prefix = q->kp.as<uint64_t>();
+  d.bucket_plan = q->bplan.as<int32_t>();
+  d.node_base = q->nbase.as<int64_t>();
+  d.node_pos = q->npos.as<int64_t>();
+  d.bucket_bad = q->bbad.as<int32_t>();
+  d.bit_offsets = q->bo.as<uint64_t>();
+  d.stream = q->sw.as<uint64_t>();
+  d.stream_bit_len = stream_bit_len;
+  d.stream_nwords = stream_nwords;
+  d.pn_kind = q->kind.as<int32_t>();
+  d.pn_g = q->g.as<int32_t>();
+  d.pn_m = q->mm.as<int32_t>();
+  d.pn_child = q->child.as<int32_t>();
+  d.pn_sizes = q->sizes.as<int32_t>();
+  d.pn_fanout = q->fan.as<int32_t>();
+  d.plan_off = q->poff.as<int64_t>();
+  d.rib_seed = rib_seed;
+  d.rib_m = rib_m;
+  d.rib_words = q->rw.as<uint64_t>();
+  d.rib_nwords = rnw;
+  RC(shk_launch_node_index(d, q->npos.as<int64_t>(), q->bbad.as<int32_t>(), c->stream));
+  RC(csync(c));
+  *out = guard.release();
+  return 0;
+}
+
+int shk_query(shk_qdesc* q, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out, int clamp, int flags) {
+  shk_ctx* c = q->c;
+  if (Q <= 0) return 0;
+  DBuf th(c), tl(c), to(c);
+  const void *dh, *dl;
+  void* dout;
+  RC(stage_in(c, flags, hi, (size_t)Q * 8, th, &dh));
+  RC(stage_in(c, flags, lo, (size_t)Q * 8, tl, &dl));
+  RC(stage_out(c, flags, out, (size_t)Q * 8, to, &dout));
+  int* err = c->d_counter + 5;
+  SHK_CUDA(cudaMemsetAsync(err, 0, 4, c->stream));
+  RC(shk_launch_query(q->d, (const uint64_t*)dh, (const uint64_t*)dl, Q, (uint64_t*)dout, err, clamp, c->stream));
+  RC(finish_out(c, flags, out, to, (size_t)Q * 8));
+  int herr = 0;
+  RC(d2h(c, &herr, err, 4));
+  RC(csync(c));
+  if (herr) {
+    shk_set_error("bit stream overrun");
+    return SHK_FORMAT;
+  }
+  return 0;
+}
+
+int shk_qdesc_destroy(shk_qdesc* q) {
+  delete q;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// Internal launch interface between the C-ABI layer (shk_capi.cu) and the
+// kernel translation units.  Everything here takes DEVICE pointers and a
+// stream; nothing synchronizes.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+void shk_set_error(const char* fmt, ...);
+
+struct ShkLeafLaunch {
+  const uint64_t* hi;
+  const uint64_t* lo;
+  const int64_t* off;
+  int64_t L;
+  int max_n;
+  uint64_t max_seed;
+  int mode;  // 0 plain, 1 rotate
+  int cache_k;
+  int cache_min_leaf;
+  int64_t* seed_out;
+  uint64_t* fbits_out;
+  uint8_t* choice_out;
+  int64_t* stats_out;
+  int* counter;
+  int* error;
+  int team_warps;  // 0 = heuristic
+  int num_sms;
+  int stride;                     // 1: separate hi/lo arrays; 2: interleaved pairs (lo = hi + 1)
+  const int64_t* seed_slot;       // optional scatter index for seed_out
+  unsigned long long* stats_acc;  // optional [4] totals (evals, passes, checks, a_evals)
+  int* exhausted;                 // optional flag
+  int64_t* place_out;             // optional [N] global slot per key
+};
+int shk_launch_leaf_search(const ShkLeafLaunch& p, cudaStream_t st);
+int shk_launch_orient(const uint8_t* eu, const uint8_t* ev, const int64_t* off, int64_t L, uint64_t* fbits, int* ok,
+                      cudaStream_t st);
+
+// Split tasks: one per split node.  Keys of the node are [start, start + m)
+// of the (bucket-sorted, partially partitioned) key arrays.
+struct ShkSplitTask {
+  int64_t start;
+  int32_t m;
+  int32_t fanout;
+  int32_t sizes[4];
+  int64_t seed_slot;  // index into the node seed array
+};
+struct ShkSplitLaunch {
+  uint64_t* hi;      // interleaved (hi, lo) key pairs
+  uint64_t* lo;      // unused (kept null)
+  uint64_t* tmp_hi;  // scratch pairs, same size
+  uint64_t* tmp_lo;  // unused
+  const ShkSplitTask* tasks;
+  int64_t ntasks;
+  uint64_t max_seed;
+  int64_t* seeds;      // per node
+  int64_t* evals_out;  // per task or null
+  int* counter;
+  int num_sms;
+  int partition;  // 1: stable-partition keys after the search
+  int* exhausted; // optional flag: a node had no seed below max_seed
+};
+int shk_launch_split(const ShkSplitLaunch& p, cudaStream_t st);
+
+// Bucketing.
+// skeys: interleaved (hi, lo) pairs [2N], sorted by (bucket, hi, lo).
+int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nbuckets, uint64_t* skeys,
+                  uint64_t* key_prefix /*[nb+1]*/, int* dup_flag, void* scratch, size_t scratch_bytes,
+                  int64_t* max_bucket_out, cudaStream_t st);
+size_t shk_bucketize_scratch(int64_t N, int64_t nbuckets);
+
+// Generic exclusive scan of int64 (n elements) -> out[n+1] (out[n] = total).
+int shk_exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* scratch, size_t scratch_bytes,
+                           cudaStream_t st);
+size_t shk_scan_scratch(int64_t n);
+
+// Rice: node seeds + g -> bit lengths; scan; scatter into zeroed words.
+int shk_rice_lengths(const int64_t* seeds, const int32_t* g, int64_t nn, int64_t* len, cudaStream_t st);
+int shk_rice_scatter(const int64_t* seeds, const int32_t* g, const int64_t* pos, int64_t nn, uint64_t* words,
+                     cudaStream_t st);
+
+// Ribbon.
+struct ShkRibbon;
+int shk_ribbon_create(ShkRibbon** out);
+void shk_ribbon_destroy(ShkRibbon* r);
+// rows from keys (seed) -> solve; words_out device [ceil(m/64)]; *consistent set.
+// keys: interleaved (hi, lo) pairs [2N].
+int shk_ribbon_solve_keys(ShkRibbon* r, const uint64_t* keys, const uint8_t* rhs, int64_t N, int64_t m,
+                          uint64_t seed, uint64_t* words_out, int* consistent, cudaStream_t st);
+// explicit rows
+int shk_ribbon_solve_rows(ShkRibbon* r, const int64_t* starts, const uint64_t* p0, const uint64_t* p1,
+                          const uint8_t* rhs, int64_t N, int64_t m, uint64_t* words_out, int* consistent,
+                          cudaStream_t st);
+int shk_launch_ribbon_rows(const uint64_t* hi, const uint64_t* lo, int stride, int64_t N, int64_t m, uint64_t seed,
+                           int64_t* starts, uint64_t* p0, uint64_t* p1, cudaStream_t st);
+// Split-hash part index of every key (split_parts seam).
+int shk_launch_split_parts(const uint64_t* hi, const uint64_t* lo, int64_t m, uint64_t seed, const int64_t* sizes,
+                           int fanout, int64_t* parts, cudaStream_t st);
+// Pack separate hi/lo arrays into interleaved pairs.
+int shk_launch_interleave(const uint64_t* hi, const uint64_t* lo, int64_t N, uint64_t* pairs, cudaStream_t st);
+int shk_launch_deinterleave(const uint64_t* pairs, int64_t N, uint64_t* hi, uint64_t* lo, cudaStream_t st);
+int shk_launch_ribbon_query(const int64_t* starts, const uint64_t* p0, const uint64_t* p1, int64_t N,
+                            const uint64_t* words, int64_t nwords, uint8_t* out, cudaStream_t st);
+
+// Query.
+struct ShkQueryDesc {
+  int64_t nbuckets;
+  int64_t n_keys;
+  int mode;
+  int64_t cache_k;
+  const uint64_t* key_prefix;   // [nb+1]
+  const int32_t* bucket_plan;   // [nb]  plan id (or -1 for empty)
+  const int64_t* node_base;     // [nb]  first global node of the bucket
+  const int64_t* node_pos;      // [total nodes] bit position of each node's code
+  const int32_t* bucket_bad;    // [nb]  first node whose decode overran (INT32_MAX none)
+  const uint64_t* bit_offsets;  // [nb+1] stream bit offset of each bucket
+  const uint64_t* stream;       // words
+  int64_t stream_bit_len;
+  int64_t stream_nwords;
+  const int32_t* pn_kind;       // plan nodes, concatenated
+  const int32_t* pn_g;
+  const int32_t* pn_m;
+  const int32_t* pn_child;      // [node][4] plan-local child index
+  const int32_t* pn_sizes;      // [node][4]
+  const int32_t* pn_fanout;
+  const int64_t* plan_off;      // [nplans+1]
+  uint64_t rib_seed;
+  int64_t rib_m;
+  const uint64_t* rib_words;
+  int64_t rib_nwords;
+};
+int shk_launch_node_index(const ShkQueryDesc& d, int64_t* node_pos, int32_t* bucket_bad, cudaStream_t st);
+int shk_launch_query(const ShkQueryDesc& d, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out,
+                     int* err, int clamp, cudaStream_t st);
+
+// Rice-decode a sequence of codes (test / seam parity).
+int shk_launch_rice_decode(const uint64_t* words, int64_t bit_len, int64_t pos, const int32_t* g, int64_t count,
+                           int64_t* values, int64_t* positions, int* err, cudaStream_t st);
+
+// blake2b-128 master hash over CSR byte keys.
+int shk_launch_blake2b(const uint8_t* blob, const int64_t* off, int64_t N, uint64_t salt, uint64_t* hi,
+                       uint64_t* lo, cudaStream_t st);
+int shk_launch_blake2b_fixed(const uint8_t* blob, int key_len, int64_t N, uint64_t salt, uint64_t* hi, uint64_t* lo,
+                             cudaStream_t st);

@@ -1,0 +1,145 @@
+// Batched MPHF evaluation.
+//
+// Restates _core.pyx:642-742 (query_stream) / _pure.py:489-550 and
+// recsplit.py:251-275 (clamp to N-1).  The reference walks the preorder plan
+// of the key's bucket and Rice-decodes EVERY node before the key's leaf (the
+// seeds of skipped left subtrees included, ~38 decodes per query at n=40,
+// b=2000).  Here a derived per-node bit-position index is built once per
+// descriptor (one thread per bucket decodes the bucket's nodes in order), so a
+// query decodes only the split nodes on its root-to-leaf path plus its leaf.
+// Outputs are identical; so are the FormatError cases: a query fails iff the
+// reference's sequential decode would overrun before reaching the key's leaf,
+// i.e. iff the first undecodable node of its bucket has preorder index <= the
+// leaf's.
+#include "shk_common.cuh"
+#include "shk_kernels.h"
+#include "shk_rice.cuh"
+
+namespace shk {
+
+__global__ void node_index_kernel(ShkQueryDesc d, int64_t* node_pos, int32_t* bucket_bad) {
+  for (int64_t bu = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bu < d.nbuckets;
+       bu += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t plan = d.bucket_plan[bu];
+    int32_t bad = 0x7FFFFFFF;
+    if (plan >= 0) {
+      const int64_t p0 = d.plan_off[plan], p1 = d.plan_off[plan + 1];
+      const int64_t nb = d.node_base[bu];
+      int64_t pos = (int64_t)d.bit_offsets[bu];
+      for (int64_t j = 0; j < p1 - p0; ++j) {
+        node_pos[nb + j] = pos;
+        int64_t v;
+        if (rice_decode(d.stream, d.stream_bit_len, &pos, d.pn_g[p0 + j], &v)) {
+          bad = (int32_t)j;
+          break;
+        }
+      }
+    }
+    bucket_bad[bu] = bad;
+  }
+}
+
+SHK_D uint64_t rib_choice(const ShkQueryDesc& d, u2 kh, u2 kl) {
+  if (!d.rib_m) return 0;
+  const uint64_t span = (uint64_t)(d.rib_m - RIBBON_W + 1);
+  const u2 vs = remix_d(kh, kl, split64(seed_mixer(d.rib_seed, TAG_RSTART)));
+  const int64_t s = (int64_t)(((uint64_t)vs.hi * span) >> 32);
+  const u2 a = remix_d(kh, kl, split64(seed_mixer(d.rib_seed, TAG_RPAT0)));
+  const u2 b = remix_d(kh, kl, split64(seed_mixer(d.rib_seed, TAG_RPAT1)));
+  const uint64_t pat0 = join64(a.lo | 1u, a.hi), pat1 = join64(b.lo, b.hi);
+  const int64_t wi = s >> 6;
+  const int sh = (int)(s & 63);
+  const int64_t nw = d.rib_nwords;
+  const uint64_t w0 = wi < nw ? d.rib_words[wi] : 0;
+  const uint64_t w1 = wi + 1 < nw ? d.rib_words[wi + 1] : 0;
+  const uint64_t w2 = wi + 2 < nw ? d.rib_words[wi + 2] : 0;
+  uint64_t v0, v1;
+  if (sh) {
+    v0 = (w0 >> sh) | (w1 << (64 - sh));
+    v1 = (w1 >> sh) | (w2 << (64 - sh));
+  } else {
+    v0 = w0;
+    v1 = w1;
+  }
+  return (uint64_t)((__popcll(v0 & pat0) + __popcll(v1 & pat1)) & 1);
+}
+
+__global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64_t* hi, const uint64_t* lo, int64_t Q,
+                                                    uint64_t* out, int* err, int clamp) {
+  const u2 xb = split64(seed_mixer(0, TAG_BUCKET));
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (int64_t)gridDim.x * blockDim.x) {
+    const u2 kh = split64(hi[t]), kl = split64(lo[t]);
+    const u2 vb = remix_d(kh, kl, xb);
+    const int64_t bucket = (int64_t)__umulhi(vb.hi, (uint32_t)d.nbuckets);
+    const uint64_t kp0 = d.key_prefix[bucket];
+    const int64_t msize = (int64_t)(d.key_prefix[bucket + 1] - kp0);
+    uint64_t offset = 0;
+    if (msize > 0) {
+      const int32_t plan = d.bucket_plan[bucket];
+      const int64_t pb = d.plan_off[plan];
+      const int64_t nbase = d.node_base[bucket];
+      const int32_t bad = d.bucket_bad[bucket];
+      int idx = 0;
+      bool fail = false;
+      while (d.pn_kind[pb + idx] == 0) {
+        if (idx >= bad) {
+          fail = true;
+          break;
+        }
+        int64_t pos = d.node_pos[nbase + idx], seed;
+        rice_decode(d.stream, d.stream_bit_len, &pos, d.pn_g[pb + idx], &seed);
+        const u2 v = remix_d(kh, kl, split64(seed_mixer((uint64_t)seed, TAG_SPLIT)));
+        const uint32_t r = __umulhi(v.hi, (uint32_t)d.pn_m[pb + idx]);
+        const int32_t* sz = d.pn_sizes + 4 * (pb + idx);
+        const int fan = d.pn_fanout[pb + idx];
+        uint32_t acc = 0;
+        int part = 0;
+        for (; part < fan - 1; ++part) {
+          if (r < acc + (uint32_t)sz[part]) break;
+          acc += (uint32_t)sz[part];
+        }
+        offset += acc;
+        idx = d.pn_child[4 * (pb + idx) + part];
+      }
+      if (fail || idx >= bad) {
+        atomicOr(err, 1);
+        out[t] = 0;
+        continue;
+      }
+      int64_t pos = d.node_pos[nbase + idx], q;
+      rice_decode(d.stream, d.stream_bit_len, &pos, d.pn_g[pb + idx], &q);
+      const int mleaf = d.pn_m[pb + idx];
+      const int choice = (int)rib_choice(d, kh, kl);
+      const int cell = leaf_cell(hi[t], lo[t], q, mleaf, d.mode, d.cache_k, choice);
+      offset += (uint64_t)cell;
+    }
+    uint64_t o = kp0 + offset;
+    if (clamp) {
+      const uint64_t mx = d.n_keys > 0 ? (uint64_t)(d.n_keys - 1) : 0;
+      if (o > mx) o = mx;
+    }
+    out[t] = o;
+  }
+}
+
+}  // namespace shk
+
+using namespace shk;
+
+int shk_launch_node_index(const ShkQueryDesc& d, int64_t* node_pos, int32_t* bucket_bad, cudaStream_t st) {
+  if (d.nbuckets <= 0) return 0;
+  int64_t g = (d.nbuckets + 127) / 128;
+  node_index_kernel<<<(unsigned)g, 128, 0, st>>>(d, node_pos, bucket_bad);
+  SHK_LAUNCHED();
+  return 0;
+}
+
+int shk_launch_query(const ShkQueryDesc& d, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out, int* err,
+                     int clamp, cudaStream_t st) {
+  if (Q <= 0) return 0;
+  int64_t g = (Q + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  query_kernel<<<(unsigned)g, 256, 0, st>>>(d, hi, lo, Q, out, err, clamp);
+  SHK_LAUNCHED();
+  return 0;
+}

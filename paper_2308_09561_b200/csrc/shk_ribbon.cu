@@ -1,0 +1,613 @@
+// 1-bit retrieval: banded GF(2) system with a 128-bit band ("ribbon").
+//
+// Restates _core.pyx:435-568 (ribbon_rows, ribbon_solve, window128,
+// parity128, ribbon_query_many) and retrieval.py:93-106.
+//
+// The reference eliminates rows on the fly in key order into one slot per
+// pivot column, then back-substitutes right to left with free columns = 0.
+// That solution is unique given the row space, and so is
+// consistency, so ANY elimination order gives the reference's words.  GPU
+// scheme:
+//   1. rows (start, 128-bit pattern, rhs) are generated and counting-sorted
+//      by elimination chunk (CE columns);
+//   2. one CTA per chunk eliminates its rows into its slots in shared memory
+//      (a single lane walks each row: XOR with the occupied slot, shift to
+//      the next set bit); rows whose pivot walks past the chunk end are
+//      emitted as overflow and inserted by the next pass into the chunk they
+//      reached; passes repeat until no row overflows;
+//   3. back substitution over back-chunks of CB columns runs in parallel
+//      with the solution of the 127 columns right of each chunk as symbolic
+//      unknowns: a warp carries 128 bit-sliced affine forms (4 per lane), so
+//      each chunk yields the affine map from its right neighbour's first 127
+//      bits to its own first 127 bits;
+//   4. a single warp walks the chunks right to left evaluating those maps
+//      (the only sequential step: 127x128 GF(2) mat-vec per chunk);
+//   5. every chunk then back-substitutes for real with its now-known right
+//      boundary and writes its solution words.
+#include "shk_common.cuh"
+#include "shk_kernels.h"
+
+namespace shk {
+
+constexpr int CE = 1024;  // elimination chunk (columns)
+constexpr int CB = 8192;  // back-substitution chunk (columns), multiple of CE and 64
+
+struct RRow {
+  uint64_t p0, p1;
+  int64_t s;  // start column; bit 62 = rhs
+};
+constexpr int64_t RHS_BIT = 1ll << 62;
+constexpr int64_t S_MASK = RHS_BIT - 1;
+
+// ---------------------------------------------------------------------------
+// Row generation (ribbon_rows) + chunk histogram.
+__global__ void ribbon_rows_kernel(const uint64_t* hi, const uint64_t* lo, int stride, int64_t N, int64_t m,
+                                   uint64_t seed, int64_t* starts, uint64_t* p0, uint64_t* p1) {
+  const u2 xs = split64(seed_mixer(seed, TAG_RSTART));
+  const u2 x0 = split64(seed_mixer(seed, TAG_RPAT0));
+  const u2 x1 = split64(seed_mixer(seed, TAG_RPAT1));
+  const uint64_t span = (uint64_t)(m - RIBBON_W + 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    u2 kh = split64(hi[i * stride]), kl = split64(lo[i * stride]);
+    u2 v = remix_d(kh, kl, xs);
+    starts[i] = (int64_t)(((uint64_t)v.hi * span) >> 32);
+    u2 a = remix_d(kh, kl, x0);
+    u2 b = remix_d(kh, kl, x1);
+    p0[i] = join64(a.lo | 1u, a.hi);
+    p1[i] = join64(b.lo, b.hi);
+  }
+}
+
+// Rows from keys directly into chunk buckets (fused generation + histogram).
+__global__ void ribbon_keyrows_hist_kernel(const ulonglong2* keys, int64_t N, int64_t m, uint64_t seed,
+                                           int64_t* hist) {
+  const u2 xs = split64(seed_mixer(seed, TAG_RSTART));
+  const uint64_t span = (uint64_t)(m - RIBBON_W + 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 k = keys[i];
+    u2 v = remix_d(split64(k.x), split64(k.y), xs);
+    int64_t s = (int64_t)(((uint64_t)v.hi * span) >> 32);
+    atomicAdd((unsigned long long*)&hist[s / CE], 1ull);
+  }
+}
+
+__global__ void ribbon_keyrows_scatter_kernel(const ulonglong2* keys, const uint8_t* rhs, int64_t N, int64_t m,
+                                              uint64_t seed, int64_t* cursor, RRow* rows) {
+  const u2 xs = split64(seed_mixer(seed, TAG_RSTART));
+  const u2 x0 = split64(seed_mixer(seed, TAG_RPAT0));
+  const u2 x1 = split64(seed_mixer(seed, TAG_RPAT1));
+  const uint64_t span = (uint64_t)(m - RIBBON_W + 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 k = keys[i];
+    u2 kh = split64(k.x), kl = split64(k.y);
+    u2 v = remix_d(kh, kl, xs);
+    int64_t s = (int64_t)(((uint64_t)v.hi * span) >> 32);
+    u2 a = remix_d(kh, kl, x0);
+    u2 b = remix_d(kh, kl, x1);
+    int64_t pos = (int64_t)atomicAdd((unsigned long long*)&cursor[s / CE], 1ull);
+    RRow r;
+    r.p0 = join64(a.lo | 1u, a.hi);
+    r.p1 = join64(b.lo, b.hi);
+    r.s = s | ((rhs[i] & 1) ? RHS_BIT : 0);
+    rows[pos] = r;
+  }
+}
+
+// Explicit rows (ribbon_solve seam).
+__global__ void ribbon_rows_hist_kernel(const int64_t* starts, int64_t N, int64_t* hist) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long*)&hist[starts[i] / CE], 1ull);
+}
+
+__global__ void ribbon_rows_scatter_kernel(const int64_t* starts, const uint64_t* p0, const uint64_t* p1,
+                                           const uint8_t* rhs, int64_t N, int64_t* cursor, RRow* rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = starts[i];
+    int64_t pos = (int64_t)atomicAdd((unsigned long long*)&cursor[s / CE], 1ull);
+    RRow r;
+    r.p0 = p0[i];
+    r.p1 = p1[i];
+    r.s = s | ((rhs[i] & 1) ? RHS_BIT : 0);
+    rows[pos] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Elimination pass: one CTA (one warp) per chunk with pending rows.
+// Slot state in global memory: sp0/sp1 per column, occ/rhs bitmaps per word.
+__global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const int64_t* row_off, int64_t nchunks,
+                                                         int64_t m, uint64_t* sp0, uint64_t* sp1, uint32_t* occ,
+                                                         uint32_t* sbit, RRow* ovf, int64_t* ovf_count,
+                                                         int* inconsistent) {
+  __shared__ uint64_t q0s[CE], q1s[CE];
+  __shared__ uint32_t occs[CE / 32], sbs[CE / 32];
+  const int64_t c = blockIdx.x;
+  if (c >= nchunks) return;
+  const int64_t r0 = row_off[c], r1 = row_off[c + 1];
+  if (r0 == r1) return;
+  const int lane = threadIdx.x;
+  const int64_t base = c * CE;
+  const int64_t cols = (m - base < CE) ? (m - base) : CE;
+  for (int j = lane; j < CE; j += 32) {
+    if (j < cols) {
+      q0s[j] = sp0[base + j];
+      q1s[j] = sp1[base + j];
+    } else {
+      q0s[j] = 0;
+      q1s[j] = 0;
+    }
+  }
+  const int64_t wbase = base / 32;
+  for (int j = lane; j < CE / 32; j += 32) {
+    bool in = (j * 32) < cols;
+    occs[j] = in ? occ[wbase + j] : 0;
+    sbs[j] = in ? sbit[wbase + j] : 0;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    bool bad = false;
+    for (int64_t ri = r0; ri < r1 && !bad; ++ri) {
+      RRow r = rows[ri];
+      uint64_t a0 = r.p0, a1 = r.p1;
+      uint32_t b = (r.s & RHS_BIT) ? 1u : 0u;
+      int64_t j = (r.s & S_MASK) - base;
+      for (;;) {
+        if (j >= CE) {
+          int64_t k = (int64_t)atomicAdd((unsigned long long*)ovf_count, 1ull);
+          RRow o;
+          o.p0 = a0;
+          o.p1 = a1;
+          o.s = (base + j) | (b ? RHS_BIT : 0);
+          ovf[k] = o;
+          break;
+        }
+        const uint32_t bitm = 1u << (j & 31);
+        const uint32_t w = occs[j >> 5];
+        if (!(w & bitm)) {
+          occs[j >> 5] = w | bitm;
+          if (b) sbs[j >> 5] |= bitm;
+          q0s[j] = a0;
+          q1s[j] = a1;
+          break;
+        }
+        a0 ^= q0s[j];
+        a1 ^= q1s[j];
+        b ^= (sbs[j >> 5] >> (j & 31)) & 1u;
+        if ((a0 | a1) == 0) {
+          if (b) bad = true;
+          break;
+        }
+        int t;
+        if (a0) {
+          t = __ffsll((long long)a0) - 1;
+          a0 = (a0 >> t) | (t ? (a1 << (64 - t)) : 0);
+          a1 >>= t;
+        } else {
+          t = 63 + __ffsll((long long)a1);  // 64 + ctz(a1)
+          a0 = a1 >> (t - 64);
+          a1 = 0;
+        }
+        j += t;
+      }
+    }
+    if (bad) atomicOr(inconsistent, 1);
+  }
+  __syncwarp();
+  for (int j = lane; j < cols; j += 32) {
+    sp0[base + j] = q0s[j];
+    sp1[base + j] = q1s[j];
+  }
+  for (int j = lane; j < CE / 32; j += 32) {
+    if ((j * 32) < cols) {
+      occ[wbase + j] = occs[j];
+      sbit[wbase + j] = sbs[j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Symbolic back substitution (affine forms), one warp per back-chunk.
+// Lane L owns unknowns u = 4L..4L+3 (u = 127 is the constant term); for each
+// it keeps W_u: a 128-bit window whose bit k is the coefficient of u in
+// sol[c + 1 + k].  forms_out[chunk][u] = W_u after the chunk's first column.
+__global__ void __launch_bounds__(32) ribbon_forms_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
+                                                          const uint64_t* sp1, const uint32_t* occ,
+                                                          const uint32_t* sbit, uint4* forms) {
+  __shared__ uint64_t tp0[256], tp1[256];
+  __shared__ uint32_t tocc[8], tsb[8];
+  const int64_t c = blockIdx.x;
+  if (c >= nbchunks) return;
+  const int lane = threadIdx.x;
+  const int64_t s0 = c * CB;
+  const int64_t e = (s0 + CB < m) ? s0 + CB : m;
+  uint32_t W[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int u = 4 * lane + q;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) W[q][w] = (u < 127 && (u >> 5) == w) ? (1u << (u & 31)) : 0u;
+  }
+  // process columns e-1 down to s0 in tiles of 256 (tile start aligned to 256)
+  int64_t col = e - 1;
+  while (col >= s0) {
+    const int64_t tstart = (col / 256) * 256 > s0 ? (col / 256) * 256 : s0;
+    const int ntile = (int)(col - tstart + 1);
+    __syncwarp();
+    for (int j = lane; j < ntile; j += 32) {
+      tp0[j] = sp0[tstart + j];
+      tp1[j] = sp1[tstart + j];
+    }
+    if (lane < 8) {
+      int64_t wi = tstart / 32 + lane;
+      bool in = (int64_t)lane * 32 < ntile;
+      tocc[lane] = in ? occ[wi] : 0;
+      tsb[lane] = in ? sbit[wi] : 0;
+    }
+    __syncwarp();
+    for (int j = ntile - 1; j >= 0; --j) {
+      const uint32_t o = (tocc[j >> 5] >> (j & 31)) & 1u;
+      uint32_t nb[4] = {0, 0, 0, 0};
+      if (o) {
+        const uint64_t a0 = tp0[j], a1 = tp1[j];
+        // p >> 1 as four 32-bit words
+        const uint32_t pw0 = (uint32_t)(a0 >> 1) | ((uint32_t)(a0 >> 32) << 31);
+        const uint32_t pw1 = (uint32_t)(a0 >> 33) | ((uint32_t)a1 << 31);
+        const uint32_t pw2 = (uint32_t)(a1 >> 1) | ((uint32_t)(a1 >> 32) << 31);
+        const uint32_t pw3 = (uint32_t)(a1 >> 33);
+        const uint32_t b = (tsb[j >> 5] >> (j & 31)) & 1u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t x = (W[q][0] & pw0) ^ (W[q][1] & pw1) ^ (W[q][2] & pw2) ^ (W[q][3] & pw3);
+          nb[q] = __popc(x) & 1u;
+        }
+        if (lane == 31) nb[3] ^= b;  // u = 127: constant term
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        W[q][3] = (W[q][3] << 1) | (W[q][2] >> 31);
+        W[q][2] = (W[q][2] << 1) | (W[q][1] >> 31);
+        W[q][1] = (W[q][1] << 1) | (W[q][0] >> 31);
+        W[q][0] = (W[q][0] << 1) | nb[q];
+      }
+    }
+    col = tstart - 1;
+  }
+  uint4* f = forms + c * 128;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) f[4 * lane + q] = make_uint4(W[q][0], W[q][1], W[q][2], W[q][3]);
+}
+
+// Right-to-left chain over back-chunks: y[c] = first 127 solution bits of
+// chunk c + 1 (right boundary of chunk c).  One warp.
+__global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, const uint4* forms, uint4* ybound) {
+  const int lane = threadIdx.x;
+  uint4 y = make_uint4(0, 0, 0, 0);  // boundary right of the last chunk: zero
+  for (int64_t c = nbchunks - 1; c >= 0; --c) {
+    ybound[c] = y;
+    const uint4* f = forms + c * 128;
+    uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int u = 4 * lane + q;
+      uint32_t yw = (u >> 5) == 0 ? y.x : (u >> 5) == 1 ? y.y : (u >> 5) == 2 ? y.z : y.w;
+      uint32_t sel = (u == 127) ? 1u : ((yw >> (u & 31)) & 1u);
+      uint4 w = f[u];
+      uint32_t msk = 0u - sel;
+      acc0 ^= w.x & msk;
+      acc1 ^= w.y & msk;
+      acc2 ^= w.z & msk;
+      acc3 ^= w.w & msk;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc0 ^= __shfl_xor_sync(FULL_WARP, acc0, o);
+      acc1 ^= __shfl_xor_sync(FULL_WARP, acc1, o);
+      acc2 ^= __shfl_xor_sync(FULL_WARP, acc2, o);
+      acc3 ^= __shfl_xor_sync(FULL_WARP, acc3, o);
+    }
+    y = make_uint4(acc0, acc1, acc2, acc3 & 0x7FFFFFFFu);  // 127 bits
+  }
+}
+
+// Final back substitution with the known right boundary: one thread per
+// back-chunk, 128-bit window, writes the chunk's solution words.
+__global__ void ribbon_final_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0, const uint64_t* sp1,
+                                    const uint32_t* occ, const uint32_t* sbit, const uint4* ybound, uint64_t* words) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nbchunks) return;
+  const int64_t s0 = c * CB;
+  const int64_t e = (s0 + CB < m) ? s0 + CB : m;
+  uint4 y = ybound[c];
+  // window bit k = sol[col + 1 + k]
+  uint64_t w0 = (uint64_t)y.x | ((uint64_t)y.y << 32);
+  uint64_t w1 = (uint64_t)y.z | ((uint64_t)y.w << 32);
+  uint64_t outw = 0;
+  for (int64_t col = e - 1; col >= s0; --col) {
+    uint32_t bit = 0;
+    if ((occ[col >> 5] >> (col & 31)) & 1u) {
+      const uint64_t a0 = sp0[col], a1 = sp1[col];
+      const uint64_t q0 = (a0 >> 1) | (a1 << 63), q1 = a1 >> 1;
+      bit = (uint32_t)((__popcll(q0 & w0) + __popcll(q1 & w1)) & 1) ^ ((sbit[col >> 5] >> (col & 31)) & 1u);
+    }
+    w1 = (w1 << 1) | (w0 >> 63);
+    w0 = (w0 << 1) | bit;
+    outw |= (uint64_t)bit << (col & 63);
+    if ((col & 63) == 0) {
+      words[col >> 6] = outw;
+      outw = 0;
+    }
+  }
+  // e is a multiple of 64 except possibly at m; the first column s0 is a
+  // multiple of 64, so every word was flushed at col % 64 == 0.
+}
+
+__global__ void ribbon_query_kernel(const int64_t* starts, const uint64_t* p0, const uint64_t* p1, int64_t N,
+                                    const uint64_t* words, int64_t nwords, uint8_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = starts[i];
+    int64_t wi = s >> 6;
+    int sh = (int)(s & 63);
+    uint64_t v0 = 0, v1 = 0;
+    uint64_t a = wi < nwords ? words[wi] : 0;
+    uint64_t b = wi + 1 < nwords ? words[wi + 1] : 0;
+    uint64_t c = wi + 2 < nwords ? words[wi + 2] : 0;
+    if (sh) {
+      v0 = (a >> sh) | (b << (64 - sh));
+      v1 = (b >> sh) | (c << (64 - sh));
+    } else {
+      v0 = a;
+      v1 = b;
+    }
+    out[i] = (uint8_t)((__popcll(v0 & p0[i]) + __popcll(v1 & p1[i])) & 1);
+  }
+}
+
+__global__ void ribbon_ovf_hist_kernel(const RRow* o, int64_t n, int64_t* hist) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long*)&hist[(o[i].s & S_MASK) / CE], 1ull);
+}
+__global__ void ribbon_ovf_scatter_kernel(const RRow* o, int64_t n, int64_t* cursor, RRow* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    RRow r = o[i];
+    int64_t p = (int64_t)atomicAdd((unsigned long long*)&cursor[(r.s & S_MASK) / CE], 1ull);
+    out[p] = r;
+  }
+}
+
+}  // namespace shk
+
+using namespace shk;
+
+struct ShkRibbon {
+  // device buffers, grown on demand
+  void* buf = nullptr;
+  size_t cap = 0;
+};
+
+int shk_ribbon_create(ShkRibbon** out) {
+  *out = new ShkRibbon();
+  return 0;
+}
+
+void shk_ribbon_destroy(ShkRibbon* r) {
+  if (!r) return;
+  if (r->buf) cudaFree(r->buf);
+  delete r;
+}
+
+namespace {
+
+struct RibLayout {
+  size_t off_rows, off_rows2, off_ovf, off_hist, off_rowoff, off_cursor, off_sp0, off_sp1, off_occ, off_sb, off_forms,
+      off_y, off_cnt, off_scan, total;
+};
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+RibLayout layout(int64_t N, int64_t m) {
+  RibLayout L;
+  int64_t nch = (m + CE - 1) / CE;
+  int64_t nbc = (m + CB - 1) / CB;
+  int64_t nw32 = (m + 31) / 32 + CE / 32;
+  size_t o = 0;
+  L.off_rows = o;
+  o += al((size_t)(N + 1) * sizeof(RRow));
+  L.off_rows2 = o;
+  o += al((size_t)(N + 1) * sizeof(RRow));
+  L.off_ovf = o;
+  o += al((size_t)(N + 1) * sizeof(RRow));
+  L.off_hist = o;
+  o += al((size_t)(nch + 1) * 8);
+  L.off_rowoff = o;
+  o += al((size_t)(nch + 2) * 8);
+  L.off_cursor = o;
+  o += al((size_t)(nch + 1) * 8);
+  L.off_sp0 = o;
+  o += al((size_t)(m + 64) * 8);
+  L.off_sp1 = o;
+  o += al((size_t)(m + 64) * 8);
+  L.off_occ = o;
+  o += al((size_t)nw32 * 4);
+  L.off_sb = o;
+  o += al((size_t)nw32 * 4);
+  L.off_forms = o;
+  o += al((size_t)nbc * 128 * 16);
+  L.off_y = o;
+  o += al((size_t)nbc * 16);
+  L.off_cnt = o;
+  o += 256;
+  L.off_scan = o;
+  o += al(shk_scan_scratch(nch));
+  L.total = o;
+  return L;
+}
+
+int ensure(ShkRibbon* r, size_t bytes) {
+  if (r->cap >= bytes) return 0;
+  if (r->buf) cudaFree(r->buf);
+  r->buf = nullptr;
+  r->cap = 0;
+  SHK_CUDA(cudaMalloc(&r->buf, bytes));
+  r->cap = bytes;
+  return 0;
+}
+
+int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// Shared driver once rows are in r->buf at off_rows with the chunk offsets
+// in off_rowoff.
+int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_t* words_out, int* consistent,
+                 cudaStream_t st) {
+  char* B = (char*)R->buf;
+  const int64_t nch = (m + CE - 1) / CE;
+  const int64_t nbc = (m + CB - 1) / CB;
+  const int64_t nw32 = (m + 31) / 32 + CE / 32;
+  RRow* rows = (RRow*)(B + L.off_rows);
+  RRow* rows2 = (RRow*)(B + L.off_rows2);
+  RRow* ovf = (RRow*)(B + L.off_ovf);
+  int64_t* hist = (int64_t*)(B + L.off_hist);
+  int64_t* rowoff = (int64_t*)(B + L.off_rowoff);
+  int64_t* cursor = (int64_t*)(B + L.off_cursor);
+  uint64_t* sp0 = (uint64_t*)(B + L.off_sp0);
+  uint64_t* sp1 = (uint64_t*)(B + L.off_sp1);
+  uint32_t* occ = (uint32_t*)(B + L.off_occ);
+  uint32_t* sb = (uint32_t*)(B + L.off_sb);
+  uint4* forms = (uint4*)(B + L.off_forms);
+  uint4* yb = (uint4*)(B + L.off_y);
+  int64_t* cnt = (int64_t*)(B + L.off_cnt);  // [0] ovf count, [1] inconsistent flag (int)
+  void* scan = B + L.off_scan;
+
+  SHK_CUDA(cudaMemsetAsync(sp0, 0, (size_t)(m + 64) * 8, st));
+  SHK_CUDA(cudaMemsetAsync(sp1, 0, (size_t)(m + 64) * 8, st));
+  SHK_CUDA(cudaMemsetAsync(occ, 0, (size_t)nw32 * 4, st));
+  SHK_CUDA(cudaMemsetAsync(sb, 0, (size_t)nw32 * 4, st));
+  SHK_CUDA(cudaMemsetAsync(cnt, 0, 256, st));
+  int* bad = (int*)(cnt + 1);
+  int64_t pending = N;
+  RRow* cur = rows;
+  for (int pass = 0; pending > 0; ++pass) {
+    SHK_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
+    ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(cur, rowoff, nch, m, sp0, sp1, occ, sb, ovf, cnt, bad);
+    SHK_LAUNCHED();
+    int64_t h[2];
+    SHK_CUDA(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, st));
+    SHK_CUDA(cudaStreamSynchronize(st));
+    if ((int)h[1]) break;
+    pending = h[0];
+    if (!pending) break;
+    // regroup overflow rows by chunk into rows2
+    SHK_CUDA(cudaMemsetAsync(hist, 0, (size_t)(nch + 1) * 8, st));
+    ribbon_ovf_hist_kernel<<<grid_for(pending), 256, 0, st>>>(ovf, pending, hist);
+    SHK_LAUNCHED();
+    int rc = shk_exclusive_scan_i64(hist, rowoff, nch, scan, shk_scan_scratch(nch), st);
+    if (rc) return rc;
+    SHK_CUDA(cudaMemcpyAsync(cursor, rowoff, (size_t)nch * 8, cudaMemcpyDeviceToDevice, st));
+    ribbon_ovf_scatter_kernel<<<grid_for(pending), 256, 0, st>>>(ovf, pending, cursor, rows2);
+    SHK_LAUNCHED();
+    cur = rows2;
+    if (pass > 100000) {
+      shk_set_error("ribbon elimination did not converge");
+      return -1;
+    }
+  }
+  int hbad = 0;
+  SHK_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaStreamSynchronize(st));
+  if (hbad) {
+    *consistent = 0;
+    return 0;
+  }
+  *consistent = 1;
+  ribbon_forms_kernel<<<(unsigned)nbc, 32, 0, st>>>(m, nbc, sp0, sp1, occ, sb, forms);
+  SHK_LAUNCHED();
+  ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, forms, yb);
+  SHK_LAUNCHED();
+  ribbon_final_kernel<<<(unsigned)((nbc + 63) / 64), 64, 0, st>>>(m, nbc, sp0, sp1, occ, sb, yb, words_out);
+  SHK_LAUNCHED();
+  return 0;
+}
+
+}  // namespace
+
+
+int shk_ribbon_solve_keys(ShkRibbon* R, const uint64_t* keys_u64, const uint8_t* rhs, int64_t N, int64_t m,
+                          uint64_t seed, uint64_t* words_out, int* consistent, cudaStream_t st) {
+  const ulonglong2* keys = reinterpret_cast<const ulonglong2*>(keys_u64);
+  if (m < RIBBON_W) {
+    shk_set_error("ribbon needs m >= 128");
+    return 3;
+  }
+  RibLayout L = layout(N, m);
+  int rc = ensure(R, L.total);
+  if (rc) return rc;
+  char* B = (char*)R->buf;
+  const int64_t nch = (m + CE - 1) / CE;
+  int64_t* hist = (int64_t*)(B + L.off_hist);
+  int64_t* rowoff = (int64_t*)(B + L.off_rowoff);
+  int64_t* cursor = (int64_t*)(B + L.off_cursor);
+  SHK_CUDA(cudaMemsetAsync(hist, 0, (size_t)(nch + 1) * 8, st));
+  if (N > 0) {
+    ribbon_keyrows_hist_kernel<<<grid_for(N), 256, 0, st>>>(keys, N, m, seed, hist);
+    SHK_LAUNCHED();
+  }
+  rc = shk_exclusive_scan_i64(hist, rowoff, nch, B + L.off_scan, shk_scan_scratch(nch), st);
+  if (rc) return rc;
+  SHK_CUDA(cudaMemcpyAsync(cursor, rowoff, (size_t)nch * 8, cudaMemcpyDeviceToDevice, st));
+  if (N > 0) {
+    ribbon_keyrows_scatter_kernel<<<grid_for(N), 256, 0, st>>>(keys, rhs, N, m, seed, cursor,
+                                                               (RRow*)(B + L.off_rows));
+    SHK_LAUNCHED();
+  }
+  return solve_sorted(R, L, N, m, words_out, consistent, st);
+}
+
+int shk_ribbon_solve_rows(ShkRibbon* R, const int64_t* starts, const uint64_t* p0, const uint64_t* p1,
+                          const uint8_t* rhs, int64_t N, int64_t m, uint64_t* words_out, int* consistent,
+                          cudaStream_t st) {
+  if (m < RIBBON_W) {
+    shk_set_error("ribbon needs m >= 128");
+    return 3;
+  }
+  RibLayout L = layout(N, m);
+  int rc = ensure(R, L.total);
+  if (rc) return rc;
+  char* B = (char*)R->buf;
+  const int64_t nch = (m + CE - 1) / CE;
+  int64_t* hist = (int64_t*)(B + L.off_hist);
+  int64_t* rowoff = (int64_t*)(B + L.off_rowoff);
+  int64_t* cursor = (int64_t*)(B + L.off_cursor);
+  SHK_CUDA(cudaMemsetAsync(hist, 0, (size_t)(nch + 1) * 8, st));
+  if (N > 0) {
+    ribbon_rows_hist_kernel<<<grid_for(N), 256, 0, st>>>(starts, N, hist);
+    SHK_LAUNCHED();
+  }
+  rc = shk_exclusive_scan_i64(hist, rowoff, nch, B + L.off_scan, shk_scan_scratch(nch), st);
+  if (rc) return rc;
+  SHK_CUDA(cudaMemcpyAsync(cursor, rowoff, (size_t)nch * 8, cudaMemcpyDeviceToDevice, st));
+  if (N > 0) {
+    ribbon_rows_scatter_kernel<<<grid_for(N), 256, 0, st>>>(starts, p0, p1, rhs, N, cursor, (RRow*)(B + L.off_rows));
+    SHK_LAUNCHED();
+  }
+  return solve_sorted(R, L, N, m, words_out, consistent, st);
+}
+
+int shk_launch_ribbon_rows(const uint64_t* hi, const uint64_t* lo, int stride, int64_t N, int64_t m, uint64_t seed,
+                           int64_t* starts, uint64_t* p0, uint64_t* p1, cudaStream_t st) {
+  if (N <= 0) return 0;
+  ribbon_rows_kernel<<<grid_for(N), 256, 0, st>>>(hi, lo, stride, N, m, seed, starts, p0, p1);
+  SHK_LAUNCHED();
+  return 0;
+}
+
+int shk_launch_ribbon_query(const int64_t* starts, const uint64_t* p0, const uint64_t* p1, int64_t N,
+                            const uint64_t* words, int64_t nwords, uint8_t* out, cudaStream_t st) {
+  if (N <= 0) return 0;
+  ribbon_query_kernel<<<grid_for(N), 256, 0, st>>>(starts, p0, p1, N, words, nwords, out);
+  SHK_LAUNCHED();
+  return 0;
+}
