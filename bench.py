@@ -1,0 +1,389 @@
+#!/usr/bin/env python3
+"""Benchmark: ShockHash-RS MPHF build on B200 (BASELINE.json configs[3], "C4").
+
+Workload (one step): build the minimal perfect hash function of N=10,000,000
+uniform random 64-bit keys (8-byte little-endian strings, ``default_rng(4)``),
+leaf size n=40, bucket size b=2000, rotation fitting — the largest
+single-GPU configuration of BASELINE.json; the 1e8-query pass of the same
+config is measured after the build steps and reported beside it.
+
+  value : keys/s of the build from master hash codes resident in HBM
+          (bucketize -> split searches -> leaf searches + orientation ->
+          Rice stream -> ribbon), CUDA events on the launching stream.
+  e2e   : keys/s through the public C-ABI/Python API with HOST buffers:
+          8-byte key blob H2D -> blake2b -> build -> descriptor bytes D2H.
+
+Multi-GPU (torchrun): buckets are sharded by range over ranks (strong
+scaling, total N fixed); one all-gather joins streams and choice bits;
+rank 0 solves the global ribbon.  Time = max over ranks.
+
+``--impl reference`` times the reference's CPU implementation of the same
+path: its own compiled kernels (oracle/_ref, built from /root/reference by
+oracle/build_ref.sh) under the reference's build orchestration restated in
+oracle/refbuild.py, with all host cores over buckets, on a bounded sample.
+"""
+
+import argparse
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(N=10_000_000, n=40, b=2000, mode=1, queries=100_000_000)
+W_KEY = 53   # int32 ops per key-hash-eval, 64-bit masks
+W_SEED = 22  # per seed mixer + mask compare
+W_ROT = 10   # per rotation test, 64-bit masks
+W_SPLIT = 46  # per split key-eval
+INT_OPS_PER_CLK_SM = 128  # 4 SMSPs x 32 lanes, ALU + FMA pipes (one warp-instr/clk/SMSP)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.rows = []
+        self.gpu = gpu_index
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *e):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = []
+        mx = None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() in ("active", "1", "yes"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def input_keys():
+    from paper_2308_09561_b200 import workloads as W
+
+    k = W.build_keys(4)
+    blob = np.frombuffer(np.ascontiguousarray(k, dtype="<u8").tobytes(), dtype=np.uint8)
+    return k, blob
+
+
+def roofline_numbers(prof, hash_evals, n, clock_mhz, sms):
+    """Integer-issue roofline of the dominant kernel (split or leaf search)."""
+    ph = prof["phase_ms"]
+    leaf_ops = hash_evals * W_KEY + (hash_evals / 2) * W_ROT + (hash_evals / (2 * n)) * 2 * W_SEED
+    split_ops = prof["split_evals"] * W_SPLIT
+    peak = INT_OPS_PER_CLK_SM * sms * 1965e6 / 1e12  # Tops/s at max clock
+    kern = {
+        "leaf_search": (leaf_ops, ph["leaf_search"]),
+        "split_search": (split_ops, ph["split_search"]),
+    }
+    dom = max(kern, key=lambda k: kern[k][1])
+    ops, ms = kern[dom]
+    ach = ops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    other = {k: {"achieved": round(v[0] / (v[1] * 1e-3) / 1e12, 3) if v[1] > 0 else None,
+                 "ms": round(v[1], 3), "algorithmic_ops": int(v[0])} for k, v in kern.items()}
+    return {
+        "kernel": dom,
+        "bound": "int32-issue",
+        "achieved": round(ach, 3),
+        "peak": round(peak, 2),
+        "unit": "Tops/s",
+        "frac": round(ach / peak, 4),
+        "traffic": None,
+        "peak_source": "nominal 128 int32 ops/clk/SM x %d SMs x 1965 MHz (no integer peak in MEASURED_PEAKS.json)" % sms,
+        "frac_at_run_clock": round(ach / (peak * clock_mhz / 1965.0), 4) if clock_mhz else None,
+        "per_kernel": other,
+    }
+
+
+def cpu_baseline_sample(seconds_target=15.0):
+    """Reference CPU path on a bounded sample of the same workload (rank 0)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refbuild
+
+    return refbuild.time_build_sample(seconds_target=seconds_target)
+
+
+def run_ours(args):
+    rank, world, local = dist_info()
+    os.environ.setdefault("SHK_DEVICE", str(local))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2308_09561_b200 import dist as shdist
+    from paper_2308_09561_b200 import device as dev
+    from paper_2308_09561_b200 import recsplit
+    from paper_2308_09561_b200 import workloads as W
+
+    N, n, b = CFG["N"], CFG["n"], CFG["b"]
+    k, blob = input_keys()
+    sms = dev.num_sms()
+    # resident inputs: the master codes, computed once on the GPU
+    d_blob = dev.DeviceBuffer.from_host(blob)
+    d_hi = dev.DeviceBuffer(8 * N)
+    d_lo = dev.DeviceBuffer(8 * N)
+    dev.blake2b_fixed_device(d_blob, 8, N, 0, d_hi, d_lo)
+    dev.sync()
+
+    def step():
+        if world == 1:
+            d = recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"])
+            return d, d.device_profile
+        d, prof = shdist.build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"],
+                                                     device=__import__("torch").device("cuda", local))
+        prof = dict(prof)
+        prof["phase_ms"] = dict(zip(("bucketize", "split_search", "leaf_search", "rice", "ribbon"), prof["phase_ms"]))
+        return d, prof
+
+    for _ in range(args.warmup):
+        desc, prof = step()
+    parity = {}
+    if rank == 0 and desc is not None:
+        blob_desc = desc.serialize()
+        parity["desc_sha256"] = hashlib.sha256(blob_desc).hexdigest()
+        gpath = os.path.join(ROOT, "tests", "golden", "c4.json")
+        if os.path.exists(gpath):
+            g = json.load(open(gpath))
+            parity["desc_matches_reference"] = parity["desc_sha256"] == g["desc_sha"]
+        parity["bits_per_key"] = round(len(blob_desc) * 8 / N, 6)
+    barrier(world)
+    dev.sync()
+    launches0 = dev.launch_count()
+    with ClockSampler(local) as clk:
+        barrier(world)
+        dev.sync()
+        t_wall = time.perf_counter()
+        with dev.timer() as tm:
+            profs = []
+            for _ in range(args.steps):
+                desc, prof = step()
+                profs.append(prof)
+        dev.sync()
+        wall = time.perf_counter() - t_wall
+        barrier(world)
+    launches = dev.launch_count() - launches0
+    ms_total = max_over_ranks(tm.ms, world)
+    ms_step = ms_total / args.steps
+    value = N / (ms_step * 1e-3)
+
+    # e2e through the public API with host buffers (single process view)
+    e2e = None
+    if world == 1:
+        desc_bytes = 0
+        dev.sync()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            d2 = recsplit.build_blob(blob, 8, b, n, CFG["mode"])
+            out = d2.serialize()
+            desc_bytes = len(out)
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": round(N / e2e_s, 1), "unit": "keys/s", "h2d_bytes_per_step": int(blob.nbytes),
+               "d2h_bytes_per_step": int(desc_bytes), "ms_per_step": round(e2e_s * 1e3, 3),
+               "path": "recsplit.build_blob(host 8-byte key blob) -> serialize(); H2D+blake2b+build+D2H timed"}
+        if args.check:
+            parity["e2e_desc_matches_reference"] = hashlib.sha256(out).hexdigest() == parity.get("desc_sha256")
+
+    # queries (C4: 1e8 keys drawn from the set), device-resident
+    query = None
+    if rank == 0 and args.queries > 0 and desc is not None:
+        query = bench_queries(desc, k, args, dev, sms)
+
+    if rank != 0:
+        return
+    prof = profs[-1]
+    hash_evals = desc.build_stats.get("hash_evals") if desc.build_stats else None
+    clocks = clk.summary()
+    line = {
+        "metric": "keys/s MPHF build (ShockHash-RS, N=1e7, n=40, b=2000, rotate)",
+        "value": round(value, 1),
+        "unit": "keys/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u64",
+        "data": "synthetic: default_rng(4) uniform 64-bit keys as 8-byte LE strings (the reference's recipe, SURVEY.md §8(d))",
+        "config": {"workload": "C4: ShockHash-RS build N=10,000,000, leaf n=40, bucket b=2000, mode rotate, eps=0.05",
+                   "N": N, "n": n, "b": b, "parallelism": f"bucket-range x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs 160 MB of resident master codes + 160 MB working keys > 126 MB L2 (no flush needed)"},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "wall_s_timed": round(wall, 3),
+        "phase_ms": {k2: round(v, 3) for k2, v in prof["phase_ms"].items()},
+        "parity": parity,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if hash_evals is not None and world == 1:
+        line["roofline"] = roofline_numbers(prof, hash_evals, n, clocks.get("sm_mhz"), sms)
+    if query:
+        line["query"] = query
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
+        except Exception as e:  # report, never crash the GPU line
+            line["cpu_baseline"] = {"error": f"{type(e).__name__}: {e}"}
+    print(json.dumps(line), flush=True)
+
+
+def bench_queries(desc, k, args, dev, sms):
+    from paper_2308_09561_b200 import workloads as W
+
+    Q = args.queries
+    idx = W.query_indices(4, Q)
+    # master codes of the query keys (blake2b on the GPU from the key bytes)
+    qblob = np.frombuffer(np.ascontiguousarray(k[idx], dtype="<u8").tobytes(), dtype=np.uint8)
+    d_qblob = dev.DeviceBuffer.from_host(qblob)
+    d_qhi = dev.DeviceBuffer(8 * Q)
+    d_qlo = dev.DeviceBuffer(8 * Q)
+    dev.blake2b_fixed_device(d_qblob, 8, Q, desc.salt, d_qhi, d_qlo)
+    d_qblob.free()
+    d_out = dev.DeviceBuffer(8 * Q)
+    dd = desc.device()
+    dd.query_device(d_qhi.ptr, d_qlo.ptr, Q, d_out.ptr)
+    dev.sync()
+    reps = max(1, args.query_reps)
+    with dev.timer() as tm:
+        for _ in range(reps):
+            dd.query_device(d_qhi.ptr, d_qlo.ptr, Q, d_out.ptr)
+    ms = tm.ms / reps
+    res = {"queries": Q, "value": round(Q / (ms * 1e-3), 1), "unit": "queries/s", "ms": round(ms, 3)}
+    hbm = 24.0 * Q / (ms * 1e-3) / 1e9
+    res["hbm_GBps_algorithmic"] = round(hbm, 1)
+    res["hbm_frac_of_measured"] = round(hbm / 6531.9, 4)
+    if args.check:
+        out = d_out.download(np.uint64, Q)
+        qsha = hashlib.sha256(out.astype("<u8").tobytes()).hexdigest()
+        gpath = os.path.join(ROOT, "tests", "golden", "c4.json")
+        if os.path.exists(gpath):
+            res["matches_reference"] = qsha == json.load(open(gpath))["query_sha"]
+    for b_ in (d_qhi, d_qlo, d_out):
+        b_.free()
+    return res
+
+
+def run_reference(args):
+    rank, world, local = dist_info()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refbuild
+
+    r = refbuild.time_build_sample(seconds_target=args.cpu_seconds, steps=args.steps, warmup=args.warmup)
+    line = {
+        "impl": "reference",
+        "metric": "keys/s MPHF build (ShockHash-RS, N=1e7, n=40, b=2000, rotate)",
+        "value": r["value"],
+        "unit": "keys/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": r["ms_per_step"],
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u64",
+        "data": "synthetic: default_rng(4) uniform 64-bit keys (bounded sample of the C4 workload)",
+        "config": {"workload": "C4: ShockHash-RS build N=10,000,000, leaf n=40, bucket b=2000, mode rotate, eps=0.05",
+                   "N": CFG["N"], "n": CFG["n"], "b": CFG["b"], "parallelism": "host cores over buckets"},
+        "cpu_baseline": {"value": r["value"], "unit": "keys/s", "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": r["value"], "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--queries", type=int, default=CFG["queries"])
+    ap.add_argument("--query-reps", type=int, default=3)
+    ap.add_argument("--check", action="store_true", default=True)
+    ap.add_argument("--no-check", dest="check", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 1)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

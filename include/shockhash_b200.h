@@ -128,6 +128,10 @@ int shk_rice_decode(shk_ctx* ctx, const uint64_t* words, int64_t nwords, int64_t
  * keys.py:46-58).  Keys are a byte blob with CSR offsets off[N+1]. */
 int shk_blake2b128(shk_ctx* ctx, const uint8_t* blob, int64_t blob_len, const int64_t* off, int64_t N, uint64_t salt,
                    uint64_t* hi, uint64_t* lo, int flags);
+/* Same for N keys of key_len (1..128) bytes each, back to back (the
+ * benchmark's 8-byte little-endian keys). */
+int shk_blake2b128_fixed(shk_ctx* ctx, const uint8_t* blob, int key_len, int64_t N, uint64_t salt, uint64_t* hi,
+                         uint64_t* lo, int flags);
 
 /* ---- plan tables (recsplit.flatten_plan, recsplit.py:95-119), one per
  * distinct bucket size, concatenated: plan p covers nodes
@@ -173,6 +177,10 @@ int shk_build_set_record_placements(shk_build* b, int on);
 int shk_build_placements(shk_build* b, int64_t* out /* [N] host */);
 int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int64_t m, int max_tries,
                      uint64_t* seed_out, uint64_t* words_out /* [ceil(m/64)] host */);
+/* Device time of the last phases (CUDA events on the context stream), ms:
+ * [0] bucketize [1] split searches [2] leaf searches [3] Rice stream
+ * [4] ribbon; split_evals = the reference's split `evals` counter summed. */
+int shk_build_phase_ms(shk_build* b, float* ms /* [5] */, int64_t* split_evals);
 int shk_build_destroy(shk_build* b);
 
 /* ---- MPHF evaluation (MphfDescriptor.query_hashed_many ->

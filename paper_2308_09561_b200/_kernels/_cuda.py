@@ -485,6 +485,13 @@ class GpuBuild:
               "ribbon")
         return int(seed.value), words
 
+    def phase_ms(self):
+        """Device ms of [bucketize, splits, leaves, rice, ribbon] + split evals."""
+        ms = (ctypes.c_float * 5)()
+        ev = ctypes.c_int64(0)
+        check(_L().shk_build_phase_ms(self.handle, ms, ctypes.byref(ev)))
+        return [float(x) for x in ms], int(ev.value)
+
     def close(self):
         if self.handle is not None and _lib._lib is not None:
             _lib._lib.shk_build_destroy(self.handle)

@@ -584,25 +584,45 @@ int shk_blake2b128(shk_ctx* c, const uint8_t* blob, int64_t blob_len, const int6
   DBuf tb(c), to(c), th(c), tl(c);
   const void *db, *doff;
   void *dh, *dl;
+  // Fixed-length fast path when every key has the same length (host offsets):
+  // the offsets need not cross PCIe at all.
+  int64_t L0 = 0;
+  if (!(flags & SHK_DEVICE) && off[0] == 0 && blob_len == off[N]) {
+    L0 = off[1] - off[0];
+    if (L0 < 1 || L0 > 128 || L0 * N != blob_len) L0 = 0;
+    for (int64_t i = 0; i < N && L0; ++i)
+      if (off[i + 1] - off[i] != L0) L0 = 0;
+  }
   RC(stage_in(c, flags, blob, (size_t)(blob_len > 0 ? blob_len : 1), tb, &db));
-  RC(stage_in(c, flags, off, (size_t)(N + 1) * 8, to, &doff));
   RC(stage_out(c, flags, hi, (size_t)N * 8, th, &dh));
   RC(stage_out(c, flags, lo, (size_t)N * 8, tl, &dl));
-  // Fixed-length fast path when every key has the same length (host offsets).
-  int fixed = 0;
-  if (!(flags & SHK_DEVICE) && off[0] == 0 && blob_len == off[N] && N > 0) {
-    int64_t L0 = off[1] - off[0];
-    if (L0 >= 1 && L0 <= 128 && L0 * N == blob_len) {
-      fixed = 1;
-      for (int64_t i = 0; i < N && fixed; ++i)
-        if (off[i + 1] - off[i] != L0) fixed = 0;
-      if (fixed)
-        RC(shk_launch_blake2b_fixed((const uint8_t*)db, (int)L0, N, salt, (uint64_t*)dh, (uint64_t*)dl, c->stream));
-    }
-  }
-  if (!fixed)
+  if (L0) {
+    RC(shk_launch_blake2b_fixed((const uint8_t*)db, (int)L0, N, salt, (uint64_t*)dh, (uint64_t*)dl, c->stream));
+  } else {
+    RC(stage_in(c, flags, off, (size_t)(N + 1) * 8, to, &doff));
     RC(shk_launch_blake2b((const uint8_t*)db, (const int64_t*)doff, N, salt, (uint64_t*)dh, (uint64_t*)dl,
                           c->stream));
+  }
+  RC(finish_out(c, flags, hi, th, (size_t)N * 8));
+  RC(finish_out(c, flags, lo, tl, (size_t)N * 8));
+  if (!(flags & SHK_DEVICE)) RC(csync(c));
+  return 0;
+}
+
+int shk_blake2b128_fixed(shk_ctx* c, const uint8_t* blob, int key_len, int64_t N, uint64_t salt, uint64_t* hi,
+                         uint64_t* lo, int flags) {
+  if (N <= 0) return 0;
+  if (key_len < 1 || key_len > 128) {
+    shk_set_error("fixed-length keys must be 1..128 bytes");
+    return SHK_INVALID;
+  }
+  DBuf tb(c), th(c), tl(c);
+  const void* db;
+  void *dh, *dl;
+  RC(stage_in(c, flags, blob, (size_t)key_len * N, tb, &db));
+  RC(stage_out(c, flags, hi, (size_t)N * 8, th, &dh));
+  RC(stage_out(c, flags, lo, (size_t)N * 8, tl, &dl));
+  RC(shk_launch_blake2b_fixed((const uint8_t*)db, key_len, N, salt, (uint64_t*)dh, (uint64_t*)dl, c->stream));
   RC(finish_out(c, flags, hi, th, (size_t)N * 8));
   RC(finish_out(c, flags, lo, tl, (size_t)N * 8));
   if (!(flags & SHK_DEVICE)) RC(csync(c));
@@ -714,8 +734,27 @@ struct shk_build {
   bool ran = false;
   bool record = false;
   DBuf place;
+  // phase timing (CUDA events on the context stream): 0 bucketize, 1 splits,
+  // 2 leaves, 3 rice, 4 ribbon (last run)
+  cudaEvent_t ev[12] = {};
+  float phase_ms[6] = {0, 0, 0, 0, 0, 0};
+  int64_t split_evals = 0;
   explicit shk_build(shk_ctx* ctx)
       : c(ctx), keys(ctx), tmp(ctx), prefix(ctx), choice(ctx), words(ctx), place(ctx) {}
+  ~shk_build() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  void mark(int i) {
+    if (!ev[i]) cudaEventCreate(&ev[i]);
+    cudaEventRecord(ev[i], c->stream);
+  }
+  float span(int a, int z) {
+    float ms = 0;
+    if (ev[a] && ev[z] && cudaEventElapsedTime(&ms, ev[a], ev[z]) == cudaSuccess) return ms;
+    cudaGetLastError();
+    return 0;
+  }
 };
 
 __global__ void gather_bitoff_kernel(const int64_t* pos, const int64_t* node_base, int64_t nb, uint64_t* out) {
@@ -763,6 +802,7 @@ int shk_build_create(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
     size_t ss = shk_bucketize_scratch(N, nbuckets);
     if ((rc = scratch.alloc(ss))) break;
     int* ddup = c->d_counter + 3;
+    b->mark(0);
     if ((rc = shk_bucketize((const uint64_t*)dh, (const uint64_t*)dl, N, nbuckets, b->keys.as<uint64_t>(),
                             b->prefix.as<uint64_t>(), ddup, scratch.p, ss, &b->max_bucket, c->stream)))
       break;
@@ -770,7 +810,9 @@ int shk_build_create(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
     if ((rc = d2h(c, b->h_prefix.data(), b->prefix.p, (size_t)(nbuckets + 1) * 8))) break;
     int hd = 0;
     if ((rc = d2h(c, &hd, ddup, 4))) break;
+    b->mark(1);
     if ((rc = csync(c))) break;
+    b->phase_ms[0] = b->span(0, 1);
     *dup = hd;
     if (max_bucket) *max_bucket = b->max_bucket;
   } while (0);
@@ -900,6 +942,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   int* exh = c->d_counter + 4;
   SHK_CUDA(cudaMemsetAsync(exh, 0, 4, c->stream));
   // ---- splits, level by level (every node of one depth in one launch)
+  b->mark(2);
   {
     size_t o = 0;
     for (auto& v : tasks) {
@@ -916,12 +959,14 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
         p.num_sms = c->num_sms;
         p.partition = 1;
         p.exhausted = exh;
+        p.evals_acc = dacc.as<unsigned long long>() + 6;
         RC(shk_launch_split(p, c->stream));
       }
       o += v.size();
     }
   }
   // ---- leaves
+  b->mark(3);
   if (L > 0) {
     ShkLeafLaunch p{};
     p.hi = b->keys.as<uint64_t>();
@@ -950,6 +995,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     }
     RC(shk_launch_leaf_search(p, c->stream));
   }
+  b->mark(4);
   int hex = 0;
   RC(d2h(c, &hex, exh, 4));
   RC(csync(c));
@@ -987,7 +1033,12 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   RC(d2h(c, b->bit_off.data(), dbo.p, (size_t)(nbr + 1) * 8));
   unsigned long long acc[8];
   RC(d2h(c, acc, dacc.p, 64));
+  b->mark(5);
   RC(csync(c));
+  b->phase_ms[1] = b->span(2, 3);
+  b->phase_ms[2] = b->span(3, 4);
+  b->phase_ms[3] = b->span(4, 5);
+  b->split_evals = (int64_t)acc[6];
   if (stats_out) {
     stats_out[0] = (int64_t)acc[0];
     stats_out[1] = (int64_t)acc[1];
@@ -1059,9 +1110,19 @@ int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int6
   const int64_t nw = (m + 63) / 64;
   DBuf tw(c);
   RC(tw.alloc((size_t)nw * 8));
+  b->mark(6);
   RC(ribbon_seed_loop(c, b->keys.as<uint64_t>(), drhs, b->N, m, max_tries, seed_out, tw.as<uint64_t>()));
+  b->mark(7);
   RC(d2h(c, words_out, tw.p, (size_t)nw * 8));
-  return csync(c);
+  RC(csync(c));
+  b->phase_ms[4] = b->span(6, 7);
+  return 0;
+}
+
+int shk_build_phase_ms(shk_build* b, float* ms, int64_t* split_evals) {
+  for (int i = 0; i < 5; ++i) ms[i] = b->phase_ms[i];
+  if (split_evals) *split_evals = b->split_evals;
+  return 0;
 }
 
 int shk_build_destroy(shk_build* b) {

@@ -58,6 +58,7 @@ struct ShkSplitLaunch {
   int num_sms;
   int partition;  // 1: stable-partition keys after the search
   int* exhausted; // optional flag: a node had no seed below max_seed
+  unsigned long long* evals_acc;  // optional running total of split evals
 };
 int shk_launch_split(const ShkSplitLaunch& p, cudaStream_t st);
 

@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(256) split_kernel(ShkSplitLaunch a) {
       a.seeds[task.seed_slot] = seed;
       if (a.evals_out) a.evals_out[t] = (int64_t)evals;
       if (seed < 0 && a.exhausted) atomicOr(a.exhausted, 1);
+      if (a.evals_acc) atomicAdd(a.evals_acc, (unsigned long long)evals);
     }
     if (seed < 0 || !a.partition) continue;
     // Stable partition by part (recsplit.py:558-561), via tmp, in place.

@@ -1,0 +1,90 @@
+"""GPU-resident data for the hot path (benchmarks, zero-copy pipelines).
+
+Device memory comes from the C-ABI context's caching pool; kernels run on the
+context stream; ``timer`` brackets device work with CUDA events recorded on
+that same stream (the stream the kernels are launched on).
+"""
+
+import ctypes
+
+import numpy as np
+
+from ._kernels import _lib
+from ._kernels._lib import SHK_DEVICE, check, ctx
+
+
+class DeviceBuffer:
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        p = ctypes.c_void_p()
+        check(_lib.load_library().shk_dev_alloc(ctx(), max(self.nbytes, 1), ctypes.byref(p)), "device alloc")
+        self.ptr = p.value
+
+    @classmethod
+    def from_host(cls, a: np.ndarray) -> "DeviceBuffer":
+        a = np.ascontiguousarray(a)
+        b = cls(a.nbytes)
+        b.upload(a)
+        return b
+
+    def upload(self, a: np.ndarray):
+        a = np.ascontiguousarray(a)
+        check(_lib.load_library().shk_memcpy(ctx(), self.ptr, a.ctypes.data, a.nbytes, 0), "H2D")
+
+    def download(self, dtype, count) -> np.ndarray:
+        out = np.empty(count, dtype=dtype)
+        check(_lib.load_library().shk_memcpy(ctx(), out.ctypes.data, self.ptr, out.nbytes, 1), "D2H")
+        return out
+
+    def free(self):
+        if self.ptr and _lib._lib is not None:
+            _lib._lib.shk_dev_free(ctx(), self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def sync():
+    check(_lib.load_library().shk_ctx_sync(ctx()), "sync")
+
+
+class timer:
+    """CUDA-event timing on the context stream: ``with timer() as t: ...; t.ms``."""
+
+    def __enter__(self):
+        check(_lib.load_library().shk_timer_start(ctx()))
+        return self
+
+    def __exit__(self, *exc):
+        ms = ctypes.c_float(0)
+        check(_lib.load_library().shk_timer_stop(ctx(), ctypes.byref(ms)))
+        self.ms = float(ms.value)
+        return False
+
+
+def launch_count() -> int:
+    return int(_lib.load_library().shk_launch_count(ctx()))
+
+
+def num_sms() -> int:
+    return int(_lib.load_library().shk_ctx_num_sms(ctx()))
+
+
+def blake2b_fixed_device(d_blob: DeviceBuffer, key_len: int, N: int, salt: int, d_hi: DeviceBuffer, d_lo: DeviceBuffer):
+    check(_lib.load_library().shk_blake2b128_fixed(ctx(), d_blob.ptr, int(key_len), int(N), int(salt), d_hi.ptr,
+                                                   d_lo.ptr, SHK_DEVICE), "blake2b")
+
+
+def blake2b_fixed_host(blob: np.ndarray, key_len: int, salt: int = 0):
+    """Host buffers in, host codes out; H2D/D2H inside the call."""
+    blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    N = len(blob) // key_len
+    hi = np.empty(N, dtype=np.uint64)
+    lo = np.empty(N, dtype=np.uint64)
+    check(_lib.load_library().shk_blake2b128_fixed(ctx(), blob.ctypes.data, int(key_len), N, int(salt),
+                                                   hi.ctypes.data, lo.ctypes.data, 0), "blake2b")
+    return hi, lo

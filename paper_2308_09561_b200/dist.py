@@ -1,0 +1,142 @@
+"""Multi-GPU construction by bucket range.
+
+Buckets are independent, so rank r of W owns buckets
+[r*nb//W, (r+1)*nb//W).  Every rank fingerprints and bucket-sorts all keys
+(cheap, and it avoids an all-to-all), builds its range (splits, leaves,
+orientation, Rice stream), and one exchange joins the per-rank results:
+an all-gather of (stream bit length, stream words, per-bucket bit offsets,
+choice bits).  Concatenating the rank streams at their global bit offsets
+gives exactly the single-GPU stream (same preorder, same seeds), so the
+descriptor is bit-identical for any world size.  The ribbon is global (one
+system over all N keys) and is solved by rank 0.
+
+The host-side merge is plain numpy (``merge_streams``) so the N>1 logic is
+tested on CPU with the gloo backend; the collective goes through
+``torch.distributed`` (NCCL over NVLink on the GPU box).
+"""
+
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+
+def shard_range(nbuckets: int, rank: int, world: int) -> Tuple[int, int]:
+    return (nbuckets * rank) // world, (nbuckets * (rank + 1)) // world
+
+
+def or_bits_at(dst: np.ndarray, src: np.ndarray, bit_off: int, nbits: int) -> None:
+    """dst |= src (nbits LSB-first) placed at bit position bit_off."""
+    if nbits <= 0:
+        return
+    nw = (nbits + 63) // 64
+    src = np.asarray(src[:nw], dtype=np.uint64).copy()
+    tail = nbits & 63
+    if tail:
+        src[-1] &= np.uint64((1 << tail) - 1)
+    w0, sh = divmod(int(bit_off), 64)
+    if sh == 0:
+        dst[w0 : w0 + nw] |= src
+        return
+    s = np.uint64(sh)
+    dst[w0 : w0 + nw] |= src << s
+    hi = src >> np.uint64(64 - sh)
+    end = min(w0 + 1 + nw, len(dst))
+    dst[w0 + 1 : end] |= hi[: end - (w0 + 1)]
+
+
+def merge_streams(parts: Sequence[Tuple[np.ndarray, int, np.ndarray]]):
+    """Concatenate per-rank Rice streams (in bucket order).
+
+    parts[r] = (words, bit_len, rel_offsets[nb_r + 1]) with rel_offsets
+    relative to the rank's stream start.  Returns (words, bit_len,
+    bit_offsets[nb + 1]) of the whole descriptor."""
+    total = int(sum(int(p[1]) for p in parts))
+    out = np.zeros((total + 63) // 64, dtype=np.uint64)
+    offs: List[np.ndarray] = []
+    base = 0
+    for words, bit_len, rel in parts:
+        or_bits_at(out, words, base, int(bit_len))
+        rel = np.asarray(rel, dtype=np.uint64)
+        offs.append(rel[:-1] + np.uint64(base))
+        base += int(bit_len)
+    offs.append(np.asarray([base], dtype=np.uint64))
+    return out, total, np.concatenate(offs)
+
+
+def allgather_arrays(arr: np.ndarray, device=None) -> List[np.ndarray]:
+    """All-gather a 1-D numpy array of any length from every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size()
+    raw = np.ascontiguousarray(arr).view(np.uint8)
+    dev = device if device is not None else torch.device("cpu")
+    n = torch.tensor([raw.size], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes) if sizes else 0
+    buf = torch.zeros(max(mx, 1), dtype=torch.uint8, device=dev)
+    if raw.size:
+        buf[: raw.size] = torch.from_numpy(raw.copy()).to(dev)
+    outs = [torch.zeros(max(mx, 1), dtype=torch.uint8, device=dev) for _ in range(world)]
+    dist.all_gather(outs, buf)
+    return [o[:s].cpu().numpy().view(arr.dtype) for o, s in zip(outs, sizes)]
+
+
+def exchange_and_merge(words, bit_len, rel_offsets, choice_slice, device=None):
+    """The one exchange step: gather every rank's stream pieces and choice
+    bits; every rank returns (stream words, bit_len, bit_offsets, choice)."""
+    meta = np.asarray([int(bit_len)], dtype=np.int64)
+    all_meta = allgather_arrays(meta, device)
+    all_words = allgather_arrays(np.asarray(words, dtype=np.uint64), device)
+    all_rel = allgather_arrays(np.asarray(rel_offsets, dtype=np.uint64), device)
+    packed = np.packbits(np.asarray(choice_slice, dtype=np.uint8), bitorder="little")
+    all_choice = allgather_arrays(packed, device)
+    lens = allgather_arrays(np.asarray([len(choice_slice)], dtype=np.int64), device)
+    parts = [(w, int(m[0]), r) for w, m, r in zip(all_words, all_meta, all_rel)]
+    sw, bl, bo = merge_streams(parts)
+    choice = np.concatenate([np.unpackbits(c, bitorder="little")[: int(n[0])] for c, n in zip(all_choice, lens)])
+    return sw, bl, bo, choice
+
+
+def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8, epsilon=0.05, device=None):
+    """Bucket-range-sharded build over the current torch.distributed group.
+
+    Returns the descriptor on rank 0 (None elsewhere) and this rank's
+    device-time profile."""
+    import time
+
+    import torch.distributed as dist
+
+    from . import recsplit, retrieval
+    from . import shockhash as leaf_mod
+    from ._kernels import kernels as K
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    t0 = time.perf_counter()
+    nb = (n_keys + b - 1) // b
+    gb = K.GpuBuild(None, None, nb, hi_ptr=hi_ptr, lo_ptr=lo_ptr, n=n_keys)
+    if gb.duplicate:
+        raise recsplit.HashCollisionError("equal 128-bit codes in the input")
+    key_prefix = gb.key_prefix()
+    b0, b1 = shard_range(nb, rank, world)
+    leaf_g = recsplit.leaf_g_table(n)
+    sizes = np.unique(np.diff(key_prefix[b0 : b1 + 1].astype(np.int64)))
+    plans = recsplit.plans_for_sizes(sizes, n, leaf_g)
+    ck = cache_k if mode == leaf_mod.MODE_ROTATE_CACHED else 0
+    gb.run(plans, 0 if mode == leaf_mod.MODE_PLAIN else 1, ck, leaf_mod.CACHE_MIN_LEAF, b0, b1, leaf_mod.MAX_SEED)
+    words, bit_len, bo = gb.stream()
+    rel = bo[: b1 - b0 + 1]
+    choice = gb.choice()[int(key_prefix[b0]) : int(key_prefix[b1])]
+    sw, bl, bit_offsets, choice_all = exchange_and_merge(words, bit_len, rel, choice, device)
+    desc = None
+    if rank == 0:
+        m = retrieval._columns(n_keys, epsilon)
+        rseed, rwords = gb.ribbon(m, retrieval.RETRY_CAP, choice=choice_all)
+        ribbon = retrieval.RibbonSystem(epsilon, rseed, m, rwords)
+        desc = recsplit.MphfDescriptor(n_keys, b, n, mode, cache_k, 0, leaf_g, key_prefix, bit_offsets, sw, bl, ribbon)
+        desc.build_stats = {"build_seconds": time.perf_counter() - t0}
+    phase, split_evals = gb.phase_ms()
+    gb.close()
+    return desc, {"phase_ms": phase, "split_evals": split_evals, "buckets": (b0, b1)}

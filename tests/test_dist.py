@@ -1,0 +1,100 @@
+"""Multi-GPU construction logic (bucket-range sharding + one exchange) on
+CPU: the merge is checked against the oracle's single-process stream, and
+the exchange runs with torch.distributed gloo at world_size 2."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle.host as OH
+
+
+def sub_stream(words, a, b):
+    """Bits [a, b) of an LSB-first word stream as a new word array."""
+    nbits = b - a
+    nw = (nbits + 63) // 64
+    out = np.zeros(nw, dtype=np.uint64)
+    for i in range(nw):
+        pos = a + 64 * i
+        w, sh = divmod(pos, 64)
+        v = int(words[w]) >> sh if w < len(words) else 0
+        if sh and w + 1 < len(words):
+            v |= (int(words[w + 1]) << (64 - sh)) & ((1 << 64) - 1)
+        take = min(64, b - pos)
+        out[i] = v & ((1 << take) - 1)
+    return out
+
+
+@pytest.fixture(scope="module")
+def c2_parts():
+    from paper_2308_09561_b200 import workloads as W
+
+    keys = W.keys_as_bytes(W.build_keys(2))
+    hi, lo = W.blake2b_host(keys, 0)
+    blob, res = OH.build_descriptor(hi, lo, 500, 24)
+    return res
+
+
+def rank_part(res, r, world):
+    from paper_2308_09561_b200.dist import shard_range
+
+    nb = len(res["key_prefix"]) - 1
+    b0, b1 = shard_range(nb, r, world)
+    bo = res["bit_offsets"].astype(np.int64)
+    a, b = int(bo[b0]), int(bo[b1])
+    words = sub_stream(res["words"], a, b)
+    rel = (bo[b0 : b1 + 1] - a).astype(np.uint64)
+    kp = res["key_prefix"].astype(np.int64)
+    return words, b - a, rel, res["choice"][kp[b0] : kp[b1]]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_merge_streams_reassembles(c2_parts, world):
+    from paper_2308_09561_b200.dist import merge_streams
+
+    res = c2_parts
+    parts = [rank_part(res, r, world)[:3] for r in range(world)]
+    words, bl, bo = merge_streams(parts)
+    assert bl == res["bit_len"]
+    assert (words == res["words"]).all()
+    assert (bo == res["bit_offsets"]).all()
+
+
+def _worker(rank, world, port, res, q):
+    import torch.distributed as dist
+
+    from paper_2308_09561_b200.dist import exchange_and_merge
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        words, bl, rel, choice = rank_part(res, rank, world)
+        sw, b2, bo, ch = exchange_and_merge(words, bl, rel, choice)
+        ok = (b2 == res["bit_len"] and (sw == res["words"]).all() and (bo == res["bit_offsets"]).all()
+              and (ch == res["choice"]).all())
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_exchange(c2_parts):
+    import socket
+
+    import torch.multiprocessing as tmp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    res = {k: c2_parts[k] for k in ("key_prefix", "bit_offsets", "words", "bit_len", "choice")}
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, res, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    out = dict(q.get(timeout=5) for _ in range(2))
+    assert out == {0: True, 1: True}

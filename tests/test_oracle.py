@@ -1,0 +1,153 @@
+"""Pin the CPU oracle (oracle/shk_oracle.c) against the reference's golden
+vectors.  CPU only; these make the oracle a trustworthy checker for the
+GPU parity tests."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+import oracle.host as OH
+from conftest import golden
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def synthetic_hashed(count, gen_seed):
+    # keys.py:102-112 recipe (test input generator)
+    base = np.uint64(OH._mix64_np(np.asarray([gen_seed], dtype=np.uint64))[0] ^ np.uint64(0x5851F42D4C957F2D))
+    idx = np.arange(count, dtype=np.uint64)
+    return OH._mix64_np(base + np.uint64(2) * idx), OH._mix64_np(base + np.uint64(2) * idx + np.uint64(1))
+
+
+def test_mix64_kat():
+    # test_keys.py:33-39 (SplitMix64 reference sequence)
+    assert oracle.mix64(0x9E3779B97F4A7C15) == 0xE220A8397B1DCDAF
+    assert oracle.mix64((2 * 0x9E3779B97F4A7C15) % 2**64) == 0x6E789E6AA1B965F4
+    assert oracle.mix64((3 * 0x9E3779B97F4A7C15) % 2**64) == 0x06C45D188009454F
+
+
+def test_scalar_golden():
+    g = golden("kat.json")
+    for r in g["scalars"]:
+        assert oracle.mix64(r["hi"]) == r["mix64"]
+        assert oracle.seed_mixer(r["s"], r["tag"]) == r["seed_mixer"]
+        assert oracle.remix(r["hi"], r["lo"], r["s"], r["tag"]) == r["remix"]
+        assert oracle.hash_range(r["hi"], r["n"]) == r["hash_range"]
+        assert list(oracle.leaf_pair(r["hi"], r["lo"], r["s"], r["n"])) == r["leaf_pair"]
+        assert oracle.split_bit(r["hi"], r["lo"], r["s"]) == r["split_bit"]
+    for r in g["leaf_cell"]:
+        assert oracle.leaf_cell(r["hi"], r["lo"], r["q"], r["n"], r["mode"], r["ck"], r["choice"]) == r["cell"]
+
+
+@pytest.mark.parametrize("which", ["plain", "rotate", "rotate_cached"])
+def test_leaf_golden(which):
+    for r in golden("leaves.json"):
+        n, e = r["n"], r[which]
+        if which == "plain":
+            t = oracle.search_plain(r["hi"], r["lo"], n, 1 << 40)
+            edges = oracle.edges_plain(r["hi"], r["lo"], t[0], n)
+        else:
+            ck = 0 if which == "rotate" else e["ck"]
+            t = oracle.search_rotate(r["hi"], r["lo"], n, ck, 1 << 40)
+            edges = oracle.edges_rotate(r["hi"], r["lo"], t[0], n, ck)
+        assert list(t) == e["stats"]
+        assert oracle.orient(edges, n) == e["fbits"]
+
+
+def test_c1_golden():
+    from paper_2308_09561_b200 import workloads as W
+
+    g = golden("c1.json")
+    hi, lo = W.leaf_inputs(1)
+    seeds = oracle.search_plain_batch(hi, lo)
+    assert int(seeds.sum()) == g["sum_seed"] == 64870  # SURVEY.md App. B anchor
+    assert seeds.tolist() == g["seeds"]
+    fb = [oracle.orient(oracle.edges_plain(hi[i], lo[i], int(seeds[i]), 16), 16) for i in range(len(seeds))]
+    assert fb == g["fbits"]
+    assert sha(seeds.astype("<i8").tobytes() + np.asarray(fb, dtype="<u8").tobytes())[:16] == g["sha16"]
+
+
+def test_c3_sample_golden():
+    from paper_2308_09561_b200 import workloads as W
+
+    g = golden("c3.json")
+    hi, lo = W.leaf_inputs(3, 500)
+    seeds = oracle.search_plain_batch(hi, lo)
+    assert seeds.tolist() == g["seeds"][:500]
+
+
+def test_c5_sample_golden():
+    g = golden("c5.json")
+    rng = np.random.default_rng(5)
+    fp = rng.integers(0, 2**64, (20000, 56, 2), dtype=np.uint64)[:4]
+    seeds = oracle.search_plain_batch(np.ascontiguousarray(fp[..., 0]), np.ascontiguousarray(fp[..., 1]))
+    assert seeds.tolist() == g["seeds"][:4]
+
+
+def test_split_golden():
+    for r in golden("split.json")["cases"]:
+        hi, lo = synthetic_hashed(r["m"], r["gen"])
+        assert oracle.split_seed_search(hi, lo, r["sizes"], 1 << 30) == (r["seed"], r["evals"])
+        parts = oracle.split_parts(hi, lo, r["seed"], r["sizes"])
+        assert sha(parts.astype("<i8").tobytes()) == r["parts_sha"]
+        assert OH.split_rice_param(r["m"], tuple(r["sizes"])) == r["g"]
+    assert [OH.leaf_rice_param(m) for m in range(65)] == golden("split.json")["leaf_g"]
+
+
+def test_ribbon_golden():
+    for r in golden("ribbon.json"):
+        N, m, seed = r["N"], r["m"], r["seed"]
+        rng = np.random.default_rng(N)
+        hi, lo = synthetic_hashed(N, r["gen"])
+        rhs = rng.integers(0, 2, N).astype(np.uint8)
+        st, p0, p1 = oracle.ribbon_rows(hi, lo, seed, m)
+        assert sha(st.astype("<i8").tobytes() + p0.astype("<u8").tobytes() + p1.astype("<u8").tobytes()) == r["rows_sha"]
+        w = oracle.ribbon_solve(st, p0, p1, rhs, m)
+        assert (w is not None) == r["solvable"]
+        if w is not None:
+            assert sha(w.astype("<u8").tobytes()) == r["words_sha"]
+            assert (oracle.ribbon_query(st, p0, p1, w, m) == rhs).all()
+
+
+def test_rice_golden():
+    g = golden("rice.json")
+    pos = 0
+    for v, gg in g["items"]:
+        x, pos = oracle.rice_decode(g["words"], g["bit_len"], pos, gg)
+        assert x == v
+    assert pos == g["bit_len"]
+
+
+def test_c2_full_build_golden():
+    """C2 end to end on the oracle: identical descriptor bytes and 1e6 queries."""
+    from paper_2308_09561_b200 import workloads as W
+
+    g = golden("c2.json")
+    keys = W.keys_as_bytes(W.build_keys(2))
+    hi, lo = W.blake2b_host(keys, 0)
+    blob, res = OH.build_descriptor(hi, lo, 500, 24)
+    assert sha(blob) == g["desc_sha"]
+    with open("tests/golden/c2_desc.bin", "rb") as f:
+        assert blob == f.read()
+    idx = W.query_indices(2)
+    out = OH.query(res, 24, 1, 8, hi[idx], lo[idx])
+    assert sha(out.astype("<u8").tobytes()) == g["query_sha"]
+
+
+def test_small_builds_golden():
+    from paper_2308_09561_b200 import workloads as W
+    from paper_2308_09561_b200.keys import synthetic_keys
+
+    for r in golden("builds.json"):
+        if r.get("hashed"):
+            hi, lo = synthetic_hashed(r["N"], r["gen"])
+        else:
+            hi, lo = W.blake2b_host(synthetic_keys(r["N"], r["gen"]), 0)
+        blob, res = OH.build_descriptor(hi, lo, r["b"], r["n"], r["mode"])
+        assert sha(blob) == r["desc_sha"], r
+        out = OH.query(res, r["n"], r["mode"], 8, hi, lo)
+        assert sha(out.astype("<u8").tobytes()) == r["query_sha"], r
