@@ -204,6 +204,13 @@ def run_ours(args):
         prof["phase_ms"] = dict(zip(("bucketize", "split_search", "leaf_search", "rice", "ribbon"), prof["phase_ms"]))
         return d, prof
 
+    # One untimed instrumented build counts the reference's split `evals`
+    # (algorithmic work of the split searches; the timed builds run the
+    # verdict-only search, identical seeds).
+    dev.set_option(dev.OPT_EXACT_SPLIT_EVALS, 1)
+    _, prof_exact = step()
+    dev.set_option(dev.OPT_EXACT_SPLIT_EVALS, 0)
+    split_evals_exact = prof_exact["split_evals"]
     for _ in range(args.warmup):
         desc, prof = step()
     parity = {}
@@ -259,7 +266,8 @@ def run_ours(args):
 
     if rank != 0:
         return
-    prof = profs[-1]
+    prof = dict(profs[-1])
+    prof["split_evals"] = split_evals_exact
     hash_evals = desc.build_stats.get("hash_evals") if desc.build_stats else None
     clocks = clk.summary()
     line = {

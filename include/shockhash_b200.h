@@ -56,6 +56,12 @@ int shk_ctx_sync(shk_ctx* ctx);
 void* shk_ctx_stream(shk_ctx* ctx);
 int shk_ctx_set_stream(shk_ctx* ctx, void* stream);
 int shk_ctx_num_sms(shk_ctx* ctx);
+/* Tuning / instrumentation options of a context. */
+enum {
+  SHK_OPT_EXACT_SPLIT_EVALS = 0, /* 1: builds also count the reference's split `evals` (slower) */
+  SHK_OPT_LEAF_TEAM_WARPS = 1    /* warps per leaf in builds (0 = heuristic) */
+};
+int shk_ctx_set_option(shk_ctx* ctx, int opt, int64_t value);
 /* Device memory from the context's caching pool (bench / zero-copy users). */
 int shk_dev_alloc(shk_ctx* ctx, size_t bytes, void** out);
 int shk_dev_free(shk_ctx* ctx, void* p);

@@ -61,6 +61,7 @@ _SIGS = {
     "shk_ctx_stream": (_P, [_P]),
     "shk_ctx_set_stream": (_I, [_P, _P]),
     "shk_ctx_num_sms": (_I, [_P]),
+    "shk_ctx_set_option": (_I, [_P, _I, _I64]),
     "shk_dev_alloc": (_I, [_P, ctypes.c_size_t, _P]),
     "shk_dev_free": (_I, [_P, _P]),
     "shk_memcpy": (_I, [_P, _P, _P, ctypes.c_size_t, _I]),

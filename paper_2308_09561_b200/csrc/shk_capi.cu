@@ -54,6 +54,7 @@ struct shk_ctx {
   int* d_counter = nullptr;  // scratch ints: [0] counter [1] flag [2] flag
   ShkRibbon* rib = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  int64_t opt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // shk_ctx_set_option
 };
 
 static size_t round_up(size_t b) {
@@ -228,6 +229,14 @@ int shk_ctx_set_stream(shk_ctx* c, void* s) {
   return 0;
 }
 int shk_ctx_num_sms(shk_ctx* c) { return c->num_sms; }
+int shk_ctx_set_option(shk_ctx* c, int opt, int64_t value) {
+  if (opt < 0 || opt >= 8) {
+    shk_set_error("unknown option %d", opt);
+    return SHK_INVALID;
+  }
+  c->opt[opt] = value;
+  return 0;
+}
 
 int shk_dev_alloc(shk_ctx* c, size_t bytes, void** out) { return pool_alloc(c, bytes, out); }
 int shk_dev_free(shk_ctx* c, void* p) {
@@ -413,6 +422,7 @@ int shk_split_search(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
   p.counter = c->d_counter;
   p.num_sms = c->num_sms;
   p.partition = 0;
+  p.exact_evals = 1;
   RC(shk_launch_split(p, c->stream));
   RC(d2h(c, seed_out, seeds.p, 8));
   RC(d2h(c, evals_out, ev.p, 8));
@@ -960,6 +970,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
         p.partition = 1;
         p.exhausted = exh;
         p.evals_acc = dacc.as<unsigned long long>() + 6;
+        p.exact_evals = c->opt[SHK_OPT_EXACT_SPLIT_EVALS] ? 1 : 0;
         RC(shk_launch_split(p, c->stream));
       }
       o += v.size();
@@ -989,6 +1000,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     p.error = c->d_counter + 1;
     p.exhausted = exh;
     p.num_sms = c->num_sms;
+    p.team_warps = (int)c->opt[SHK_OPT_LEAF_TEAM_WARPS];
     if (b->record) {
       RC(b->place.alloc((size_t)b->N * 8));
       p.place_out = b->place.as<int64_t>();

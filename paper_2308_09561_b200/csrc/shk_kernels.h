@@ -59,6 +59,7 @@ struct ShkSplitLaunch {
   int partition;  // 1: stable-partition keys after the search
   int* exhausted; // optional flag: a node had no seed below max_seed
   unsigned long long* evals_acc;  // optional running total of split evals
+  int exact_evals;  // 1: track the reference's exact `evals` (seam API); 0: fast verdict-only search
 };
 int shk_launch_split(const ShkSplitLaunch& p, cudaStream_t st);
 

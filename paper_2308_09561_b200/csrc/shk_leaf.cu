@@ -58,12 +58,14 @@ struct LeafSmem {
   int64_t leaf;
 };
 
+// A CTA holds TEAMS independent teams of TW warps; a team synchronizes on
+// its own named barrier (id team+1), so teams never wait for each other.
 template <int TW>
-SHK_D void team_sync() {
+SHK_D void team_sync(int team) {
   if (TW == 1)
     __syncwarp();
   else
-    __syncthreads();
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TW * 32) : "memory");
 }
 
 // -------------------------------------------------------------------------
@@ -98,25 +100,28 @@ SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e, bo
   }
 }
 
-template <int TW, bool WIDE>
-__global__ void __launch_bounds__(TW * 32) leaf_plain_kernel(LeafArgs a) {
-  __shared__ LeafSmem<TW> sm;
+template <int TW, int TEAMS, bool WIDE>
+__global__ void __launch_bounds__(TW * 32 * TEAMS) leaf_plain_kernel(LeafArgs a) {
+  __shared__ LeafSmem<TW> sm_all[TEAMS];
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int team = (threadIdx.x >> 5) / TW;
+  const int warp = (threadIdx.x >> 5) % TW;  // warp within the team
+  const int tt = threadIdx.x - team * TW * 32;
+  LeafSmem<TW>& sm = sm_all[team];
   uint16_t* e = &sm.edges[warp][lane];
   const bool store = true;
   for (;;) {
-    if (threadIdx.x == 0) sm.leaf = atomicAdd(a.counter, 1);
-    __syncthreads();
+    if (tt == 0) sm.leaf = atomicAdd(a.counter, 1);
+    team_sync<TW>(team);
     const int64_t leaf = sm.leaf;
     if (leaf >= a.L) break;
     const int64_t k0 = a.off[leaf];
     const int n = (int)(a.off[leaf + 1] - k0);
-    for (int i = threadIdx.x; i < n; i += TW * 32) {
+    for (int i = tt; i < n; i += TW * 32) {
       u2 h = split64(a.hi[(k0 + i) * a.stride]), l = split64(a.lo[(k0 + i) * a.stride]);
       sm.keys[i] = make_uint4(h.lo, h.hi, l.lo, l.hi);
     }
-    __syncthreads();
+    team_sync<TW>(team);
     int64_t seed = -1;
     uint64_t passes = 0;
     if (n <= 1) {
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(TW * 32) leaf_plain_kernel(LeafArgs a) {
           sm.slot_pass_le[par][warp] = __popc(le);
           sm.slot_pass[par][warp] = __popc(pb);
         }
-        team_sync<TW>();
+        team_sync<TW>(team);
         int64_t win = -1;
         uint64_t round_pass = 0;
 #pragma unroll
@@ -207,31 +212,34 @@ __global__ void __launch_bounds__(TW * 32) leaf_plain_kernel(LeafArgs a) {
         if (seed < 0 && a.exhausted) atomicOr(a.exhausted, 1);
       }
     }
-    __syncthreads();
+    team_sync<TW>(team);
   }
 }
 
 // -------------------------------------------------------------------------
 // Rotation fitting: lane per base seed.
-template <int TW, bool WIDE>
-__global__ void __launch_bounds__(TW * 32) leaf_rotate_kernel(LeafArgs a) {
-  __shared__ LeafSmem<TW> sm;
+template <int TW, int TEAMS, bool WIDE>
+__global__ void __launch_bounds__(TW * 32 * TEAMS) leaf_rotate_kernel(LeafArgs a) {
+  __shared__ LeafSmem<TW> sm_all[TEAMS];
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int team = (threadIdx.x >> 5) / TW;
+  const int warp = (threadIdx.x >> 5) % TW;  // warp within the team
+  const int tt = threadIdx.x - team * TW * 32;
+  LeafSmem<TW>& sm = sm_all[team];
   uint16_t* e = &sm.edges[warp][lane];
   for (;;) {
-    if (threadIdx.x == 0) sm.leaf = atomicAdd(a.counter, 1);
-    __syncthreads();
+    if (tt == 0) sm.leaf = atomicAdd(a.counter, 1);
+    team_sync<TW>(team);
     const int64_t leaf = sm.leaf;
     if (leaf >= a.L) break;
     const int64_t k0 = a.off[leaf];
     const int n = (int)(a.off[leaf + 1] - k0);
     const int64_t ck = (n > a.cache_min_leaf) ? a.cache_k : 0;
-    for (int i = threadIdx.x; i < n; i += TW * 32) {
+    for (int i = tt; i < n; i += TW * 32) {
       u2 h = split64(a.hi[(k0 + i) * a.stride]), l = split64(a.lo[(k0 + i) * a.stride]);
       sm.keys[i] = make_uint4(h.lo, h.hi, l.lo, l.hi);
     }
-    __syncthreads();
+    team_sync<TW>(team);
     int64_t q = -1;
     uint64_t passes = 0, evals = 0, aev = 0;
     if (n <= 1) {
@@ -339,7 +347,7 @@ __global__ void __launch_bounds__(TW * 32) leaf_rotate_kernel(LeafArgs a) {
           sm.slot_aev_le[par][warp] = c_aev_le;
           sm.slot_aev[par][warp] = t_aev;
         }
-        team_sync<TW>();
+        team_sync<TW>(team);
         int64_t winb = -1;
         int winr = 0;
 #pragma unroll
@@ -418,7 +426,7 @@ __global__ void __launch_bounds__(TW * 32) leaf_rotate_kernel(LeafArgs a) {
         if (q < 0 && a.exhausted) atomicOr(a.exhausted, 1);
       }
     }
-    __syncthreads();
+    team_sync<TW>(team);
   }
 }
 
@@ -485,27 +493,29 @@ int shk_launch_leaf_search(const ShkLeafLaunch& p, cudaStream_t st) {
     if (p.mode == 0)
       tw = p.max_n <= 24 ? 1 : (p.max_n <= 40 ? 4 : 8);
     else
-      tw = p.max_n <= 24 ? 1 : 2;
+      tw = p.max_n <= 24 ? 1 : 1;
   }
   int occ = 0;
-#define SHK_LEAF_LAUNCH(TW)                                                                      \
+  // CTAs of 4 warps (TEAMS = 4 / TW independent teams; TW = 8 -> one team).
+#define SHK_LEAF_LAUNCH(TW, TEAMS)                                                               \
   do {                                                                                           \
     void (*kfn)(LeafArgs);                                                                       \
     if (p.mode == 0)                                                                             \
-      kfn = wide ? leaf_plain_kernel<TW, true> : leaf_plain_kernel<TW, false>;                   \
+      kfn = wide ? leaf_plain_kernel<TW, TEAMS, true> : leaf_plain_kernel<TW, TEAMS, false>;     \
     else                                                                                         \
-      kfn = wide ? leaf_rotate_kernel<TW, true> : leaf_rotate_kernel<TW, false>;                 \
-    SHK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, TW * 32, 0));             \
+      kfn = wide ? leaf_rotate_kernel<TW, TEAMS, true> : leaf_rotate_kernel<TW, TEAMS, false>;   \
+    SHK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, TW * 32 * TEAMS, 0));     \
     if (occ < 1) occ = 1;                                                                        \
     int64_t blocks = (int64_t)sms * occ;                                                         \
-    if (blocks > p.L) blocks = p.L;                                                              \
-    kfn<<<(unsigned)blocks, TW * 32, 0, st>>>(a);                                                \
+    int64_t need = (p.L + TEAMS - 1) / TEAMS;                                                    \
+    if (blocks > need) blocks = need;                                                            \
+    kfn<<<(unsigned)blocks, TW * 32 * TEAMS, 0, st>>>(a);                                        \
   } while (0)
   switch (tw) {
-    case 1: SHK_LEAF_LAUNCH(1); break;
-    case 2: SHK_LEAF_LAUNCH(2); break;
-    case 4: SHK_LEAF_LAUNCH(4); break;
-    case 8: SHK_LEAF_LAUNCH(8); break;
+    case 1: SHK_LEAF_LAUNCH(1, 4); break;
+    case 2: SHK_LEAF_LAUNCH(2, 2); break;
+    case 4: SHK_LEAF_LAUNCH(4, 1); break;
+    case 8: SHK_LEAF_LAUNCH(8, 1); break;
     default: shk_set_error("team_warps must be 1, 2, 4 or 8"); return 3;
   }
 #undef SHK_LEAF_LAUNCH

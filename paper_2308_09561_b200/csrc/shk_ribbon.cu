@@ -113,12 +113,21 @@ __global__ void ribbon_rows_scatter_kernel(const int64_t* starts, const uint64_t
 }
 
 // ---------------------------------------------------------------------------
-// Elimination pass: one CTA (one warp) per chunk with pending rows.
-// Slot state in global memory: sp0/sp1 per column, occ/rhs bitmaps per word.
+// Elimination pass: one warp per chunk with pending rows; all 32 lanes insert
+// rows concurrently.  Slot state (pivot row per column, occupancy and rhs
+// bitmaps) lives in shared memory for the pass and in global memory between
+// passes.  Lock-step protocol per iteration: (A) every lane reads the slot at
+// its row's current pivot column; __syncwarp; (B) a lane that saw the slot
+// occupied XORs the stored row into its own and moves to the next set bit; a
+// lane that saw it empty claims it with atomicOr on the occupancy word and,
+// if it won, stores its row there (same phase), else it retries next
+// iteration (then it sees the winner's row).  A set occupancy bit therefore
+// always refers to data written before the previous __syncwarp.  Any
+// insertion order yields the same final solution.
 __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const int64_t* row_off, int64_t nchunks,
                                                          int64_t m, uint64_t* sp0, uint64_t* sp1, uint32_t* occ,
                                                          uint32_t* sbit, RRow* ovf, int64_t* ovf_count,
-                                                         int* inconsistent) {
+                                                         int* inconsistent, int first_pass) {
   __shared__ uint64_t q0s[CE], q1s[CE];
   __shared__ uint32_t occs[CE / 32], sbs[CE / 32];
   const int64_t c = blockIdx.x;
@@ -128,79 +137,107 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
   const int lane = threadIdx.x;
   const int64_t base = c * CE;
   const int64_t cols = (m - base < CE) ? (m - base) : CE;
-  for (int j = lane; j < CE; j += 32) {
-    if (j < cols) {
-      q0s[j] = sp0[base + j];
-      q1s[j] = sp1[base + j];
-    } else {
-      q0s[j] = 0;
-      q1s[j] = 0;
+  const int64_t nrows = r1 - r0;
+  const int64_t wbase = base / 32;
+  if (first_pass) {  // slots start empty: no global state to load
+    for (int j = lane; j < CE / 32; j += 32) occs[j] = sbs[j] = 0;
+  } else {
+    for (int j = lane; j < CE; j += 32) {
+      const bool in = j < cols;
+      q0s[j] = in ? sp0[base + j] : 0;
+      q1s[j] = in ? sp1[base + j] : 0;
+    }
+    for (int j = lane; j < CE / 32; j += 32) {
+      const bool in = (j * 32) < cols;
+      occs[j] = in ? occ[wbase + j] : 0;
+      sbs[j] = in ? sbit[wbase + j] : 0;
     }
   }
-  const int64_t wbase = base / 32;
-  for (int j = lane; j < CE / 32; j += 32) {
-    bool in = (j * 32) < cols;
-    occs[j] = in ? occ[wbase + j] : 0;
-    sbs[j] = in ? sbit[wbase + j] : 0;
-  }
   __syncwarp();
-  if (lane == 0) {
-    bool bad = false;
-    for (int64_t ri = r0; ri < r1 && !bad; ++ri) {
-      RRow r = rows[ri];
-      uint64_t a0 = r.p0, a1 = r.p1;
-      uint32_t b = (r.s & RHS_BIT) ? 1u : 0u;
-      int64_t j = (r.s & S_MASK) - base;
-      for (;;) {
-        if (j >= CE) {
-          int64_t k = (int64_t)atomicAdd((unsigned long long*)ovf_count, 1ull);
-          RRow o;
-          o.p0 = a0;
-          o.p1 = a1;
-          o.s = (base + j) | (b ? RHS_BIT : 0);
-          ovf[k] = o;
-          break;
-        }
+  int64_t next = lane;
+  bool active = false, bad = false;
+  uint64_t a0 = 0, a1 = 0;
+  uint32_t b = 0;
+  int j = 0;
+  auto fetch = [&]() {
+    active = next < nrows;
+    if (active) {
+      const RRow r = rows[r0 + next];
+      next += 32;
+      a0 = r.p0;
+      a1 = r.p1;
+      b = (r.s & RHS_BIT) ? 1u : 0u;
+      j = (int)((r.s & S_MASK) - base);
+    }
+  };
+  fetch();
+  while (__any_sync(FULL_WARP, active)) {
+    // phase A: read the slot at the current pivot
+    const bool esc = active && j >= CE;
+    uint32_t w = 0, sw = 0;
+    uint64_t q0 = 0, q1 = 0;
+    if (active && !esc) {
+      w = occs[j >> 5];
+      sw = sbs[j >> 5];
+      q0 = q0s[j];
+      q1 = q1s[j];
+    }
+    __syncwarp();
+    // phase B: act
+    if (active) {
+      if (esc) {
+        const int64_t kk = (int64_t)atomicAdd((unsigned long long*)ovf_count, 1ull);
+        RRow o;
+        o.p0 = a0;
+        o.p1 = a1;
+        o.s = (base + j) | (b ? RHS_BIT : 0);
+        ovf[kk] = o;
+        fetch();
+      } else {
         const uint32_t bitm = 1u << (j & 31);
-        const uint32_t w = occs[j >> 5];
-        if (!(w & bitm)) {
-          occs[j >> 5] = w | bitm;
-          if (b) sbs[j >> 5] |= bitm;
-          q0s[j] = a0;
-          q1s[j] = a1;
-          break;
-        }
-        a0 ^= q0s[j];
-        a1 ^= q1s[j];
-        b ^= (sbs[j >> 5] >> (j & 31)) & 1u;
-        if ((a0 | a1) == 0) {
-          if (b) bad = true;
-          break;
-        }
-        int t;
-        if (a0) {
-          t = __ffsll((long long)a0) - 1;
-          a0 = (a0 >> t) | (t ? (a1 << (64 - t)) : 0);
-          a1 >>= t;
+        if (w & bitm) {
+          a0 ^= q0;
+          a1 ^= q1;
+          b ^= (sw >> (j & 31)) & 1u;
+          if ((a0 | a1) == 0) {
+            if (b) bad = true;
+            fetch();
+          } else {
+            int t;
+            if (a0) {
+              t = __ffsll((long long)a0) - 1;
+              a0 = (a0 >> t) | (t ? (a1 << (64 - t)) : 0);
+              a1 >>= t;
+            } else {
+              t = 63 + __ffsll((long long)a1);  // 64 + ctz(a1)
+              a0 = a1 >> (t - 64);
+              a1 = 0;
+            }
+            j += t;
+          }
         } else {
-          t = 63 + __ffsll((long long)a1);  // 64 + ctz(a1)
-          a0 = a1 >> (t - 64);
-          a1 = 0;
+          const uint32_t old = atomicOr(&occs[j >> 5], bitm);
+          if (!(old & bitm)) {
+            q0s[j] = a0;
+            q1s[j] = a1;
+            if (b) atomicOr(&sbs[j >> 5], bitm);
+            fetch();
+          }
         }
-        j += t;
       }
     }
-    if (bad) atomicOr(inconsistent, 1);
+    __syncwarp();
   }
+  if (__any_sync(FULL_WARP, bad) && lane == 0) atomicOr(inconsistent, 1);
   __syncwarp();
-  for (int j = lane; j < cols; j += 32) {
-    sp0[base + j] = q0s[j];
-    sp1[base + j] = q1s[j];
+  for (int jj = lane; jj < cols; jj += 32) {
+    sp0[base + jj] = q0s[jj];
+    sp1[base + jj] = q1s[jj];
   }
-  for (int j = lane; j < CE / 32; j += 32) {
-    if ((j * 32) < cols) {
-      occ[wbase + j] = occs[j];
-      sbit[wbase + j] = sbs[j];
+  for (int jj = lane; jj < CE / 32; jj += 32) {
+    if ((jj * 32) < cols) {
+      occ[wbase + jj] = occs[jj];
+      sbit[wbase + jj] = sbs[jj];
     }
   }
 }
@@ -309,12 +346,18 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
   }
 }
 
-// Final back substitution with the known right boundary: one thread per
-// back-chunk, 128-bit window, writes the chunk's solution words.
-__global__ void ribbon_final_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0, const uint64_t* sp1,
-                                    const uint32_t* occ, const uint32_t* sbit, const uint4* ybound, uint64_t* words) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Final back substitution with the known right boundary: one warp per
+// back-chunk; the warp stages 256-column tiles of pivot rows in shared memory
+// (coalesced) and lane 0 walks them right to left with a 128-bit window.
+__global__ void __launch_bounds__(32) ribbon_final_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
+                                                          const uint64_t* sp1, const uint32_t* occ,
+                                                          const uint32_t* sbit, const uint4* ybound,
+                                                          uint64_t* words) {
+  __shared__ uint64_t tp0[256], tp1[256];
+  __shared__ uint32_t tocc[8], tsb[8];
+  const int64_t c = blockIdx.x;
   if (c >= nbchunks) return;
+  const int lane = threadIdx.x;
   const int64_t s0 = c * CB;
   const int64_t e = (s0 + CB < m) ? s0 + CB : m;
   uint4 y = ybound[c];
@@ -322,23 +365,41 @@ __global__ void ribbon_final_kernel(int64_t m, int64_t nbchunks, const uint64_t*
   uint64_t w0 = (uint64_t)y.x | ((uint64_t)y.y << 32);
   uint64_t w1 = (uint64_t)y.z | ((uint64_t)y.w << 32);
   uint64_t outw = 0;
-  for (int64_t col = e - 1; col >= s0; --col) {
-    uint32_t bit = 0;
-    if ((occ[col >> 5] >> (col & 31)) & 1u) {
-      const uint64_t a0 = sp0[col], a1 = sp1[col];
-      const uint64_t q0 = (a0 >> 1) | (a1 << 63), q1 = a1 >> 1;
-      bit = (uint32_t)((__popcll(q0 & w0) + __popcll(q1 & w1)) & 1) ^ ((sbit[col >> 5] >> (col & 31)) & 1u);
+  int64_t col = e - 1;
+  while (col >= s0) {
+    const int64_t tstart = (col / 256) * 256;
+    const int ntile = (int)(col - tstart + 1);
+    __syncwarp();
+    for (int j = lane; j < ntile; j += 32) {
+      tp0[j] = sp0[tstart + j];
+      tp1[j] = sp1[tstart + j];
     }
-    w1 = (w1 << 1) | (w0 >> 63);
-    w0 = (w0 << 1) | bit;
-    outw |= (uint64_t)bit << (col & 63);
-    if ((col & 63) == 0) {
-      words[col >> 6] = outw;
-      outw = 0;
+    if (lane < 8) {
+      const bool in = lane * 32 < ntile;
+      tocc[lane] = in ? occ[tstart / 32 + lane] : 0;
+      tsb[lane] = in ? sbit[tstart / 32 + lane] : 0;
     }
+    __syncwarp();
+    if (lane == 0) {
+      for (int j = ntile - 1; j >= 0; --j) {
+        const int64_t cc = tstart + j;
+        uint32_t bit = 0;
+        if ((tocc[j >> 5] >> (j & 31)) & 1u) {
+          const uint64_t a0 = tp0[j], a1 = tp1[j];
+          const uint64_t q0 = (a0 >> 1) | (a1 << 63), q1 = a1 >> 1;
+          bit = (uint32_t)((__popcll(q0 & w0) + __popcll(q1 & w1)) & 1) ^ ((tsb[j >> 5] >> (j & 31)) & 1u);
+        }
+        w1 = (w1 << 1) | (w0 >> 63);
+        w0 = (w0 << 1) | bit;
+        outw |= (uint64_t)bit << (cc & 63);
+        if ((cc & 63) == 0) {
+          words[cc >> 6] = outw;
+          outw = 0;
+        }
+      }
+    }
+    col = tstart - 1;
   }
-  // e is a multiple of 64 except possibly at m; the first column s0 is a
-  // multiple of 64, so every word was flushed at col % 64 == 0.
 }
 
 __global__ void ribbon_query_kernel(const int64_t* starts, const uint64_t* p0, const uint64_t* p1, int64_t N,
@@ -492,7 +553,8 @@ int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_
   RRow* cur = rows;
   for (int pass = 0; pending > 0; ++pass) {
     SHK_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
-    ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(cur, rowoff, nch, m, sp0, sp1, occ, sb, ovf, cnt, bad);
+    ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(cur, rowoff, nch, m, sp0, sp1, occ, sb, ovf, cnt, bad,
+                                                      pass == 0 ? 1 : 0);
     SHK_LAUNCHED();
     int64_t h[2];
     SHK_CUDA(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, st));
@@ -527,7 +589,7 @@ int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_
   SHK_LAUNCHED();
   ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, forms, yb);
   SHK_LAUNCHED();
-  ribbon_final_kernel<<<(unsigned)((nbc + 63) / 64), 64, 0, st>>>(m, nbc, sp0, sp1, occ, sb, yb, words_out);
+  ribbon_final_kernel<<<(unsigned)nbc, 32, 0, st>>>(m, nbc, sp0, sp1, occ, sb, yb, words_out);
   SHK_LAUNCHED();
   return 0;
 }

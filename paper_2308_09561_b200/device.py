@@ -66,6 +66,15 @@ class timer:
         return False
 
 
+OPT_EXACT_SPLIT_EVALS = 0
+OPT_LEAF_TEAM_WARPS = 1
+
+
+def set_option(opt: int, value: int):
+    """Context tuning/instrumentation option (include/shockhash_b200.h)."""
+    check(_lib.load_library().shk_ctx_set_option(ctx(), int(opt), int(value)), "option")
+
+
 def launch_count() -> int:
     return int(_lib.load_library().shk_launch_count(ctx()))
 
