@@ -59,7 +59,8 @@ int shk_ctx_num_sms(shk_ctx* ctx);
 /* Tuning / instrumentation options of a context. */
 enum {
   SHK_OPT_EXACT_SPLIT_EVALS = 0, /* 1: builds also count the reference's split `evals` (slower) */
-  SHK_OPT_LEAF_TEAM_WARPS = 1    /* warps per leaf in builds (0 = heuristic) */
+  SHK_OPT_LEAF_TEAM_WARPS = 1,   /* warps per leaf in the per-level schedule (0 = heuristic) */
+  SHK_OPT_SCHEDULE = 2           /* 0: one persistent task-queue launch per build; 1: one launch per level */
 };
 int shk_ctx_set_option(shk_ctx* ctx, int opt, int64_t value);
 /* Device memory from the context's caching pool (bench / zero-copy users). */
@@ -187,6 +188,9 @@ int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int6
  * [0] bucketize [1] split searches [2] leaf searches [3] Rice stream
  * [4] ribbon; split_evals = the reference's split `evals` counter summed. */
 int shk_build_phase_ms(shk_build* b, float* ms /* [5] */, int64_t* split_evals);
+/* Device ms of each split level (one launch per tree depth) of the last run;
+ * returns the number of levels written. */
+int shk_build_level_ms(shk_build* b, float* ms, int32_t* depth, int max_levels);
 int shk_build_destroy(shk_build* b);
 
 /* ---- MPHF evaluation (MphfDescriptor.query_hashed_many ->

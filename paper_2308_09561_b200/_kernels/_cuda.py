@@ -492,6 +492,13 @@ class GpuBuild:
         check(_L().shk_build_phase_ms(self.handle, ms, ctypes.byref(ev)))
         return [float(x) for x in ms], int(ev.value)
 
+    def level_ms(self):
+        """Device ms per split level (tree depth) of the last run."""
+        ms = (ctypes.c_float * 64)()
+        dp = (ctypes.c_int32 * 64)()
+        k = _L().shk_build_level_ms(self.handle, ms, dp, 64)
+        return {int(dp[i]): round(float(ms[i]), 3) for i in range(k)}
+
     def close(self):
         if self.handle is not None and _lib._lib is not None:
             _lib._lib.shk_build_destroy(self.handle)

@@ -87,6 +87,7 @@ _SIGS = {
     "shk_blake2b128": (_I, [_P, _P, _I64, _P, _I64, _U64, _P, _P, _I]),
     "shk_blake2b128_fixed": (_I, [_P, _P, _I, _I64, _U64, _P, _P, _I]),
     "shk_build_phase_ms": (_I, [_P, _P, _P]),
+    "shk_build_level_ms": (_I, [_P, _P, _P, _I]),
     "shk_build_create": (_I, [_P, _P, _P, _I64, _I64, _I, _P, _P, _P]),
     "shk_build_key_prefix": (_I, [_P, _P]),
     "shk_build_sorted_keys": (_I, [_P, _P, _P]),

@@ -754,10 +754,26 @@ struct shk_build {
   ~shk_build() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    level_reset();
   }
   void mark(int i) {
     if (!ev[i]) cudaEventCreate(&ev[i]);
     cudaEventRecord(ev[i], c->stream);
+  }
+  // per split level (depth) timing
+  std::vector<cudaEvent_t> lev;
+  std::vector<int> lev_depth;
+  void level_mark(int depth) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c->stream);
+    lev.push_back(e);
+    lev_depth.push_back(depth);
+  }
+  void level_reset() {
+    for (auto e : lev) cudaEventDestroy(e);
+    lev.clear();
+    lev_depth.clear();
   }
   float span(int a, int z) {
     float ms = 0;
@@ -888,17 +904,34 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   std::vector<std::vector<ShkSplitTask>> tasks((size_t)S.max_depth + 1);
   std::vector<int64_t> leaf_off, leaf_slot;
   leaf_off.reserve((size_t)(b->N / 8 + 16));
+  const bool use_tree = c->opt[SHK_OPT_SCHEDULE] == 0 && !c->opt[SHK_OPT_EXACT_SPLIT_EVALS];
+  std::vector<ShkTreeNode> tnodes(use_tree ? (size_t)nn : 0);
+  std::vector<int64_t> tqueue;
+  if (use_tree) tqueue.assign((size_t)nn, -1);
+  int64_t nroots = 0;
   int max_leaf = 0;
   for (int64_t i = 0; i < nbr; ++i) {
     if (bplan[i] < 0) continue;
     const int64_t bu = b0 + i;
     const int64_t kstart = (int64_t)b->h_prefix[bu];
     const int64_t pa = S.plan_off[bplan[i]], pb = S.plan_off[bplan[i] + 1];
+    if (use_tree) tqueue[nroots++] = node_base[i];
     for (int64_t j = pa; j < pb; ++j) {
       const PlanNode& nd = S.nodes[j];
       const int64_t slot = node_base[i] + (j - pa);
       ng[slot] = nd.g;
       nkind[slot] = (uint8_t)(nd.kind != 0);
+      if (use_tree) {
+        ShkTreeNode& tn = tnodes[slot];
+        tn.start = kstart + nd.off;
+        tn.m = nd.m;
+        tn.kind = nd.kind != 0;
+        tn.fanout = nd.kind == 0 ? nd.fanout : 0;
+        for (int k = 0; k < 4; ++k) {
+          tn.sizes[k] = nd.sizes[k];
+          tn.child[k] = (nd.kind == 0 && k < nd.fanout) ? node_base[i] + nd.child[k] : -1;
+        }
+      }
       if (nd.kind == 0) {
         if (nd.m >= 32768) {
           shk_set_error("split node of %d keys exceeds the 32767-key split kernel limit", nd.m);
@@ -922,7 +955,8 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
       }
     }
   }
-  const int64_t L = (int64_t)leaf_off.size();
+  int64_t L = (int64_t)leaf_off.size();
+  const int64_t n_leaves = L;
   // leaves are contiguous in key order: CSR end = range end
   leaf_off.push_back((int64_t)b->h_prefix[b1]);
   // ---- device tables
@@ -951,9 +985,46 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   SHK_CUDA(cudaMemsetAsync(dacc.p, 0, 64, c->stream));
   int* exh = c->d_counter + 4;
   SHK_CUDA(cudaMemsetAsync(exh, 0, 4, c->stream));
-  // ---- splits, level by level (every node of one depth in one launch)
   b->mark(2);
-  {
+  b->level_reset();
+  DBuf dnodes(c), dqueue(c), dqctl(c);
+  if (use_tree && nn > 0) {
+    // ---- one persistent launch for every split node and leaf (shk_tree.cu)
+    RC(dnodes.alloc((size_t)nn * sizeof(ShkTreeNode)));
+    RC(dqueue.alloc((size_t)nn * 8));
+    RC(dqctl.alloc(256));
+    RC(h2d(c, dnodes.p, tnodes.data(), (size_t)nn * sizeof(ShkTreeNode)));
+    RC(h2d(c, dqueue.p, tqueue.data(), (size_t)nn * 8));
+    unsigned long long qc[2] = {0ull, (unsigned long long)nroots};
+    RC(h2d(c, dqctl.p, qc, 16));
+    ShkTreeLaunch p{};
+    p.keys = b->keys.as<uint64_t>();
+    p.tmp = b->tmp.as<uint64_t>();
+    p.nodes = dnodes.as<ShkTreeNode>();
+    p.nnodes = nn;
+    p.queue = dqueue.as<int64_t>();
+    p.head = dqctl.as<unsigned long long>();
+    p.tail = dqctl.as<unsigned long long>() + 1;
+    p.max_seed = max_seed;
+    p.seeds = dseeds.as<int64_t>();
+    p.mode = mode;
+    p.cache_k = cache_k;
+    p.cache_min_leaf = cache_min_leaf;
+    p.max_n = max_leaf;
+    p.choice_out = b->choice.as<uint8_t>();
+    if (b->record) {
+      RC(b->place.alloc((size_t)b->N * 8));
+      p.place_out = b->place.as<int64_t>();
+    }
+    p.stats_acc = dacc.as<unsigned long long>();
+    p.exhausted = exh;
+    p.num_sms = c->num_sms;
+    RC(shk_launch_tree(p, c->stream));
+    b->mark(3);
+    L = 0;  // leaves already solved
+  }
+  // ---- splits, level by level (every node of one depth in one launch)
+  if (!use_tree) {
     size_t o = 0;
     for (auto& v : tasks) {
       if (!v.empty()) {
@@ -971,10 +1042,12 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
         p.exhausted = exh;
         p.evals_acc = dacc.as<unsigned long long>() + 6;
         p.exact_evals = c->opt[SHK_OPT_EXACT_SPLIT_EVALS] ? 1 : 0;
+        b->level_mark((int)(&v - &tasks[0]));
         RC(shk_launch_split(p, c->stream));
       }
       o += v.size();
     }
+    b->level_mark((int)tasks.size());
   }
   // ---- leaves
   b->mark(3);
@@ -1058,7 +1131,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     stats_out[3] = (int64_t)acc[3];
     stats_out[4] = (int64_t)acc[4];  // leaf seed bits
     stats_out[5] = (int64_t)acc[5];  // split seed bits
-    stats_out[6] = L;
+    stats_out[6] = n_leaves;
   }
   b->b0 = b0;
   b->b1 = b1;
@@ -1129,6 +1202,17 @@ int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int6
   RC(csync(c));
   b->phase_ms[4] = b->span(6, 7);
   return 0;
+}
+
+int shk_build_level_ms(shk_build* b, float* ms, int32_t* depth, int max_levels) {
+  int k = 0;
+  for (size_t i = 0; i + 1 < b->lev.size() && k < max_levels; ++i, ++k) {
+    float t = 0;
+    if (cudaEventElapsedTime(&t, b->lev[i], b->lev[i + 1]) != cudaSuccess) cudaGetLastError();
+    ms[k] = t;
+    if (depth) depth[k] = b->lev_depth[i];
+  }
+  return k;
 }
 
 int shk_build_phase_ms(shk_build* b, float* ms, int64_t* split_evals) {

@@ -82,6 +82,126 @@ SHK_D bool pf_accepts(const uint16_t* e, int stride, int nkeys, int n, int rot) 
   return true;
 }
 
+// Warp-cooperative exact pseudoforest check of one candidate (all 32 lanes
+// participate; lane t owns edges t and t+32).  Used instead of a per-lane
+// union-find so a rare candidate costs ~100 warp instructions, not ~1000
+// single-lane ones.
+//  1. Degrees (shared atomics).  An isolated edge (both cells of degree 1)
+//     is a tree component: reject.  This catches ~84% of the candidates that
+//     pass the coverage filter at n=40.
+//  2. Components by min-label hooking + pointer jumping (labels only move to
+//     smaller indices, so jumping always ends at a root; a round that hooked
+//     anything is followed by another, so a lost concurrent hook is redone).
+//  3. Pseudoforest iff every component has as many edges as cells.
+// ew: edges of the warp, column per lane (ew[i*32 + L] = candidate lane L's
+// edge i, packed u | v << 8 | rotation-set-B << 15); rot: B-cell shift.
+struct WarpChk {
+  int deg[64];
+  int par[64];
+  int ce[64];
+  int cv[64];
+};
+
+SHK_D bool warp_pf_check(const uint16_t* ew, int L, int rot, int n, int lane, WarpChk& s) {
+  int u0 = -1, v0 = 0, u1 = -1, v1 = 0;
+  if (lane < n) {
+    uint32_t w = ew[lane * 32 + L];
+    u0 = w & 0x7F;
+    v0 = (w >> 8) & 0x7F;
+    if (w & 0x8000u) {
+      u0 += rot;
+      v0 += rot;
+      if (u0 >= n) u0 -= n;
+      if (v0 >= n) v0 -= n;
+    }
+  }
+  if (lane + 32 < n) {
+    uint32_t w = ew[(lane + 32) * 32 + L];
+    u1 = w & 0x7F;
+    v1 = (w >> 8) & 0x7F;
+    if (w & 0x8000u) {
+      u1 += rot;
+      v1 += rot;
+      if (u1 >= n) u1 -= n;
+      if (v1 >= n) v1 -= n;
+    }
+  }
+  s.deg[lane] = 0;
+  s.deg[lane + 32] = 0;
+  s.par[lane] = lane;
+  s.par[lane + 32] = lane + 32;
+  __syncwarp();
+  if (u0 >= 0) {
+    atomicAdd(&s.deg[u0], 1);
+    atomicAdd(&s.deg[v0], 1);
+  }
+  if (u1 >= 0) {
+    atomicAdd(&s.deg[u1], 1);
+    atomicAdd(&s.deg[v1], 1);
+  }
+  __syncwarp();
+  const bool iso = (u0 >= 0 && s.deg[u0] == 1 && s.deg[v0] == 1) || (u1 >= 0 && s.deg[u1] == 1 && s.deg[v1] == 1);
+  if (__any_sync(FULL_WARP, iso)) return false;
+  for (int it = 0; it < 128; ++it) {
+    bool ch = false;
+    if (u0 >= 0) {
+      int a = s.par[u0], b = s.par[v0];
+      if (a != b) {
+        atomicMin(&s.par[a > b ? a : b], a < b ? a : b);
+        ch = true;
+      }
+    }
+    if (u1 >= 0) {
+      int a = s.par[u1], b = s.par[v1];
+      if (a != b) {
+        atomicMin(&s.par[a > b ? a : b], a < b ? a : b);
+        ch = true;
+      }
+    }
+    __syncwarp();
+    for (int x = lane; x < n; x += 32) {
+      int p = s.par[x];
+      while (s.par[p] != p) p = s.par[p];
+      s.par[x] = p;
+    }
+    __syncwarp();
+    if (!__any_sync(FULL_WARP, ch)) break;
+  }
+  s.ce[lane] = 0;
+  s.ce[lane + 32] = 0;
+  s.cv[lane] = 0;
+  s.cv[lane + 32] = 0;
+  __syncwarp();
+  for (int x = lane; x < n; x += 32) atomicAdd(&s.cv[s.par[x]], 1);
+  if (u0 >= 0) atomicAdd(&s.ce[s.par[u0]], 1);
+  if (u1 >= 0) atomicAdd(&s.ce[s.par[u1]], 1);
+  __syncwarp();
+  bool bad = false;
+  for (int x = lane; x < n; x += 32)
+    if (s.par[x] == x && s.ce[x] != s.cv[x]) bad = true;
+  const bool ok = !__any_sync(FULL_WARP, bad);
+  __syncwarp();
+  return ok;
+}
+
+// First accepted candidate in (lane, r) order among the lanes' candidate
+// masks (bit r of cand = the coverage filter passed for rotation r).
+// Returns r on the winning lane, -1 elsewhere (all lanes get the same L).
+SHK_D int warp_first_accept(const uint16_t* ew, uint64_t cand, int n, int lane, WarpChk& s) {
+  unsigned lanes = __ballot_sync(FULL_WARP, cand != 0);
+  while (lanes) {
+    const int L = __ffs(lanes) - 1;
+    lanes &= lanes - 1;
+    uint64_t pm = __shfl_sync(FULL_WARP, cand, L);
+    while (pm) {
+      const int r = __ffsll((long long)pm) - 1;
+      pm &= pm - 1;
+      if (warp_pf_check(ew, L, r, n, lane, s)) return lane == L ? r : -1;
+    }
+  }
+  return -1;
+}
+
 // Canonical 1-orientation of a pseudoforest (pseudoforest.py:149-201):
 // peel degree-1 cells (the single remaining edge takes that cell), then walk
 // each remaining cycle from its lowest-index key, which takes its first cell.

@@ -63,6 +63,35 @@ struct ShkSplitLaunch {
 };
 int shk_launch_split(const ShkSplitLaunch& p, cudaStream_t st);
 
+// One node of a bucket range for the persistent construction kernel.
+struct ShkTreeNode {
+  int64_t start;     // first key (global index into the working key array)
+  int32_t m;         // keys in the node
+  int32_t kind;      // 0 split, 1 leaf
+  int32_t fanout;    // split parts (kind 0)
+  int32_t sizes[4];  // part sizes (kind 0)
+  int32_t pad;
+  int64_t child[4];  // global node ids of the parts (kind 0)
+};
+struct ShkTreeLaunch {
+  uint64_t* keys;  // interleaved (hi, lo) pairs
+  uint64_t* tmp;   // scratch pairs
+  const ShkTreeNode* nodes;
+  int64_t nnodes;
+  int64_t* queue;  // [nnodes]: roots first, -1 = not yet published
+  unsigned long long* head;
+  unsigned long long* tail;
+  uint64_t max_seed;
+  int64_t* seeds;  // per node
+  int mode, cache_k, cache_min_leaf, max_n;
+  uint8_t* choice_out;
+  int64_t* place_out;
+  unsigned long long* stats_acc;
+  int* exhausted;
+  int num_sms;
+};
+int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st);
+
 // Bucketing.
 // skeys: interleaved (hi, lo) pairs [2N], sorted by (bucket, hi, lo).
 int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nbuckets, uint64_t* skeys,

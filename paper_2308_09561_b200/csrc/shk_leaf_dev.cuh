@@ -1,0 +1,386 @@
+// ShockHash leaf seed search (plain and rotation fitting) + orientation, as
+// team-level device functions shared by the batched leaf kernels
+// (shk_leaf.cu) and the persistent construction kernel (shk_tree.cu).
+//
+// Restates _core.pyx:186-229 (search_plain), :232-334 (search_rotate) and
+// pseudoforest.py:149-201 (orient) for sm_100a.
+//
+// A TEAM of TW warps owns one leaf.  Every lane tests one candidate (a seed
+// for plain search, a base seed for rotation fitting); a team round covers
+// TW*32 consecutive candidates.  The leaf's keys sit in shared memory and are
+// read with broadcast LDS.128, the coverage masks live in registers, and
+// every lane stores its candidate's edges in shared memory while hashing.
+// Candidates that pass the coverage filter get the exact pseudoforest check
+// warp-cooperatively (warp_first_accept, in (lane, r) order).  After each
+// round the team takes the lowest accepting candidate, so the result is the
+// reference's minimum seed (lexicographic (base, r) minimum for rotation)
+// and the counters (evals, passes, checks, a_evals) are the reference's.
+#pragma once
+#include "shk_common.cuh"
+
+namespace shk {
+
+struct LeafArgs {
+  const uint64_t* hi;
+  const uint64_t* lo;
+  const int64_t* off;  // CSR [L+1]; leaf i = keys [off[i], off[i+1])
+  int64_t L;
+  uint64_t max_seed;
+  int mode;             // 0 plain, 1 rotate
+  int cache_k;          // rotate: k-aligned A-set seed when m > cache_min_leaf
+  int cache_min_leaf;
+  int64_t* seed_out;    // [L] (or indexed by seed_slot)
+  uint64_t* fbits_out;  // [L] or null
+  uint8_t* choice_out;  // [N] per key (CSR order) or null
+  int64_t* stats_out;   // [L][4] or null
+  int* counter;         // dynamic leaf fetch
+  int* error;           // set on internal inconsistency
+  int stride;           // key stride in hi/lo (1 separate arrays, 2 interleaved pairs)
+  const int64_t* seed_slot;  // optional: seed_out index per leaf
+  unsigned long long* stats_acc;  // optional [4] running totals
+  int* exhausted;       // optional: set if a leaf has no seed below max_seed
+  int64_t* place_out;   // optional [N]: global slot of each key (leaf start + its cell)
+};
+
+template <int TW>
+struct LeafSmem {
+  uint4 keys[64];                 // (hi.lo, hi.hi, lo.lo, lo.hi)
+  uint16_t edges[TW][64 * 32];    // per-lane packed edges, column per lane
+  int64_t slot_win[2][TW];        // per-warp lowest accepting candidate (or -1)
+  int32_t slot_r[2][TW];          // rotation of that candidate
+  uint64_t slot_pass_le[2][TW];   // passes at candidates <= winner in warp
+  uint64_t slot_pass[2][TW];      // all passes in warp this round
+  uint64_t slot_evals_le[2][TW];
+  uint64_t slot_evals[2][TW];
+  uint64_t slot_aev_le[2][TW];
+  uint64_t slot_aev[2][TW];
+  uint8_t eu[64], ev[64];
+  uint64_t inc[64];
+  WarpChk chk[TW];                // per-warp scratch of the exact check
+  int64_t leaf;
+};
+
+// A CTA holds independent teams of TW warps; a team synchronizes on its own
+// named barrier (id team+1), so teams never wait for each other.
+template <int TW>
+SHK_D void team_sync(int team) {
+  if (TW == 1)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TW * 32) : "memory");
+}
+
+// Where a solved leaf writes its results.
+struct LeafOut {
+  int64_t seed_slot;   // index into a.seed_out
+  int64_t leaf_index;  // index into fbits_out / stats_out (or -1)
+};
+
+template <int TW>
+SHK_D void load_leaf_keys(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, int tt) {
+  for (int i = tt; i < n; i += TW * 32) {
+    u2 h = split64(a.hi[(k0 + i) * a.stride]), l = split64(a.lo[(k0 + i) * a.stride]);
+    sm.keys[i] = make_uint4(h.lo, h.hi, l.lo, l.hi);
+  }
+}
+
+// Orientation of the final edges in sm.eu/sm.ev (warp 0 of the team) and
+// result stores.
+template <int TW>
+SHK_D void leaf_finish(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, int64_t q, const LeafOut& o,
+                       uint64_t evals, uint64_t passes, uint64_t aev, int lane) {
+  if (q >= 0 && n >= 2) {
+    __syncwarp();
+    uint64_t f = 0;
+    if (lane == 0) f = orient_edges(sm.eu, sm.ev, n, sm.inc);
+    f = __shfl_sync(FULL_WARP, f, 0);
+    if (lane == 0 && a.fbits_out && o.leaf_index >= 0) a.fbits_out[o.leaf_index] = f;
+    if (a.choice_out)
+      for (int i = lane; i < n; i += 32) a.choice_out[k0 + i] = (uint8_t)((f >> i) & 1);
+    if (a.place_out)
+      for (int i = lane; i < n; i += 32) a.place_out[k0 + i] = k0 + (((f >> i) & 1) ? sm.ev[i] : sm.eu[i]);
+  } else if (lane == 0) {
+    if (a.fbits_out && o.leaf_index >= 0) a.fbits_out[o.leaf_index] = 0;
+    if (a.choice_out && n == 1) a.choice_out[k0] = 0;
+    if (a.place_out && n == 1) a.place_out[k0] = k0;
+  }
+  if (lane == 0) {
+    a.seed_out[o.seed_slot] = q;
+    if (a.stats_out && o.leaf_index >= 0) {
+      int64_t* st = a.stats_out + 4 * o.leaf_index;
+      st[0] = (int64_t)evals;
+      st[1] = (int64_t)passes;
+      st[2] = (int64_t)passes;
+      st[3] = (int64_t)aev;
+    }
+    if (a.stats_acc) {
+      atomicAdd(&a.stats_acc[0], (unsigned long long)evals);
+      atomicAdd(&a.stats_acc[1], (unsigned long long)passes);
+      atomicAdd(&a.stats_acc[2], (unsigned long long)passes);
+      atomicAdd(&a.stats_acc[3], (unsigned long long)aev);
+    }
+    if (q < 0 && a.exhausted) atomicOr(a.exhausted, 1);
+  }
+}
+
+// -------------------------------------------------------------------------
+// Plain search body for one candidate seed per lane.
+template <bool WIDE>
+SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
+  u2 x = seed_mixer_d(s, TAG_LEAF);
+  const uint32_t un = (uint32_t)n, unm1 = (uint32_t)(n - 1);
+  uint32_t m0 = 0, m1 = 0;
+#pragma unroll 4
+  for (int i = 0; i < n; ++i) {
+    uint4 k = keys[i];
+    u2 v = remix_d(u2{k.x, k.y}, u2{k.z, k.w}, x);
+    uint32_t h0, h1;
+    leaf_pair_d(v, un, unm1, h0, h1);
+    if (!WIDE) {
+      m0 |= (1u << h0) | (1u << h1);
+    } else {
+      m0 |= shl_clamp(1u, h0) | shl_clamp(1u, h1);
+      m1 |= shl_clamp(1u, h0 - 32u) | shl_clamp(1u, h1 - 32u);
+    }
+    e[i * 32] = (uint16_t)(h0 | (h1 << 8));
+  }
+  if (!WIDE) {
+    uint32_t full = (n == 32) ? 0xFFFFFFFFu : ((1u << n) - 1u);
+    return m0 == full;
+  } else {
+    // WIDE code also serves leaves of <= 32 keys in mixed batches
+    const uint32_t fulllo = (n >= 32) ? 0xFFFFFFFFu : ((1u << n) - 1u);
+    const uint32_t fullhi = (n >= 64) ? 0xFFFFFFFFu : (n > 32 ? ((1u << (n - 32)) - 1u) : 0u);
+    return m0 == fulllo && m1 == fullhi;
+  }
+}
+
+// Plain search of one leaf (keys [k0, k0+n)) by a team.  All threads of the
+// team call it; it ends team-synchronized.
+template <int TW, bool WIDE>
+SHK_D void solve_plain(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, const LeafOut& o, int team, int warp,
+                       int lane, int tt) {
+  load_leaf_keys<TW>(a, sm, k0, n, tt);
+  team_sync<TW>(team);
+  uint16_t* e = &sm.edges[warp][lane];
+  int64_t seed = -1;
+  uint64_t passes = 0;
+  if (n <= 1) {
+    seed = 0;
+    passes = 1;
+  } else {
+    // Rounds of TW*32 consecutive seeds; warp w owns [R + 32w, R + 32w + 32).
+    int par = 0;
+    for (uint64_t R = 0; R < a.max_seed; R += (uint64_t)TW * 32, par ^= 1) {
+      const uint64_t s = R + (uint64_t)warp * 32 + lane;
+      const bool valid = s < a.max_seed;
+      bool full = valid && plain_mask_full<WIDE>(sm.keys, n, s, e);
+      unsigned pb = __ballot_sync(FULL_WARP, full);
+      const bool acc = warp_first_accept(sm.edges[warp], full ? 1ull : 0ull, n, lane, sm.chk[warp]) == 0;
+      unsigned ab = __ballot_sync(FULL_WARP, acc);
+      if (lane == 0) {
+        int w = ab ? __ffs(ab) - 1 : 32;
+        unsigned le = (w == 32) ? pb : (pb & (0xFFFFFFFFu >> (31 - w)));
+        sm.slot_win[par][warp] = ab ? (int64_t)(R + (uint64_t)warp * 32 + w) : -1;
+        sm.slot_pass_le[par][warp] = __popc(le);
+        sm.slot_pass[par][warp] = __popc(pb);
+      }
+      team_sync<TW>(team);
+      int64_t win = -1;
+      uint64_t round_pass = 0;
+#pragma unroll
+      for (int w = 0; w < TW; ++w) {
+        if (win < 0) {
+          int64_t sw = sm.slot_win[par][w];
+          if (sw >= 0) {
+            win = sw;
+            round_pass += sm.slot_pass_le[par][w];
+          } else {
+            round_pass += sm.slot_pass[par][w];
+          }
+        }
+      }
+      passes += round_pass;
+      if (win >= 0) {
+        seed = win;
+        break;
+      }
+    }
+  }
+  if (warp == 0) {
+    if (seed >= 0 && n >= 2) {
+      const u2 x = seed_mixer_d((uint64_t)seed, TAG_LEAF);
+      for (int i = lane; i < n; i += 32) {
+        uint4 k = sm.keys[i];
+        u2 v = remix_d(u2{k.x, k.y}, u2{k.z, k.w}, x);
+        uint32_t h0, h1;
+        leaf_pair_d(v, (uint32_t)n, (uint32_t)(n - 1), h0, h1);
+        sm.eu[i] = (uint8_t)h0;
+        sm.ev[i] = (uint8_t)h1;
+      }
+    }
+    const uint64_t evals = (n <= 1) ? 1 : (seed >= 0 ? ((uint64_t)seed + 1) * n : a.max_seed * (uint64_t)n);
+    leaf_finish<TW>(a, sm, k0, n, seed, o, evals, passes, 0, lane);
+  }
+  team_sync<TW>(team);
+}
+
+// Rotation fitting of one leaf: lane per base seed.
+template <int TW, bool WIDE>
+SHK_D void solve_rotate(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, const LeafOut& o, int team,
+                        int warp, int lane, int tt) {
+  load_leaf_keys<TW>(a, sm, k0, n, tt);
+  team_sync<TW>(team);
+  uint16_t* e = &sm.edges[warp][lane];
+  const int64_t ck = (n > a.cache_min_leaf) ? a.cache_k : 0;
+  int64_t q = -1;
+  uint64_t passes = 0, evals = 0, aev = 0;
+  if (n <= 1) {
+    q = 0;
+    passes = 1;
+    evals = 1;
+  } else {
+    const uint64_t max_base = a.max_seed / (uint64_t)n + 1;
+    const uint32_t un = (uint32_t)n, unm1 = (uint32_t)(n - 1);
+    int par = 0;
+    for (uint64_t R = 0; R < max_base; R += (uint64_t)TW * 32, par ^= 1) {
+      const uint64_t base = R + (uint64_t)warp * 32 + lane;
+      const bool valid = base < max_base;
+      uint64_t passmask = 0;
+      uint32_t na = 0;
+      bool ws = false;
+      if (valid) {
+        const uint64_t sa = ck ? base - base % (uint64_t)ck : base;
+        ws = (base == 0) || (ck == 0) || (base % (uint64_t)ck == 0);
+        const u2 xb = seed_mixer_d(sa, TAG_SPLITBIT);
+        const u2 xa = seed_mixer_d(sa, TAG_LEAF);
+        const u2 xg = seed_mixer_d(base, TAG_LEAF);
+        uint32_t ma0 = 0, ma1 = 0, mb0 = 0, mb1 = 0;
+#pragma unroll 2
+        for (int i = 0; i < n; ++i) {
+          uint4 k = sm.keys[i];
+          u2 kh{k.x, k.y}, kl{k.z, k.w};
+          uint32_t bit = remix_top_d(kh, kl, xb);
+          u2 x;
+          x.lo = bit ? xg.lo : xa.lo;
+          x.hi = bit ? xg.hi : xa.hi;
+          u2 v = remix_d(kh, kl, x);
+          uint32_t h0, h1;
+          leaf_pair_d(v, un, unm1, h0, h1);
+          uint32_t c0, c1 = 0;
+          if (!WIDE) {
+            c0 = (1u << h0) | (1u << h1);
+          } else {
+            c0 = shl_clamp(1u, h0) | shl_clamp(1u, h1);
+            c1 = shl_clamp(1u, h0 - 32u) | shl_clamp(1u, h1 - 32u);
+          }
+          if (bit) {
+            mb0 |= c0;
+            mb1 |= c1;
+          } else {
+            ma0 |= c0;
+            ma1 |= c1;
+          }
+          na += bit ^ 1u;
+          e[i * 32] = (uint16_t)(h0 | (h1 << 8) | (bit << 15));
+        }
+        // Rotation filter: the set of r with (mask_a | rotl_n(mask_b, r))
+        // == full.  Cell j missing from A needs mask_b[(j - r) mod n], i.e.
+        // r in rotl_n(rev, j) with rev[k] = mask_b[(-k) mod n]; intersect
+        // over the missing cells (about a third of them), stop when empty.
+        const uint64_t full = (n == 64) ? ~0ull : ((1ull << n) - 1);
+        const uint64_t ma = join64(ma0, ma1), mb = join64(mb0, mb1);
+        uint64_t need = ~ma & full;
+        uint64_t rv = __brevll(mb) >> (64 - n);        // bit k = mb[n-1-k]
+        rv = ((rv << 1) | (rv >> (n - 1))) & full;      // bit k = mb[(n-k) mod n]
+        uint64_t Rm = full;
+        while (need && Rm) {
+          const int j = __ffsll((long long)need) - 1;
+          need &= need - 1;
+          Rm &= j ? (((rv << j) | (rv >> (n - j))) & full) : rv;
+        }
+        passmask = Rm;
+      }
+      // exact checks, warp-cooperative, in lexicographic (base, r) order
+      const int win_r = warp_first_accept(sm.edges[warp], passmask, n, lane, sm.chk[warp]);
+      const uint32_t nb = (uint32_t)n - na;
+      const uint64_t my_ev = valid ? (uint64_t)nb + (ws ? (uint64_t)n + na : 0) : 0;
+      const uint64_t my_aev = (valid && ws) ? na : 0;
+      const uint64_t my_pass = __popcll(passmask);
+      uint64_t my_pass_le = my_pass;
+      if (win_r >= 0) my_pass_le = __popcll(passmask & ((win_r == 63) ? ~0ull : ((2ull << win_r) - 1)));
+      unsigned ab = __ballot_sync(FULL_WARP, win_r >= 0);
+      int wl = ab ? __ffs(ab) - 1 : 32;
+      // sums over lanes <= wl (winner) and over all lanes
+      uint64_t c_ev_le = (lane <= wl) ? my_ev : 0;
+      uint64_t c_aev_le = (lane <= wl) ? my_aev : 0;
+      uint64_t c_pass_le = (lane < wl) ? my_pass : (lane == wl ? my_pass_le : 0);
+      uint64_t t_ev = warp_sum(my_ev), t_aev = warp_sum(my_aev), t_pass = warp_sum(my_pass);
+      c_ev_le = warp_sum(c_ev_le);
+      c_aev_le = warp_sum(c_aev_le);
+      c_pass_le = warp_sum(c_pass_le);
+      int wr = __shfl_sync(FULL_WARP, win_r, wl & 31);
+      if (lane == 0) {
+        sm.slot_win[par][warp] = ab ? (int64_t)(R + (uint64_t)warp * 32 + wl) : -1;
+        sm.slot_r[par][warp] = wr;
+        sm.slot_pass_le[par][warp] = c_pass_le;
+        sm.slot_pass[par][warp] = t_pass;
+        sm.slot_evals_le[par][warp] = c_ev_le;
+        sm.slot_evals[par][warp] = t_ev;
+        sm.slot_aev_le[par][warp] = c_aev_le;
+        sm.slot_aev[par][warp] = t_aev;
+      }
+      team_sync<TW>(team);
+      int64_t winb = -1;
+      int winr = 0;
+#pragma unroll
+      for (int w = 0; w < TW; ++w) {
+        if (winb < 0) {
+          int64_t sw = sm.slot_win[par][w];
+          if (sw >= 0) {
+            winb = sw;
+            winr = sm.slot_r[par][w];
+            passes += sm.slot_pass_le[par][w];
+            evals += sm.slot_evals_le[par][w];
+            aev += sm.slot_aev_le[par][w];
+          } else {
+            passes += sm.slot_pass[par][w];
+            evals += sm.slot_evals[par][w];
+            aev += sm.slot_aev[par][w];
+          }
+        }
+      }
+      if (winb >= 0) {
+        uint64_t qq = (uint64_t)winb * (uint64_t)n + (uint64_t)winr;
+        q = (qq >= a.max_seed) ? -1 : (int64_t)qq;
+        break;
+      }
+    }
+  }
+  if (warp == 0) {
+    if (q >= 0 && n >= 2) {
+      const uint64_t base = (uint64_t)q / (uint64_t)n;
+      const int r = (int)((uint64_t)q % (uint64_t)n);
+      const uint64_t sa = ck ? base - base % (uint64_t)ck : base;
+      const u2 xb = seed_mixer_d(sa, TAG_SPLITBIT), xa = seed_mixer_d(sa, TAG_LEAF), xg = seed_mixer_d(base, TAG_LEAF);
+      for (int i = lane; i < n; i += 32) {
+        uint4 k = sm.keys[i];
+        u2 kh{k.x, k.y}, kl{k.z, k.w};
+        uint32_t bit = remix_top_d(kh, kl, xb);
+        u2 v = remix_d(kh, kl, bit ? xg : xa);
+        uint32_t h0, h1;
+        leaf_pair_d(v, (uint32_t)n, (uint32_t)(n - 1), h0, h1);
+        if (bit) {
+          h0 = (h0 + r) % n;
+          h1 = (h1 + r) % n;
+        }
+        sm.eu[i] = (uint8_t)h0;
+        sm.ev[i] = (uint8_t)h1;
+      }
+    }
+    leaf_finish<TW>(a, sm, k0, n, q, o, evals, passes, aev, lane);
+  }
+  team_sync<TW>(team);
+}
+
+}  // namespace shk

@@ -16,139 +16,9 @@
 // scratch buffer, in place.
 #include "shk_common.cuh"
 #include "shk_kernels.h"
+#include "shk_split_dev.cuh"
 
 namespace shk {
-
-// Part index of split hash value r against cumulative bounds (up to 4 parts).
-SHK_D uint32_t part_of(uint32_t r, uint32_t b0, uint32_t b1, uint32_t b2) {
-  return (uint32_t)(r >= b0) + (uint32_t)(r >= b1) + (uint32_t)(r >= b2);
-}
-
-// Stable partition of a node's keys by part (recsplit.py:558-561): ballots
-// rank every key within its part, keys go to tmp and are copied back.
-SHK_D void split_partition(const ulonglong2* kp, ulonglong2* kw, ulonglong2* tmp, const ShkSplitTask& task,
-                           int64_t seed, int lane, unsigned lt) {
-  const int m = task.m;
-  const uint32_t um = (uint32_t)m;
-  uint32_t b[3], cur[4];
-  {
-    uint32_t acc = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      cur[j] = acc;
-      acc += (j < task.fanout) ? (uint32_t)task.sizes[j] : 0u;
-      if (j < 3) b[j] = (j < task.fanout - 1) ? acc : um;
-    }
-  }
-  const u2 x = seed_mixer_d((uint64_t)seed, TAG_SPLIT);
-  for (int c = 0; c < m; c += 32) {
-    const int i = c + lane;
-    const bool in = i < m;
-    ulonglong2 k = make_ulonglong2(0, 0);
-    uint32_t p = 4;
-    if (in) {
-      k = kp[i];
-      u2 v = remix_d(split64(k.x), split64(k.y), x);
-      p = part_of(__umulhi(v.hi, um), b[0], b[1], b[2]);
-    }
-    uint32_t dst = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      unsigned bal = __ballot_sync(FULL_WARP, p == (uint32_t)j);
-      if (p == (uint32_t)j) dst = cur[j] + __popc(bal & lt);
-      cur[j] += __popc(bal);
-    }
-    if (in) tmp[task.start + dst] = k;
-  }
-  __syncwarp();
-  for (int i = lane; i < m; i += 32) kw[task.start + i] = tmp[task.start + i];
-  __syncwarp();
-}
-
-// High word of remix(hi, lo, seed, tag) (all the split hash needs).
-SHK_D uint32_t remix_hi_d(u2 k_hi, u2 k_lo, u2 x) {
-  u2 z;
-  z.lo = k_hi.lo ^ x.lo;
-  z.hi = k_hi.hi ^ x.hi;
-  z = mix64_d(z);
-  z.lo ^= k_lo.lo;
-  z.hi ^= k_lo.hi;
-  z = mulc<MUL1>(xorshr<30>(z));
-  z = mulc<MUL2>(xorshr<27>(z));
-  return z.hi ^ __umulhi(z.hi, 2u);  // hi word of z ^ (z >> 31)
-}
-
-// Fast minimum-seed search for a node with F parts (build path).
-// hash_range(v, m) >= b  <=>  v.hi >= ceil(b * 2^32 / m), so parts are
-// counted by comparing the remixed high word against F-1 precomputed
-// thresholds (thermometer counts g_j = #keys with part >= j).  Overflow is
-// checked once per 8 keys (it is monotone, so the seed verdict is exact);
-// the exact first-failing key index (the reference's `evals`) is not tracked
-// here — split_search_exact does that for the seam API.
-template <int F>
-SHK_D int64_t split_search_fast(const ulonglong2* kp, const ShkSplitTask& task, uint64_t max_seed, int lane) {
-  const int m = task.m;
-  uint32_t T0 = 0, T1 = 0, T2 = 0;
-  {
-    uint64_t acc = 0;
-    acc += (uint64_t)task.sizes[0];
-    T0 = (uint32_t)(((acc << 32) + (uint64_t)m - 1) / (uint64_t)m);
-    if (F > 2) {
-      acc += (uint64_t)task.sizes[1];
-      T1 = (uint32_t)(((acc << 32) + (uint64_t)m - 1) / (uint64_t)m);
-    }
-    if (F > 3) {
-      acc += (uint64_t)task.sizes[2];
-      T2 = (uint32_t)(((acc << 32) + (uint64_t)m - 1) / (uint64_t)m);
-    }
-  }
-  const int s0 = task.sizes[0], s1 = task.sizes[1], s2 = F > 2 ? task.sizes[2] : 0, s3 = F > 3 ? task.sizes[3] : 0;
-  for (uint64_t R = 0; R < max_seed; R += 32) {
-    const uint64_t s = R + lane;
-    const u2 x = seed_mixer_d(s, TAG_SPLIT);
-    int g1 = 0, g2 = 0, g3 = 0;
-    bool fail = !(s < max_seed);
-    bool all_failed = false;
-    int i = 0;
-    for (; i + 8 <= m; i += 8) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const ulonglong2 k = __ldg(kp + i + u);
-        const uint32_t vh = remix_hi_d(split64(k.x), split64(k.y), x);
-        g1 += (vh >= T0);
-        if (F > 2) g2 += (vh >= T1);
-        if (F > 3) g3 += (vh >= T2);
-      }
-      const int done = i + 8;
-      bool ovf = (done - g1 > s0);
-      if (F == 2) ovf |= (g1 > s1);
-      if (F == 3) ovf |= (g1 - g2 > s1) | (g2 > s2);
-      if (F == 4) ovf |= (g1 - g2 > s1) | (g2 - g3 > s2) | (g3 > s3);
-      fail |= ovf;
-      if (__all_sync(FULL_WARP, fail)) {
-        all_failed = true;
-        break;
-      }
-    }
-    if (!all_failed) {
-      for (; i < m; ++i) {
-        const ulonglong2 k = __ldg(kp + i);
-        const uint32_t vh = remix_hi_d(split64(k.x), split64(k.y), x);
-        g1 += (vh >= T0);
-        if (F > 2) g2 += (vh >= T1);
-        if (F > 3) g3 += (vh >= T2);
-      }
-      bool ovf = (m - g1 > s0);
-      if (F == 2) ovf |= (g1 > s1);
-      if (F == 3) ovf |= (g1 - g2 > s1) | (g2 > s2);
-      if (F == 4) ovf |= (g1 - g2 > s1) | (g2 - g3 > s2) | (g3 > s3);
-      fail |= ovf;
-    }
-    const unsigned ab = __ballot_sync(FULL_WARP, !fail);
-    if (ab) return (int64_t)(R + (uint64_t)(__ffs(ab) - 1));
-  }
-  return -1;
-}
 
 __global__ void __launch_bounds__(256) split_kernel(ShkSplitLaunch a) {
   const int lane = threadIdx.x & 31;

@@ -1,0 +1,149 @@
+// Persistent construction kernel: every split node and every leaf of a
+// bucket range in ONE launch, scheduled through a device task queue.
+//
+// The per-level schedule (one launch per tree depth, then one leaf launch)
+// pays a tail at every level: the slowest node of a level (trial counts are
+// geometric, the worst of ~1e4 nodes needs ~10x the mean) runs alone while
+// the rest of the GPU idles.  Here each warp pops a ready node from a global
+// queue, solves it (split: minimum seed + stable partition; leaf: ShockHash
+// search + orientation) and publishes the node's children, so the tail of one
+// level overlaps the work of every other level and of the leaves.
+//
+// Queue protocol: slots are pre-sized to the node count.  The initial slots
+// hold the bucket roots; a producer reserves slots with atomicAdd on the tail
+// and publishes child ids with release stores after a __threadfence() that
+// orders its key partition before them; a consumer takes the next slot with
+// atomicAdd on the head and waits (nanosleep) until the id is published, then
+// fences (which also drops stale L1 lines of keys partitioned on another SM).
+// Every unpublished node is a child of a node that some warp is executing,
+// so a waiting warp always gets its task; warps exit once head >= node count.
+// Results are exactly those of the per-level schedule: every node sees the
+// same keys in the same order and runs the same minimum-seed search.
+#include "shk_kernels.h"
+#include "shk_leaf_dev.cuh"
+#include "shk_split_dev.cuh"
+
+namespace shk {
+
+struct TreeArgs {
+  ulonglong2* keys;
+  ulonglong2* tmp;
+  const ShkTreeNode* nodes;
+  int64_t nnodes;
+  int64_t* queue;
+  unsigned long long* head;
+  unsigned long long* tail;
+  uint64_t max_seed;
+  int64_t* seeds;
+  int* exhausted;
+  LeafArgs leaf;
+};
+
+SHK_D int64_t load_published(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+SHK_D void publish(int64_t* p, int64_t v) {
+  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <bool WIDE, int MODE>
+__global__ void __launch_bounds__(128) tree_kernel(TreeArgs t) {
+  __shared__ LeafSmem<1> sm_all[4];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  LeafSmem<1>& sm = sm_all[w];
+  for (;;) {
+    unsigned long long h = 0;
+    if (lane == 0) h = atomicAdd(t.head, 1ull);
+    h = __shfl_sync(FULL_WARP, h, 0);
+    if (h >= (unsigned long long)t.nnodes) break;
+    int64_t id = -1;
+    if (lane == 0) {
+      while ((id = load_published(t.queue + h)) < 0) __nanosleep(200);
+    }
+    id = __shfl_sync(FULL_WARP, id, 0);
+    __threadfence();  // acquire side for all lanes; invalidates stale L1 lines
+    const ShkTreeNode nd = t.nodes[id];
+    if (nd.kind == 0) {
+      ShkSplitTask task;
+      task.start = nd.start;
+      task.m = nd.m;
+      task.fanout = nd.fanout;
+      for (int k = 0; k < 4; ++k) task.sizes[k] = nd.sizes[k];
+      task.seed_slot = id;
+      const ulonglong2* kp = t.keys + nd.start;
+      const int64_t seed = nd.fanout == 2 ? split_search_fast<2>(kp, task, t.max_seed, lane)
+                           : nd.fanout == 3 ? split_search_fast<3>(kp, task, t.max_seed, lane)
+                                            : split_search_fast<4>(kp, task, t.max_seed, lane);
+      if (lane == 0) {
+        t.seeds[id] = seed;
+        if (seed < 0 && t.exhausted) atomicOr(t.exhausted, 1);
+      }
+      if (seed >= 0) split_partition(kp, t.keys, t.tmp, task, seed, lane, lt);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        // children are published even after a failed search (the build is
+        // flagged exhausted) so that no consumer waits forever
+        const unsigned long long pos = atomicAdd(t.tail, (unsigned long long)nd.fanout);
+        for (int k = 0; k < nd.fanout; ++k) publish(t.queue + pos + k, nd.child[k]);
+      }
+    } else {
+      const LeafOut o{id, -1};
+      if (MODE == 0)
+        solve_plain<1, WIDE>(t.leaf, sm, nd.start, nd.m, o, 0, 0, lane, lane);
+      else
+        solve_rotate<1, WIDE>(t.leaf, sm, nd.start, nd.m, o, 0, 0, lane, lane);
+    }
+  }
+}
+
+}  // namespace shk
+
+using namespace shk;
+
+int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
+  if (p.nnodes <= 0) return 0;
+  TreeArgs t;
+  t.keys = reinterpret_cast<ulonglong2*>(p.keys);
+  t.tmp = reinterpret_cast<ulonglong2*>(p.tmp);
+  t.nodes = p.nodes;
+  t.nnodes = p.nnodes;
+  t.queue = p.queue;
+  t.head = p.head;
+  t.tail = p.tail;
+  t.max_seed = p.max_seed;
+  t.seeds = p.seeds;
+  t.exhausted = p.exhausted;
+  LeafArgs& a = t.leaf;
+  a = LeafArgs{};
+  a.hi = p.keys;
+  a.lo = p.keys + 1;
+  a.stride = 2;
+  a.max_seed = p.max_seed;
+  a.mode = p.mode;
+  a.cache_k = p.cache_k;
+  a.cache_min_leaf = p.cache_min_leaf;
+  a.seed_out = p.seeds;
+  a.choice_out = p.choice_out;
+  a.stats_acc = p.stats_acc;
+  a.exhausted = p.exhausted;
+  a.place_out = p.place_out;
+  const bool wide = p.max_n > 32;
+  void (*kfn)(TreeArgs);
+  if (p.mode == 0)
+    kfn = wide ? tree_kernel<true, 0> : tree_kernel<false, 0>;
+  else
+    kfn = wide ? tree_kernel<true, 1> : tree_kernel<false, 1>;
+  int occ = 0;
+  SHK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, 0));
+  if (occ < 1) occ = 1;
+  const int sms = p.num_sms > 0 ? p.num_sms : 148;
+  kfn<<<(unsigned)(sms * occ), 128, 0, st>>>(t);
+  SHK_LAUNCHED();
+  return 0;
+}

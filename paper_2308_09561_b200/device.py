@@ -68,6 +68,7 @@ class timer:
 
 OPT_EXACT_SPLIT_EVALS = 0
 OPT_LEAF_TEAM_WARPS = 1
+OPT_SCHEDULE = 2  # 0 persistent task queue (default), 1 one launch per tree level
 
 
 def set_option(opt: int, value: int):
