@@ -644,13 +644,7 @@ int shk_blake2b128_fixed(shk_ctx* c, const uint8_t* blob, int key_len, int64_t N
 // ---------------------------------------------------------------------------
 // Plans: host tables derived from the reference's flattened plan arrays.
 
-struct PlanNode {
-  int32_t kind, g, m, fanout;
-  int32_t sizes[4];
-  int32_t child[4];
-  int32_t off;    // key offset inside the bucket
-  int32_t depth;
-};
+using PlanNode = ShkPlanNode;
 struct PlanSet {
   std::vector<int64_t> plan_m;
   std::vector<int64_t> plan_off;  // nplans+1
@@ -898,105 +892,133 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   }
   node_base[nbr] = nn;
   b->nnodes = nn;
-  // ---- node tables, split tasks per depth, leaf CSR
-  std::vector<int32_t> ng((size_t)nn);
-  std::vector<uint8_t> nkind((size_t)nn);
-  std::vector<std::vector<ShkSplitTask>> tasks((size_t)S.max_depth + 1);
-  std::vector<int64_t> leaf_off, leaf_slot;
-  leaf_off.reserve((size_t)(b->N / 8 + 16));
+  // ---- per-plan facts: leaf count, largest leaf, validation
   const bool use_tree = c->opt[SHK_OPT_SCHEDULE] == 0 && !c->opt[SHK_OPT_EXACT_SPLIT_EVALS];
-  std::vector<ShkTreeNode> tnodes(use_tree ? (size_t)nn : 0);
-  std::vector<int64_t> tqueue;
-  if (use_tree) tqueue.assign((size_t)nn, -1);
-  int64_t nroots = 0;
+  const int64_t nplans = (int64_t)S.plan_m.size();
+  std::vector<int64_t> plan_leaves((size_t)nplans, 0);
+  std::vector<char> plan_used((size_t)nplans, 0);
+  for (int64_t i = 0; i < nbr; ++i)
+    if (bplan[i] >= 0) plan_used[bplan[i]] = 1;
   int max_leaf = 0;
-  for (int64_t i = 0; i < nbr; ++i) {
-    if (bplan[i] < 0) continue;
-    const int64_t bu = b0 + i;
-    const int64_t kstart = (int64_t)b->h_prefix[bu];
-    const int64_t pa = S.plan_off[bplan[i]], pb = S.plan_off[bplan[i] + 1];
-    if (use_tree) tqueue[nroots++] = node_base[i];
-    for (int64_t j = pa; j < pb; ++j) {
+  for (int64_t pl = 0; pl < nplans; ++pl) {
+    if (!plan_used[pl]) continue;
+    for (int64_t j = S.plan_off[pl]; j < S.plan_off[pl + 1]; ++j) {
       const PlanNode& nd = S.nodes[j];
-      const int64_t slot = node_base[i] + (j - pa);
-      ng[slot] = nd.g;
-      nkind[slot] = (uint8_t)(nd.kind != 0);
-      if (use_tree) {
-        ShkTreeNode& tn = tnodes[slot];
-        tn.start = kstart + nd.off;
-        tn.m = nd.m;
-        tn.kind = nd.kind != 0;
-        tn.fanout = nd.kind == 0 ? nd.fanout : 0;
-        for (int k = 0; k < 4; ++k) {
-          tn.sizes[k] = nd.sizes[k];
-          tn.child[k] = (nd.kind == 0 && k < nd.fanout) ? node_base[i] + nd.child[k] : -1;
-        }
+      if (nd.kind == 0 && nd.m >= 32768) {
+        shk_set_error("split node of %d keys exceeds the 32767-key split kernel limit", nd.m);
+        return SHK_INVALID;
       }
-      if (nd.kind == 0) {
-        if (nd.m >= 32768) {
-          shk_set_error("split node of %d keys exceeds the 32767-key split kernel limit", nd.m);
-          return SHK_INVALID;
-        }
-        ShkSplitTask t{};
-        t.start = kstart + nd.off;
-        t.m = nd.m;
-        t.fanout = nd.fanout;
-        for (int k = 0; k < 4; ++k) t.sizes[k] = nd.sizes[k];
-        t.seed_slot = slot;
-        tasks[nd.depth].push_back(t);
-      } else {
+      if (nd.kind != 0) {
         if (nd.m < 1 || nd.m > 64) {
           shk_set_error("leaf of %d keys outside 1..64", nd.m);
           return SHK_INVALID;
         }
-        leaf_off.push_back(kstart + nd.off);
-        leaf_slot.push_back(slot);
+        ++plan_leaves[pl];
         if (nd.m > max_leaf) max_leaf = nd.m;
       }
     }
   }
-  int64_t L = (int64_t)leaf_off.size();
-  const int64_t n_leaves = L;
-  // leaves are contiguous in key order: CSR end = range end
-  leaf_off.push_back((int64_t)b->h_prefix[b1]);
+  int64_t n_leaves = 0;
+  for (int64_t i = 0; i < nbr; ++i)
+    if (bplan[i] >= 0) n_leaves += plan_leaves[bplan[i]];
+  // ---- node tables: on the device for the persistent schedule, on the host
+  // (split tasks per depth + leaf CSR) for the per-level schedule
+  std::vector<int32_t> ng;
+  std::vector<uint8_t> nkind;
+  std::vector<std::vector<ShkSplitTask>> tasks((size_t)S.max_depth + 1);
+  std::vector<int64_t> leaf_off, leaf_slot;
+  std::vector<int64_t> kstart_v, root_pos;
+  int64_t nroots = 0;
+  if (use_tree) {
+    kstart_v.resize((size_t)nbr);
+    root_pos.resize((size_t)nbr);
+    for (int64_t i = 0; i < nbr; ++i) {
+      kstart_v[i] = (int64_t)b->h_prefix[b0 + i];
+      root_pos[i] = bplan[i] >= 0 ? nroots++ : -1;
+    }
+  } else {
+    ng.resize((size_t)nn);
+    nkind.resize((size_t)nn);
+    leaf_off.reserve((size_t)n_leaves + 1);
+    for (int64_t i = 0; i < nbr; ++i) {
+      if (bplan[i] < 0) continue;
+      const int64_t kstart = (int64_t)b->h_prefix[b0 + i];
+      const int64_t pa = S.plan_off[bplan[i]], pb = S.plan_off[bplan[i] + 1];
+      for (int64_t j = pa; j < pb; ++j) {
+        const PlanNode& nd = S.nodes[j];
+        const int64_t slot = node_base[i] + (j - pa);
+        ng[slot] = nd.g;
+        nkind[slot] = (uint8_t)(nd.kind != 0);
+        if (nd.kind == 0) {
+          ShkSplitTask t{};
+          t.start = kstart + nd.off;
+          t.m = nd.m;
+          t.fanout = nd.fanout;
+          for (int k = 0; k < 4; ++k) t.sizes[k] = nd.sizes[k];
+          t.seed_slot = slot;
+          tasks[nd.depth].push_back(t);
+        } else {
+          leaf_off.push_back(kstart + nd.off);
+          leaf_slot.push_back(slot);
+        }
+      }
+    }
+    leaf_off.push_back((int64_t)b->h_prefix[b1]);  // leaves are contiguous: CSR end = range end
+  }
+  int64_t L = use_tree ? 0 : (int64_t)leaf_slot.size();
   // ---- device tables
   DBuf dseeds(c), dg(c), dkind(c), dtasks(c), dloff(c), dlslot(c), dlen(c), dpos(c), dnb(c), dbo(c), dacc(c),
       dscan(c);
   RC(dseeds.alloc((size_t)(nn + 1) * 8));
   RC(dg.alloc((size_t)(nn + 1) * 4));
   RC(dkind.alloc((size_t)(nn + 1)));
-  RC(h2d(c, dg.p, ng.data(), (size_t)nn * 4));
-  RC(h2d(c, dkind.p, nkind.data(), (size_t)nn));
-  size_t ntask_total = 0;
-  for (auto& v : tasks) ntask_total += v.size();
-  RC(dtasks.alloc((ntask_total + 1) * sizeof(ShkSplitTask)));
-  {
+  RC(dacc.alloc(64));
+  SHK_CUDA(cudaMemsetAsync(dacc.p, 0, 64, c->stream));
+  int* exh = c->d_counter + 4;
+  SHK_CUDA(cudaMemsetAsync(exh, 0, 4, c->stream));
+  if (!use_tree) {
+    RC(h2d(c, dg.p, ng.data(), (size_t)nn * 4));
+    RC(h2d(c, dkind.p, nkind.data(), (size_t)nn));
+    size_t ntask_total = 0;
+    for (auto& v : tasks) ntask_total += v.size();
+    RC(dtasks.alloc((ntask_total + 1) * sizeof(ShkSplitTask)));
     size_t o = 0;
     for (auto& v : tasks) {
       RC(h2d(c, dtasks.as<char>() + o * sizeof(ShkSplitTask), v.data(), v.size() * sizeof(ShkSplitTask)));
       o += v.size();
     }
+    RC(dloff.alloc((size_t)(L + 1) * 8));
+    RC(dlslot.alloc((size_t)(L + 1) * 8));
+    RC(h2d(c, dloff.p, leaf_off.data(), (size_t)(L + 1) * 8));
+    RC(h2d(c, dlslot.p, leaf_slot.data(), (size_t)L * 8));
   }
-  RC(dloff.alloc((size_t)(L + 1) * 8));
-  RC(dlslot.alloc((size_t)(L + 1) * 8));
-  RC(h2d(c, dloff.p, leaf_off.data(), (size_t)(L + 1) * 8));
-  RC(h2d(c, dlslot.p, leaf_slot.data(), (size_t)L * 8));
-  RC(dacc.alloc(64));
-  SHK_CUDA(cudaMemsetAsync(dacc.p, 0, 64, c->stream));
-  int* exh = c->d_counter + 4;
-  SHK_CUDA(cudaMemsetAsync(exh, 0, 4, c->stream));
   b->mark(2);
   b->level_reset();
-  DBuf dnodes(c), dqueue(c), dqctl(c);
+  DBuf dnodes(c), dqueue(c), dqctl(c), dpn(c), dpoff(c), dbp(c), dnbase(c), dks(c), droot(c);
   if (use_tree && nn > 0) {
-    // ---- one persistent launch for every split node and leaf (shk_tree.cu)
+    // ---- node table expanded on the device from the (small) plan tables
     RC(dnodes.alloc((size_t)nn * sizeof(ShkTreeNode)));
     RC(dqueue.alloc((size_t)nn * 8));
     RC(dqctl.alloc(256));
-    RC(h2d(c, dnodes.p, tnodes.data(), (size_t)nn * sizeof(ShkTreeNode)));
-    RC(h2d(c, dqueue.p, tqueue.data(), (size_t)nn * 8));
+    RC(dpn.alloc(S.nodes.size() * sizeof(PlanNode) + 16));
+    RC(dpoff.alloc(S.plan_off.size() * 8 + 8));
+    RC(dbp.alloc((size_t)nbr * 4 + 4));
+    RC(dnbase.alloc((size_t)nbr * 8 + 8));
+    RC(dks.alloc((size_t)nbr * 8 + 8));
+    RC(droot.alloc((size_t)nbr * 8 + 8));
+    RC(h2d(c, dpn.p, S.nodes.data(), S.nodes.size() * sizeof(PlanNode)));
+    RC(h2d(c, dpoff.p, S.plan_off.data(), S.plan_off.size() * 8));
+    RC(h2d(c, dbp.p, bplan.data(), (size_t)nbr * 4));
+    RC(h2d(c, dnbase.p, node_base.data(), (size_t)nbr * 8));
+    RC(h2d(c, dks.p, kstart_v.data(), (size_t)nbr * 8));
+    RC(h2d(c, droot.p, root_pos.data(), (size_t)nbr * 8));
+    SHK_CUDA(cudaMemsetAsync(dqueue.p, 0xFF, (size_t)nn * 8, c->stream));
     unsigned long long qc[2] = {0ull, (unsigned long long)nroots};
     RC(h2d(c, dqctl.p, qc, 16));
+    RC(shk_launch_expand_nodes(dpn.as<PlanNode>(), dpoff.as<int64_t>(), dbp.as<int32_t>(), dnbase.as<int64_t>(),
+                               dks.as<int64_t>(), droot.as<int64_t>(), nbr, dnodes.as<ShkTreeNode>(), dg.as<int32_t>(),
+                               dkind.as<uint8_t>(), dqueue.as<int64_t>(), c->stream));
+    // ---- one persistent launch for every split node and leaf (shk_tree.cu)
     ShkTreeLaunch p{};
     p.keys = b->keys.as<uint64_t>();
     p.tmp = b->tmp.as<uint64_t>();
@@ -1021,7 +1043,6 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     p.num_sms = c->num_sms;
     RC(shk_launch_tree(p, c->stream));
     b->mark(3);
-    L = 0;  // leaves already solved
   }
   // ---- splits, level by level (every node of one depth in one launch)
   if (!use_tree) {

@@ -63,6 +63,21 @@ struct ShkSplitLaunch {
 };
 int shk_launch_split(const ShkSplitLaunch& p, cudaStream_t st);
 
+// A node of a bucket-size plan (recsplit.flatten_plan + derived fields).
+struct ShkPlanNode {
+  int32_t kind, g, m, fanout;
+  int32_t sizes[4];
+  int32_t child[4];  // plan-local child indices
+  int32_t off;       // key offset inside the bucket
+  int32_t depth;
+};
+// Expand per-bucket plans into the global node table of a bucket range:
+// nodes, Rice g / kind per node, and the root of every bucket in the queue.
+int shk_launch_expand_nodes(const ShkPlanNode* plan_nodes, const int64_t* plan_off, const int32_t* bucket_plan,
+                            const int64_t* node_base, const int64_t* key_start, const int64_t* root_pos,
+                            int64_t nbuckets, struct ShkTreeNode* nodes, int32_t* node_g, uint8_t* node_kind,
+                            int64_t* queue, cudaStream_t st);
+
 // One node of a bucket range for the persistent construction kernel.
 struct ShkTreeNode {
   int64_t start;     // first key (global index into the working key array)

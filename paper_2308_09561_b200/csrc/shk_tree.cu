@@ -102,9 +102,52 @@ __global__ void __launch_bounds__(128) tree_kernel(TreeArgs t) {
   }
 }
 
+// One CTA per bucket: copy its plan's nodes into the global node table.
+__global__ void expand_nodes_kernel(const ShkPlanNode* pn, const int64_t* plan_off, const int32_t* bucket_plan,
+                                    const int64_t* node_base, const int64_t* key_start, const int64_t* root_pos,
+                                    int64_t nbuckets, ShkTreeNode* nodes, int32_t* node_g, uint8_t* node_kind,
+                                    int64_t* queue) {
+  for (int64_t bu = blockIdx.x; bu < nbuckets; bu += gridDim.x) {
+    const int32_t plan = bucket_plan[bu];
+    if (plan < 0) continue;
+    const int64_t pa = plan_off[plan], cnt = plan_off[plan + 1] - pa;
+    const int64_t nb = node_base[bu], ks = key_start[bu];
+    if (threadIdx.x == 0) queue[root_pos[bu]] = nb;
+    for (int64_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const ShkPlanNode p = pn[pa + j];
+      ShkTreeNode t;
+      t.start = ks + p.off;
+      t.m = p.m;
+      t.kind = p.kind != 0;
+      t.fanout = p.kind == 0 ? p.fanout : 0;
+      t.pad = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        t.sizes[k] = p.sizes[k];
+        t.child[k] = (p.kind == 0 && k < p.fanout) ? nb + p.child[k] : -1;
+      }
+      nodes[nb + j] = t;
+      node_g[nb + j] = p.g;
+      node_kind[nb + j] = (uint8_t)(p.kind != 0);
+    }
+  }
+}
+
 }  // namespace shk
 
 using namespace shk;
+
+int shk_launch_expand_nodes(const ShkPlanNode* plan_nodes, const int64_t* plan_off, const int32_t* bucket_plan,
+                            const int64_t* node_base, const int64_t* key_start, const int64_t* root_pos,
+                            int64_t nbuckets, ShkTreeNode* nodes, int32_t* node_g, uint8_t* node_kind, int64_t* queue,
+                            cudaStream_t st) {
+  if (nbuckets <= 0) return 0;
+  int64_t g = nbuckets < 148 * 16 ? nbuckets : 148 * 16;
+  expand_nodes_kernel<<<(unsigned)g, 128, 0, st>>>(plan_nodes, plan_off, bucket_plan, node_base, key_start, root_pos,
+                                                   nbuckets, nodes, node_g, node_kind, queue);
+  SHK_LAUNCHED();
+  return 0;
+}
 
 int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   if (p.nnodes <= 0) return 0;
