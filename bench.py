@@ -177,7 +177,9 @@ def cpu_baseline_sample(seconds_target=15.0):
 def run_ours(args):
     rank, world, local = dist_info()
     os.environ.setdefault("SHK_DEVICE", str(local))
-    if world > 1:
+    # SHK_FORCE_SHARDED=1 runs the sharded (NCCL) path even at world size 1
+    sharded = world > 1 or os.environ.get("SHK_FORCE_SHARDED") == "1"
+    if sharded:
         import torch
         import torch.distributed as dist
 
@@ -199,7 +201,7 @@ def run_ours(args):
     dev.sync()
 
     def step():
-        if world == 1:
+        if not sharded:
             d = recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"])
             return d, d.device_profile
         d, prof = shdist.build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"],
@@ -303,6 +305,10 @@ def run_ours(args):
         line["roofline"] = roofline_numbers(prof, hash_evals, n, clocks.get("sm_mhz"), sms)
     if query:
         line["query"] = query
+    if world == 1 and args.leaf_configs:
+        line["leaf_search"] = {}
+        for cfg in [int(x) for x in args.leaf_configs.split(",") if x]:
+            line["leaf_search"][f"C{cfg}"] = bench_leaf(cfg, args, dev, sms, clocks.get("sm_mhz"))
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
@@ -343,6 +349,58 @@ def bench_queries(desc, k, args, dev, sms):
         if os.path.exists(gpath):
             res["matches_reference"] = qsha == json.load(open(gpath))["query_sha"]
     for b_ in (d_qhi, d_qlo, d_out):
+        b_.free()
+    return res
+
+
+def bench_leaf(cfg, args, dev, sms, clock_mhz):
+    """Leaf-search-only configs (BASELINE configs C1/C3/C5): leaf seeds tested/s."""
+    from paper_2308_09561_b200 import workloads as W
+    from paper_2308_09561_b200._kernels import kernels as K
+
+    spec = W.LEAF_CONFIGS[cfg]
+    L, n = spec["leaves"], spec["n"]
+    if cfg == 5:
+        fp = np.random.default_rng(5).integers(0, 2**64, (L, n, 2), dtype=np.uint64)
+        d_hi = dev.DeviceBuffer.from_host(np.ascontiguousarray(fp[..., 0]).ravel())
+        d_lo = dev.DeviceBuffer.from_host(np.ascontiguousarray(fp[..., 1]).ravel())
+    else:
+        k = W.raw_keys(cfg, L * n)
+        d_blob = dev.DeviceBuffer.from_host(np.frombuffer(np.ascontiguousarray(k, dtype="<u8").tobytes(), np.uint8))
+        d_hi = dev.DeviceBuffer(8 * L * n)
+        d_lo = dev.DeviceBuffer(8 * L * n)
+        dev.blake2b_fixed_device(d_blob, 8, L * n, 0, d_hi, d_lo)
+        d_blob.free()
+    d_off = dev.DeviceBuffer.from_host(np.arange(0, (L + 1) * n, n, dtype=np.int64))
+    d_seed = dev.DeviceBuffer(8 * L)
+    d_fb = dev.DeviceBuffer(8 * L)
+    run = lambda: K.leaf_search_device(d_hi.ptr, d_lo.ptr, d_off.ptr, L, 0, d_seed.ptr, d_fb.ptr)
+    if cfg != 5:
+        run()  # warm-up
+    dev.sync()
+    reps = 1 if cfg == 5 else max(1, args.leaf_reps)
+    with dev.timer() as tm:
+        for _ in range(reps):
+            run()
+    ms = tm.ms / reps
+    seeds = d_seed.download(np.int64, L)
+    seeds_tested = float((seeds + 1).sum())
+    w_key = 50 if n <= 32 else 53
+    ops = seeds_tested * (n * w_key + W_SEED)
+    peak = INT_OPS_PER_CLK_SM * sms * 1965e6 / 1e12
+    res = {"config": f"C{cfg}: {L} leaves x n={n}, plain", "seeds_tested": int(seeds_tested),
+           "mean_seeds_per_leaf": round(seeds_tested / L, 1), "ms": round(ms, 3),
+           "value": round(seeds_tested / (ms * 1e-3), 1), "unit": "leaf seeds tested/s",
+           "roofline": {"bound": "int32-issue", "achieved": round(ops / (ms * 1e-3) / 1e12, 3),
+                        "peak": round(peak, 2), "unit": "Tops/s", "frac": round(ops / (ms * 1e-3) / 1e12 / peak, 4),
+                        "work": f"(seed+1) x (n x {w_key} + {W_SEED}) int32 ops"}}
+    gpath = os.path.join(ROOT, "tests", "golden", f"c{cfg}.json")
+    if os.path.exists(gpath):
+        g = json.load(open(gpath))
+        kk = len(g["seeds"])
+        res["parity"] = {"leaves_checked": kk, "seeds_match_reference": seeds[:kk].tolist() == g["seeds"],
+                         "fbits_match_reference": d_fb.download(np.uint64, kk).tolist() == g["fbits"]}
+    for b_ in (d_hi, d_lo, d_off, d_seed, d_fb):
         b_.free()
     return res
 
@@ -390,6 +448,8 @@ def main():
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--leaf-configs", default="1,3", help="leaf-search-only configs to add (C1,C3,C5)")
+    ap.add_argument("--leaf-reps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
     if args.impl == "reference":

@@ -117,6 +117,14 @@ def leaf_search_batch(hi, lo, leaf_off, mode, cache_k=0, cache_min_leaf=0, max_s
     return seeds, fb, st
 
 
+def leaf_search_device(hi_ptr, lo_ptr, off_ptr, L, mode, seeds_ptr, fbits_ptr=None, stats_ptr=None, cache_k=0,
+                       cache_min_leaf=0, max_seed=1 << 40, team_warps=0):
+    """Stream-ordered batched leaf search on device pointers (bench path)."""
+    check(_L().shk_leaf_search(ctx(), int(mode), int(cache_k), int(cache_min_leaf), hi_ptr, lo_ptr, off_ptr, int(L),
+                               int(max_seed), int(team_warps), seeds_ptr, fbits_ptr, stats_ptr, SHK_DEVICE),
+          "leaf search")
+
+
 def _one_leaf(hi, lo, n, mode, cache_k, max_seed):
     hi = u64(hi)
     lo = u64(lo)

@@ -19,7 +19,8 @@ from ..errors import (
     ShockHashError,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "_lib", "libshockhash_b200.so")
+LIB_PATH = os.environ.get("SHK_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "_lib", "libshockhash_b200.so")
 
 SHK_OK, SHK_EXHAUSTED, SHK_FORMAT, SHK_INVALID, SHK_UNSOLVABLE, SHK_DUPLICATE = range(6)
 SHK_DEVICE = 1

@@ -119,10 +119,29 @@ SHK_D uint64_t join64(uint32_t lo, uint32_t hi) {
 
 // z ^= z >> S in 32-bit halves; the high-word shift goes to the FMA pipe as
 // IMAD.HI(hi, 2^(32-S)).
+#ifndef SHK_ALU_SHIFTS
+#define SHK_ALU_SHIFTS 0
+#endif
+template <int S>
+SHK_D u2 xorshr_alu(u2 z);
 template <int S>
 SHK_D u2 xorshr(u2 z) {
+  if (SHK_ALU_SHIFTS) return xorshr_alu<S>(z);
   uint32_t lo_sh = __funnelshift_r(z.lo, z.hi, S);       // (z >> S) low word
   uint32_t hi_sh = __umulhi(z.hi, 1u << (32 - S));        // (z >> S) high word
+  u2 r;
+  r.lo = z.lo ^ lo_sh;
+  r.hi = z.hi ^ hi_sh;
+  return r;
+}
+
+// Same with the high-word shift on the ALU pipe (SHF): the split search's
+// loop is FMA-pipe bound (IMAD.WIDE), measured +7% (tools/remix_variants.cu).
+template <int S>
+SHK_D u2 xorshr_alu(u2 z) {
+  uint32_t lo_sh = __funnelshift_r(z.lo, z.hi, S);
+  uint32_t hi_sh;
+  asm("shr.b32 %0, %1, %2;" : "=r"(hi_sh) : "r"(z.hi), "n"(S));
   u2 r;
   r.lo = z.lo ^ lo_sh;
   r.hi = z.hi ^ hi_sh;

@@ -42,10 +42,12 @@ struct LeafArgs {
   int64_t* place_out;   // optional [N]: global slot of each key (leaf start + its cell)
 };
 
-template <int TW>
+// MAXE: most keys per leaf the team's buffers hold (64, or 40 to fit more
+// warps per SM when the build's leaves are small enough).
+template <int TW, int MAXE = 64>
 struct LeafSmem {
-  uint4 keys[64];                 // (hi.lo, hi.hi, lo.lo, lo.hi)
-  uint16_t edges[TW][64 * 32];    // per-lane packed edges, column per lane
+  uint4 keys[MAXE];               // (hi.lo, hi.hi, lo.lo, lo.hi)
+  uint16_t edges[TW][MAXE * 32];  // per-lane packed edges, column per lane
   int64_t slot_win[2][TW];        // per-warp lowest accepting candidate (or -1)
   int32_t slot_r[2][TW];          // rotation of that candidate
   uint64_t slot_pass_le[2][TW];   // passes at candidates <= winner in warp
@@ -54,8 +56,8 @@ struct LeafSmem {
   uint64_t slot_evals[2][TW];
   uint64_t slot_aev_le[2][TW];
   uint64_t slot_aev[2][TW];
-  uint8_t eu[64], ev[64];
-  uint64_t inc[64];
+  uint8_t eu[MAXE], ev[MAXE];
+  uint64_t inc[MAXE];
   WarpChk chk[TW];                // per-warp scratch of the exact check
   int64_t leaf;
 };
@@ -76,8 +78,8 @@ struct LeafOut {
   int64_t leaf_index;  // index into fbits_out / stats_out (or -1)
 };
 
-template <int TW>
-SHK_D void load_leaf_keys(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, int tt) {
+template <int TW, class SM>
+SHK_D void load_leaf_keys(const LeafArgs& a, SM& sm, int64_t k0, int n, int tt) {
   for (int i = tt; i < n; i += TW * 32) {
     u2 h = split64(a.hi[(k0 + i) * a.stride]), l = split64(a.lo[(k0 + i) * a.stride]);
     sm.keys[i] = make_uint4(h.lo, h.hi, l.lo, l.hi);
@@ -86,8 +88,8 @@ SHK_D void load_leaf_keys(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n
 
 // Orientation of the final edges in sm.eu/sm.ev (warp 0 of the team) and
 // result stores.
-template <int TW>
-SHK_D void leaf_finish(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, int64_t q, const LeafOut& o,
+template <int TW, class SM>
+SHK_D void leaf_finish(const LeafArgs& a, SM& sm, int64_t k0, int n, int64_t q, const LeafOut& o,
                        uint64_t evals, uint64_t passes, uint64_t aev, int lane) {
   if (q >= 0 && n >= 2) {
     __syncwarp();
@@ -157,8 +159,8 @@ SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
 
 // Plain search of one leaf (keys [k0, k0+n)) by a team.  All threads of the
 // team call it; it ends team-synchronized.
-template <int TW, bool WIDE>
-SHK_D void solve_plain(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, const LeafOut& o, int team, int warp,
+template <int TW, bool WIDE, class SM>
+SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafOut& o, int team, int warp,
                        int lane, int tt) {
   load_leaf_keys<TW>(a, sm, k0, n, tt);
   team_sync<TW>(team);
@@ -226,8 +228,8 @@ SHK_D void solve_plain(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, c
 }
 
 // Rotation fitting of one leaf: lane per base seed.
-template <int TW, bool WIDE>
-SHK_D void solve_rotate(const LeafArgs& a, LeafSmem<TW>& sm, int64_t k0, int n, const LeafOut& o, int team,
+template <int TW, bool WIDE, class SM>
+SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafOut& o, int team,
                         int warp, int lane, int tt) {
   load_leaf_keys<TW>(a, sm, k0, n, tt);
   team_sync<TW>(team);

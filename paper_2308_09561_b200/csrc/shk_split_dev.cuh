@@ -62,12 +62,14 @@ SHK_D uint32_t remix_hi_d(u2 k_hi, u2 k_lo, u2 x) {
   u2 z;
   z.lo = k_hi.lo ^ x.lo;
   z.hi = k_hi.hi ^ x.hi;
-  z = mix64_d(z);
+  z = mulc<MUL1>(xorshr_alu<30>(z));
+  z = mulc<MUL2>(xorshr_alu<27>(z));
+  z = xorshr_alu<31>(z);
   z.lo ^= k_lo.lo;
   z.hi ^= k_lo.hi;
-  z = mulc<MUL1>(xorshr<30>(z));
-  z = mulc<MUL2>(xorshr<27>(z));
-  return z.hi ^ __umulhi(z.hi, 2u);  // hi word of z ^ (z >> 31)
+  z = mulc<MUL1>(xorshr_alu<30>(z));
+  z = mulc<MUL2>(xorshr_alu<27>(z));
+  return z.hi ^ (z.hi >> 31);  // hi word of z ^ (z >> 31)
 }
 
 // Fast minimum-seed search for a node with F parts (build path).

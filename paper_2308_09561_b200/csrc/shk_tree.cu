@@ -49,13 +49,15 @@ SHK_D void publish(int64_t* p, int64_t v) {
   asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <bool WIDE, int MODE>
-__global__ void __launch_bounds__(128) tree_kernel(TreeArgs t) {
-  __shared__ LeafSmem<1> sm_all[4];
+// MAXE: leaf buffer capacity; MINB: CTAs per SM requested from ptxas (the
+// 40-key variant fits 10 CTAs = 40 warps per SM in registers and smem).
+template <bool WIDE, int MODE, int MAXE, int MINB>
+__global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
+  __shared__ LeafSmem<1, MAXE> sm_all[4];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  LeafSmem<1>& sm = sm_all[w];
+  LeafSmem<1, MAXE>& sm = sm_all[w];
   for (;;) {
     unsigned long long h = 0;
     if (lane == 0) h = atomicAdd(t.head, 1ull);
@@ -177,11 +179,19 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   a.exhausted = p.exhausted;
   a.place_out = p.place_out;
   const bool wide = p.max_n > 32;
+  const bool small = p.max_n <= 40;
   void (*kfn)(TreeArgs);
-  if (p.mode == 0)
-    kfn = wide ? tree_kernel<true, 0> : tree_kernel<false, 0>;
-  else
-    kfn = wide ? tree_kernel<true, 1> : tree_kernel<false, 1>;
+  if (p.mode == 0) {
+    if (small)
+      kfn = wide ? tree_kernel<true, 0, 40, 8> : tree_kernel<false, 0, 40, 8>;
+    else
+      kfn = tree_kernel<true, 0, 64, 8>;
+  } else {
+    if (small)
+      kfn = wide ? tree_kernel<true, 1, 40, 8> : tree_kernel<false, 1, 40, 8>;
+    else
+      kfn = tree_kernel<true, 1, 64, 8>;
+  }
   int occ = 0;
   SHK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, 0));
   if (occ < 1) occ = 1;
