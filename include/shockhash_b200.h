@@ -140,6 +140,19 @@ int shk_blake2b128(shk_ctx* ctx, const uint8_t* blob, int64_t blob_len, const in
 int shk_blake2b128_fixed(shk_ctx* ctx, const uint8_t* blob, int key_len, int64_t N, uint64_t salt, uint64_t* hi,
                          uint64_t* lo, int flags);
 
+/* ---- analysis entry points of the kernel seam (used by experiments.py).
+ * search_bruteforce (_core.pyx:337-371): minimum seed in [0, max_seed) whose
+ * single n-range hash is a bijection of the n keys (host hi/lo, n <= 64), or
+ * -1; *evals_out = the reference's evals counter.
+ * mc_filter_pass_count (_core.pyx:832-860): seeds in [0, trials) passing the
+ * all-cells-hit filter on the synthetic key set derived from `entropy`.
+ * enumerate_outcomes (_core.pyx:778-829): over all (n^2)^n ordered cell-pair
+ * tuples, the pseudoforest count and the sum of 2^components (n <= 8). */
+int shk_search_bruteforce(shk_ctx* ctx, const uint64_t* hi, const uint64_t* lo, int n, uint64_t max_seed,
+                          int64_t* seed_out, int64_t* evals_out);
+int shk_mc_filter_pass_count(shk_ctx* ctx, int n, int64_t trials, uint64_t entropy, int64_t* passes_out);
+int shk_enumerate_outcomes(shk_ctx* ctx, int n, uint64_t* pf_count_out, uint64_t* sum_2c_out);
+
 /* ---- plan tables (recsplit.flatten_plan, recsplit.py:95-119), one per
  * distinct bucket size, concatenated: plan p covers nodes
  * [plan_off[p], plan_off[p+1]); node fields are the reference's arrays

@@ -43,6 +43,9 @@ _SIGS = {
     "o_rice_decode": (_I, [_P, _I64, _P, _I, _P]),
     "o_build_hashed": (_I64, [_P, _P, _I64, _I64, _I, _I, _I, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "o_search_plain_batch": (None, [_P, _P, _I64, _I, _P]),
+    "o_search_bruteforce": (None, [_P, _P, _I, _I64, _P]),
+    "o_mc_filter_pass_count": (_I64, [_I, _I64, _U64]),
+    "o_enumerate_outcomes": (None, [_I, _P]),
     "o_query": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I64, _U64, _I64,
                      _P, _I64, _P]),
 }
@@ -125,6 +128,23 @@ def search_rotate(hi, lo, n, ck, max_seed):
     out = np.zeros(5, dtype=np.int64)
     lib().o_search_rotate(p(hi), p(lo), int(n), int(ck), int(max_seed), p(out))
     return tuple(int(x) for x in out)
+
+
+def search_bruteforce(hi, lo, n, max_seed):
+    hi, lo = _u64(hi), _u64(lo)
+    out = np.zeros(2, dtype=np.int64)
+    lib().o_search_bruteforce(p(hi), p(lo), int(n), int(max_seed), p(out))
+    return int(out[0]), int(out[1])
+
+
+def mc_filter_pass_count(n, trials, entropy):
+    return int(lib().o_mc_filter_pass_count(int(n), int(trials), int(entropy) & MASK64))
+
+
+def enumerate_outcomes(n):
+    out = np.zeros(2, dtype=np.uint64)
+    lib().o_enumerate_outcomes(int(n), p(out))
+    return int(out[0]), int(out[1])
 
 
 def orient(edges, n):

@@ -669,3 +669,104 @@ int o_query(const uint64_t* hi, const uint64_t* lo, int64_t Q, int64_t nbk, cons
   }
   return 0;
 }
+
+/* ---- analysis entry points of the kernel seam ---------------------------- */
+
+/* search_bruteforce, _core.pyx:337-371 / _pure.py:273-296: out = (seed, evals) */
+void o_search_bruteforce(const uint64_t* hi, const uint64_t* lo, int n, int64_t max_seed, int64_t* out) {
+  uint64_t full = n < 64 ? (((uint64_t)1 << n) - 1) : ~(uint64_t)0;
+  int64_t evals = 0;
+  for (int64_t s = 0; s < max_seed; ++s) {
+    uint64_t x = o_seed_mixer((uint64_t)s, T_LEAF), mask = 0;
+    int ok = 1;
+    for (int i = 0; i < n; ++i) {
+      uint64_t bit = (uint64_t)1 << o_hash_range(o_mix64(o_mix64(hi[i] ^ x) ^ lo[i]), (uint64_t)n);
+      if (mask & bit) {
+        ok = 0;
+        evals += i + 1;
+        break;
+      }
+      mask |= bit;
+    }
+    if (ok) {
+      evals += n;
+      if (mask == full) {
+        out[0] = s;
+        out[1] = evals;
+        return;
+      }
+    }
+  }
+  out[0] = -1;
+  out[1] = evals;
+}
+
+/* mc_filter_pass_count, _core.pyx:832-860 / _pure.py:624-645 */
+int64_t o_mc_filter_pass_count(int n, int64_t trials, uint64_t ent) {
+  if (n == 1) return trials;
+  uint64_t kh[64], kl[64];
+  for (int i = 0; i < n; ++i) {
+    kh[i] = o_mix64(ent + 2 * (uint64_t)i);
+    kl[i] = o_mix64(ent + 2 * (uint64_t)i + 1);
+  }
+  uint64_t full = n < 64 ? (((uint64_t)1 << n) - 1) : ~(uint64_t)0;
+  int64_t passes = 0;
+  for (int64_t s = 0; s < trials; ++s) {
+    uint64_t x = o_seed_mixer((uint64_t)s, T_LEAF), mask = 0;
+    for (int i = 0; i < n; ++i) {
+      int a, b;
+      pair_x(kh[i], kl[i], x, n, &a, &b);
+      mask |= ((uint64_t)1 << a) | ((uint64_t)1 << b);
+    }
+    passes += mask == full;
+  }
+  return passes;
+}
+
+/* enumerate_outcomes, _core.pyx:778-829 / _pure.py:576-621: odometer over
+ * the n^(2n) tuples with the union-find check; out = (pf_count, sum 2^comps) */
+void o_enumerate_outcomes(int n, uint64_t* out) {
+  int edges[8] = {0};
+  int total = n * n;
+  uint64_t pf = 0, s2 = 0;
+  for (;;) {
+    UF u;
+    for (int i = 0; i < n; ++i) {
+      u.parent[i] = i;
+      u.size[i] = 1;
+      u.pseudo[i] = 0;
+    }
+    int comps = n, ok = 1;
+    for (int i = 0; i < n && ok; ++i) {
+      int a = uf_find(&u, edges[i] / n), b = uf_find(&u, edges[i] % n);
+      if (a == b) {
+        if (u.pseudo[a]) ok = 0;
+        u.pseudo[a] = 1;
+      } else {
+        if (u.pseudo[a] && u.pseudo[b]) {
+          ok = 0;
+          break;
+        }
+        if (u.size[a] < u.size[b]) {
+          int t = a;
+          a = b;
+          b = t;
+        }
+        u.parent[b] = a;
+        u.size[a] += u.size[b];
+        u.pseudo[a] |= u.pseudo[b];
+        --comps;
+      }
+    }
+    if (ok) {
+      ++pf;
+      s2 += (uint64_t)1 << comps;
+    }
+    int i = n - 1;
+    while (i >= 0 && edges[i] == total - 1) edges[i--] = 0;
+    if (i < 0) break;
+    ++edges[i];
+  }
+  out[0] = pf;
+  out[1] = s2;
+}

@@ -264,6 +264,45 @@ def ribbon_build(hi, lo, rhs, m, max_tries=64):
 
 
 # ---------------------------------------------------------------------------
+# Analysis entry points (experiments.py)
+
+
+def search_bruteforce(hi, lo, n, max_seed):
+    """Single-hash bijection retry: (seed or -1, evals) (_core.pyx:337-371)."""
+    n = int(n)
+    if n < 0 or n > 64:
+        raise InvalidParameterError("search_bruteforce supports 0 <= n <= 64")
+    hi = u64(np.asarray(hi, dtype=np.uint64)[:n])
+    lo = u64(np.asarray(lo, dtype=np.uint64)[:n])
+    if len(hi) < n or len(lo) < n:
+        raise InvalidParameterError("need n keys")
+    seed = ctypes.c_int64()
+    ev = ctypes.c_int64()
+    check(_L().shk_search_bruteforce(ctx(), ptr(hi), ptr(lo), n, max(0, int(max_seed)), ctypes.byref(seed),
+                                     ctypes.byref(ev)), "search bruteforce")
+    return int(seed.value), int(ev.value)
+
+
+def mc_filter_pass_count(n, trials, entropy):
+    """Seeds in [0, trials) whose cells cover all n (_core.pyx:832-860)."""
+    out = ctypes.c_int64()
+    check(_L().shk_mc_filter_pass_count(ctx(), int(n), int(trials), int(entropy) & MASK64, ctypes.byref(out)),
+          "mc filter pass count")
+    return int(out.value)
+
+
+def enumerate_outcomes(n):
+    """(pseudoforest count, sum of 2^components) over all n^(2n) tuples (_core.pyx:778-829)."""
+    n = int(n)
+    if n > 8:
+        raise ValueError("enumeration limited to n <= 8")
+    pf = ctypes.c_uint64()
+    s2 = ctypes.c_uint64()
+    check(_L().shk_enumerate_outcomes(ctx(), n, ctypes.byref(pf), ctypes.byref(s2)), "enumerate outcomes")
+    return int(pf.value), int(s2.value)
+
+
+# ---------------------------------------------------------------------------
 # Bit stream
 
 

@@ -87,6 +87,9 @@ _SIGS = {
     "shk_rice_decode": (_I, [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _P]),
     "shk_blake2b128": (_I, [_P, _P, _I64, _P, _I64, _U64, _P, _P, _I]),
     "shk_blake2b128_fixed": (_I, [_P, _P, _I, _I64, _U64, _P, _P, _I]),
+    "shk_search_bruteforce": (_I, [_P, _P, _P, _I, _U64, _P, _P]),
+    "shk_mc_filter_pass_count": (_I, [_P, _I, _I64, _U64, _P]),
+    "shk_enumerate_outcomes": (_I, [_P, _I, _P, _P]),
     "shk_build_phase_ms": (_I, [_P, _P, _P]),
     "shk_build_level_ms": (_I, [_P, _P, _P, _I]),
     "shk_build_create": (_I, [_P, _P, _P, _I64, _I64, _I, _P, _P, _P]),

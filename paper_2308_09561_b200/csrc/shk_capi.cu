@@ -619,6 +619,107 @@ int shk_blake2b128(shk_ctx* c, const uint8_t* blob, int64_t blob_len, const int6
   return 0;
 }
 
+// ---- analysis entry points (experiments seam) ----------------------------------
+int shk_search_bruteforce(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int n, uint64_t max_seed,
+                          int64_t* seed_out, int64_t* evals_out) {
+  if (n < 0 || n > 64) {
+    shk_set_error("search_bruteforce supports 0 <= n <= 64 (got %d)", n);
+    return SHK_INVALID;
+  }
+  DBuf kh(c), kl(c), st(c);
+  RC(kh.alloc(64 * 8));
+  RC(kl.alloc(64 * 8));
+  RC(st.alloc(16));
+  RC(h2d(c, kh.p, hi, (size_t)n * 8));
+  RC(h2d(c, kl.p, lo, (size_t)n * 8));
+  unsigned long long* found = st.as<unsigned long long>();
+  unsigned long long* evals = found + 1;
+  // Batches of doubling size; the batch holding the minimum bijective seed is
+  // re-counted up to that seed, so evals match the scalar loop exactly.
+  int64_t total = 0;
+  uint64_t base = 0, batch = 1ull << 16;
+  while (base < max_seed) {
+    const uint64_t cnt = (max_seed - base < batch) ? max_seed - base : batch;
+    const unsigned long long init[2] = {~0ull, 0ull};
+    RC(h2d(c, found, init, 16));
+    RC(shk_launch_brute(kh.as<uint64_t>(), kl.as<uint64_t>(), n, base, cnt, found, evals, c->num_sms, c->stream));
+    unsigned long long res[2];
+    RC(d2h(c, res, found, 16));
+    RC(csync(c));
+    if (res[0] != ~0ull) {
+      RC(h2d(c, found, init, 16));
+      RC(shk_launch_brute(kh.as<uint64_t>(), kl.as<uint64_t>(), n, base, res[0] - base + 1, found, evals,
+                          c->num_sms, c->stream));
+      unsigned long long res2[2];
+      RC(d2h(c, res2, found, 16));
+      RC(csync(c));
+      *seed_out = (int64_t)res[0];
+      *evals_out = total + (int64_t)res2[1];
+      return SHK_OK;
+    }
+    total += (int64_t)res[1];
+    base += cnt;
+    if (batch < (1ull << 28)) batch <<= 1;
+  }
+  *seed_out = -1;
+  *evals_out = total;
+  return SHK_OK;
+}
+
+int shk_mc_filter_pass_count(shk_ctx* c, int n, int64_t trials, uint64_t entropy, int64_t* passes_out) {
+  if (n > 64) {
+    shk_set_error("mc_filter_pass_count supports n <= 64 (got %d)", n);
+    return SHK_INVALID;
+  }
+  if (trials <= 0) {
+    *passes_out = 0;
+    return SHK_OK;
+  }
+  if (n <= 1) {  // every seed covers the (at most one) cell: _core.pyx:834-835
+    *passes_out = trials;
+    return SHK_OK;
+  }
+  uint64_t h[128];
+  for (int j = 0; j < n; ++j) {  // the synthetic key set, _core.pyx:844-846
+    h[j] = shk::mix64(entropy + 2ull * (uint64_t)j);
+    h[64 + j] = shk::mix64(entropy + 2ull * (uint64_t)j + 1ull);
+  }
+  DBuf keys(c), cnt(c);
+  RC(keys.alloc(128 * 8));
+  RC(cnt.alloc(8));
+  RC(h2d(c, keys.p, h, sizeof h));
+  SHK_CUDA(cudaMemsetAsync(cnt.p, 0, 8, c->stream));
+  RC(shk_launch_mc_filter(keys.as<uint64_t>(), keys.as<uint64_t>() + 64, n, (uint64_t)trials,
+                          cnt.as<unsigned long long>(), c->num_sms, c->stream));
+  unsigned long long r = 0;
+  RC(d2h(c, &r, cnt.p, 8));
+  RC(csync(c));
+  *passes_out = (int64_t)r;
+  return SHK_OK;
+}
+
+int shk_enumerate_outcomes(shk_ctx* c, int n, uint64_t* pf_count_out, uint64_t* sum_2c_out) {
+  if (n > 8) {
+    shk_set_error("enumeration limited to n <= 8");
+    return SHK_INVALID;
+  }
+  if (n <= 0) {  // the empty tuple: one pseudoforest with 0 components
+    *pf_count_out = 1;
+    *sum_2c_out = 1;
+    return SHK_OK;
+  }
+  DBuf out(c);
+  RC(out.alloc(16));
+  SHK_CUDA(cudaMemsetAsync(out.p, 0, 16, c->stream));
+  RC(shk_launch_enumerate(n, out.as<unsigned long long>(), c->num_sms, c->stream));
+  unsigned long long r[2];
+  RC(d2h(c, r, out.p, 16));
+  RC(csync(c));
+  *pf_count_out = r[0];
+  *sum_2c_out = r[1];
+  return SHK_OK;
+}
+
 int shk_blake2b128_fixed(shk_ctx* c, const uint8_t* blob, int key_len, int64_t N, uint64_t salt, uint64_t* hi,
                          uint64_t* lo, int flags) {
   if (N <= 0) return 0;

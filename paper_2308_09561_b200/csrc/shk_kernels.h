@@ -187,3 +187,10 @@ int shk_launch_blake2b(const uint8_t* blob, const int64_t* off, int64_t N, uint6
                        uint64_t* lo, cudaStream_t st);
 int shk_launch_blake2b_fixed(const uint8_t* blob, int key_len, int64_t N, uint64_t salt, uint64_t* hi, uint64_t* lo,
                              cudaStream_t st);
+
+// Analysis kernels (shk_experiments.cu).
+int shk_launch_brute(const uint64_t* khi, const uint64_t* klo, int n, uint64_t base, uint64_t count,
+                     unsigned long long* found, unsigned long long* evals, int num_sms, cudaStream_t st);
+int shk_launch_mc_filter(const uint64_t* khi, const uint64_t* klo, int n, uint64_t count,
+                         unsigned long long* passes, int num_sms, cudaStream_t st);
+int shk_launch_enumerate(int n, unsigned long long* out, int num_sms, cudaStream_t st);

@@ -10,9 +10,9 @@
 // scheme:
 //   1. rows (start, 128-bit pattern, rhs) are generated and counting-sorted
 //      by elimination chunk (CE columns);
-//   2. one CTA per chunk eliminates its rows into its slots in shared memory
-//      (a single lane walks each row: XOR with the occupied slot, shift to
-//      the next set bit); rows whose pivot walks past the chunk end are
+//   2. one warp per chunk eliminates its rows into its slots in shared memory
+//      (32 rows in flight, lock-step claim protocol: XOR with the occupied
+//      slot, shift to the next set bit); rows whose pivot walks past the chunk end are
 //      emitted as overflow and inserted by the next pass into the chunk they
 //      reached; passes repeat until no row overflows;
 //   3. back substitution over back-chunks of CB columns runs in parallel
@@ -22,8 +22,8 @@
 //      bits to its own first 127 bits;
 //   4. a single warp walks the chunks right to left evaluating those maps
 //      (the only sequential step: 127x128 GF(2) mat-vec per chunk);
-//   5. every chunk then back-substitutes for real with its now-known right
-//      boundary and writes its solution words.
+//   5. every column's solution bit is then parity(its affine form & its
+//      chunk's boundary), a fully parallel map (step 3 stored the forms).
 #include "shk_common.cuh"
 #include "shk_kernels.h"
 
@@ -247,10 +247,14 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
 // Lane L owns unknowns u = 4L..4L+3 (u = 127 is the constant term); for each
 // it keeps W_u: a 128-bit window whose bit k is the coefficient of u in
 // sol[c + 1 + k].  forms_out[chunk][u] = W_u after the chunk's first column.
+// Every column's own affine form is also written (coef[col], 4 ballots of the
+// new bits: word q bit L = coefficient of unknown 4L + q), so the final pass
+// is a parallel map instead of a second sequential walk.
 __global__ void __launch_bounds__(32) ribbon_forms_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
                                                           const uint64_t* sp1, const uint32_t* occ,
-                                                          const uint32_t* sbit, uint4* forms) {
+                                                          const uint32_t* sbit, uint4* forms, uint4* coef) {
   __shared__ uint64_t tp0[256], tp1[256];
+  __shared__ uint4 tcoef[256];
   __shared__ uint32_t tocc[8], tsb[8];
   const int64_t c = blockIdx.x;
   if (c >= nbchunks) return;
@@ -298,6 +302,11 @@ __global__ void __launch_bounds__(32) ribbon_forms_kernel(int64_t m, int64_t nbc
           nb[q] = __popc(x) & 1u;
         }
         if (lane == 31) nb[3] ^= b;  // u = 127: constant term
+        const uint32_t b0 = __ballot_sync(FULL_WARP, nb[0]), b1 = __ballot_sync(FULL_WARP, nb[1]);
+        const uint32_t b2 = __ballot_sync(FULL_WARP, nb[2]), b3 = __ballot_sync(FULL_WARP, nb[3]);
+        if (lane == 0) tcoef[j] = make_uint4(b0, b1, b2, b3);
+      } else if (lane == 0) {
+        tcoef[j] = make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -307,6 +316,8 @@ __global__ void __launch_bounds__(32) ribbon_forms_kernel(int64_t m, int64_t nbc
         W[q][0] = (W[q][0] << 1) | nb[q];
       }
     }
+    __syncwarp();
+    for (int j = lane; j < ntile; j += 32) coef[tstart + j] = tcoef[j];
     col = tstart - 1;
   }
   uint4* f = forms + c * 128;
@@ -314,27 +325,40 @@ __global__ void __launch_bounds__(32) ribbon_forms_kernel(int64_t m, int64_t nbc
   for (int q = 0; q < 4; ++q) f[4 * lane + q] = make_uint4(W[q][0], W[q][1], W[q][2], W[q][3]);
 }
 
-// Right-to-left chain over back-chunks: y[c] = first 127 solution bits of
-// chunk c + 1 (right boundary of chunk c).  One warp.
-__global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, const uint4* forms, uint4* ybound) {
+// Right-to-left chain over back-chunks: y = first 127 solution bits of chunk
+// c + 1 (right boundary of chunk c).  One warp; the next chunk's forms are
+// loaded while the current one is evaluated.  ysel[c] is the boundary in the
+// coef layout (word q bit L = y bit 4L + q; bit 127 = 1 for the constant).
+__global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, const uint4* forms, uint4* ysel) {
   const int lane = threadIdx.x;
   uint4 y = make_uint4(0, 0, 0, 0);  // boundary right of the last chunk: zero
+  uint4 nxt[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) nxt[q] = forms[(nbchunks - 1) * 128 + 4 * lane + q];
   for (int64_t c = nbchunks - 1; c >= 0; --c) {
-    ybound[c] = y;
-    const uint4* f = forms + c * 128;
+    uint4 w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = nxt[q];
+    if (c > 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nxt[q] = __ldcg(forms + (c - 1) * 128 + 4 * lane + q);
+    }
     uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    uint32_t sel[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int u = 4 * lane + q;
       uint32_t yw = (u >> 5) == 0 ? y.x : (u >> 5) == 1 ? y.y : (u >> 5) == 2 ? y.z : y.w;
-      uint32_t sel = (u == 127) ? 1u : ((yw >> (u & 31)) & 1u);
-      uint4 w = f[u];
-      uint32_t msk = 0u - sel;
-      acc0 ^= w.x & msk;
-      acc1 ^= w.y & msk;
-      acc2 ^= w.z & msk;
-      acc3 ^= w.w & msk;
+      sel[q] = (u == 127) ? 1u : ((yw >> (u & 31)) & 1u);
+      const uint32_t msk = 0u - sel[q];
+      acc0 ^= w[q].x & msk;
+      acc1 ^= w[q].y & msk;
+      acc2 ^= w[q].z & msk;
+      acc3 ^= w[q].w & msk;
     }
+    const uint32_t s0 = __ballot_sync(FULL_WARP, sel[0]), s1 = __ballot_sync(FULL_WARP, sel[1]);
+    const uint32_t s2 = __ballot_sync(FULL_WARP, sel[2]), s3 = __ballot_sync(FULL_WARP, sel[3]);
+    if (lane == 0) ysel[c] = make_uint4(s0, s1, s2, s3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       acc0 ^= __shfl_xor_sync(FULL_WARP, acc0, o);
@@ -346,59 +370,26 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
   }
 }
 
-// Final back substitution with the known right boundary: one warp per
-// back-chunk; the warp stages 256-column tiles of pivot rows in shared memory
-// (coalesced) and lane 0 walks them right to left with a 128-bit window.
-__global__ void __launch_bounds__(32) ribbon_final_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
-                                                          const uint64_t* sp1, const uint32_t* occ,
-                                                          const uint32_t* sbit, const uint4* ybound,
-                                                          uint64_t* words) {
-  __shared__ uint64_t tp0[256], tp1[256];
-  __shared__ uint32_t tocc[8], tsb[8];
-  const int64_t c = blockIdx.x;
-  if (c >= nbchunks) return;
-  const int lane = threadIdx.x;
-  const int64_t s0 = c * CB;
-  const int64_t e = (s0 + CB < m) ? s0 + CB : m;
-  uint4 y = ybound[c];
-  // window bit k = sol[col + 1 + k]
-  uint64_t w0 = (uint64_t)y.x | ((uint64_t)y.y << 32);
-  uint64_t w1 = (uint64_t)y.z | ((uint64_t)y.w << 32);
-  uint64_t outw = 0;
-  int64_t col = e - 1;
-  while (col >= s0) {
-    const int64_t tstart = (col / 256) * 256;
-    const int ntile = (int)(col - tstart + 1);
-    __syncwarp();
-    for (int j = lane; j < ntile; j += 32) {
-      tp0[j] = sp0[tstart + j];
-      tp1[j] = sp1[tstart + j];
-    }
-    if (lane < 8) {
-      const bool in = lane * 32 < ntile;
-      tocc[lane] = in ? occ[tstart / 32 + lane] : 0;
-      tsb[lane] = in ? sbit[tstart / 32 + lane] : 0;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      for (int j = ntile - 1; j >= 0; --j) {
-        const int64_t cc = tstart + j;
-        uint32_t bit = 0;
-        if ((tocc[j >> 5] >> (j & 31)) & 1u) {
-          const uint64_t a0 = tp0[j], a1 = tp1[j];
-          const uint64_t q0 = (a0 >> 1) | (a1 << 63), q1 = a1 >> 1;
-          bit = (uint32_t)((__popcll(q0 & w0) + __popcll(q1 & w1)) & 1) ^ ((tsb[j >> 5] >> (j & 31)) & 1u);
-        }
-        w1 = (w1 << 1) | (w0 >> 63);
-        w0 = (w0 << 1) | bit;
-        outw |= (uint64_t)bit << (cc & 63);
-        if ((cc & 63) == 0) {
-          words[cc >> 6] = outw;
-          outw = 0;
-        }
+// Final back substitution, a parallel map: sol[col] = parity(coef[col] &
+// ysel[chunk]); one warp per 64-bit solution word (two ballots).
+__global__ void ribbon_final_kernel(int64_t m, int64_t nwords, const uint4* __restrict__ coef,
+                                    const uint4* __restrict__ ysel, uint64_t* words) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nwords; wi += nwarps) {
+    uint32_t bits[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t cc = wi * 64 + h * 32 + lane;
+      uint32_t bit = 0;
+      if (cc < m) {
+        const uint4 a = __ldcs(coef + cc);
+        const uint4 y = __ldg(ysel + cc / CB);
+        bit = __popc((a.x & y.x) ^ (a.y & y.y) ^ (a.z & y.z) ^ (a.w & y.w)) & 1u;
       }
+      bits[h] = __ballot_sync(FULL_WARP, bit);
     }
-    col = tstart - 1;
+    if (lane == 0) words[wi] = (uint64_t)bits[0] | ((uint64_t)bits[1] << 32);
   }
 }
 
@@ -460,7 +451,7 @@ namespace {
 
 struct RibLayout {
   size_t off_rows, off_rows2, off_ovf, off_hist, off_rowoff, off_cursor, off_sp0, off_sp1, off_occ, off_sb, off_forms,
-      off_y, off_cnt, off_scan, total;
+      off_coef, off_y, off_cnt, off_scan, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -493,6 +484,8 @@ RibLayout layout(int64_t N, int64_t m) {
   o += al((size_t)nw32 * 4);
   L.off_forms = o;
   o += al((size_t)nbc * 128 * 16);
+  L.off_coef = o;
+  o += al((size_t)m * 16);
   L.off_y = o;
   o += al((size_t)nbc * 16);
   L.off_cnt = o;
@@ -539,6 +532,7 @@ int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_
   uint32_t* occ = (uint32_t*)(B + L.off_occ);
   uint32_t* sb = (uint32_t*)(B + L.off_sb);
   uint4* forms = (uint4*)(B + L.off_forms);
+  uint4* coef = (uint4*)(B + L.off_coef);
   uint4* yb = (uint4*)(B + L.off_y);
   int64_t* cnt = (int64_t*)(B + L.off_cnt);  // [0] ovf count, [1] inconsistent flag (int)
   void* scan = B + L.off_scan;
@@ -585,11 +579,14 @@ int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_
     return 0;
   }
   *consistent = 1;
-  ribbon_forms_kernel<<<(unsigned)nbc, 32, 0, st>>>(m, nbc, sp0, sp1, occ, sb, forms);
+  ribbon_forms_kernel<<<(unsigned)nbc, 32, 0, st>>>(m, nbc, sp0, sp1, occ, sb, forms, coef);
   SHK_LAUNCHED();
   ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, forms, yb);
   SHK_LAUNCHED();
-  ribbon_final_kernel<<<(unsigned)nbc, 32, 0, st>>>(m, nbc, sp0, sp1, occ, sb, yb, words_out);
+  const int64_t nwords = (m + 63) / 64;
+  int64_t fb = (nwords + 7) / 8;
+  if (fb > 148 * 8) fb = 148 * 8;
+  ribbon_final_kernel<<<(unsigned)fb, 256, 0, st>>>(m, nwords, coef, yb, words_out);
   SHK_LAUNCHED();
   return 0;
 }

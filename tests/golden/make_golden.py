@@ -252,6 +252,31 @@ def part_small_builds():
     dump("builds.json", recs)
 
 
+def part_experiments():
+    """The analysis entry points of the kernel seam: search_bruteforce,
+    enumerate_outcomes, mc_filter_pass_count (_core.pyx:337-371, 778-860)."""
+    brute = []
+    for n in [1, 2, 3, 5, 8, 10, 12, 14, 16]:
+        for rep in range(4 if n <= 12 else 2):
+            gen = 313 + 100 * n + rep
+            hi, lo = synthetic_hashed(n, gen)
+            s, ev = K.search_bruteforce(hi, lo, n, 1 << 30)
+            brute.append(dict(n=n, gen=gen, max_seed=1 << 30, seed=int(s), evals=int(ev)))
+    for n, ms in [(10, 50), (16, 1000), (12, 0)]:
+        hi, lo = synthetic_hashed(n, 77)
+        s, ev = K.search_bruteforce(hi, lo, n, ms)
+        brute.append(dict(n=n, gen=77, max_seed=ms, seed=int(s), evals=int(ev)))
+    enum = []
+    for n in range(1, 7):
+        pf, s2 = K.enumerate_outcomes(n)
+        enum.append(dict(n=n, pf_count=int(pf), sum_2c=int(s2)))
+    mc = []
+    for n, trials, ent in [(1, 1000, 0), (2, 1000, 1), (12, 2000, 42), (16, 300000, 7), (24, 200000, 3),
+                           (32, 300000, 5), (40, 100000, 2**64 - 3), (56, 50000, 11), (64, 50000, 13)]:
+        mc.append(dict(n=n, trials=trials, entropy=ent, passes=int(K.mc_filter_pass_count(n, trials, ent))))
+    dump("experiments.json", dict(bruteforce=brute, enumerate=enum, mc_filter=mc))
+
+
 if __name__ == "__main__":
     parts = sys.argv[1:] or ["kat", "leaves", "split", "ribbon", "rice", "c1", "c3", "c5", "c2", "builds"]
     for p in parts:
@@ -276,6 +301,8 @@ if __name__ == "__main__":
             part_build(2)
         elif p == "c4":
             part_build(4)
+        elif p == "experiments":
+            part_experiments()
         elif p == "builds":
             part_small_builds()
         print(p, "done in", round(time.time() - t, 1), "s", file=sys.stderr)

@@ -211,3 +211,48 @@ def test_small_builds_golden():
             assert blob.hex() == r["desc_hex"], r
         assert sha(blob) == r["desc_sha"], r
         assert sha(np.asarray(desc.query_many(keys), "<u8").tobytes()) == r["query_sha"], r
+
+
+def _synthetic_hashed(count, gen_seed):
+    from paper_2308_09561_b200.keys import synthetic_hashed
+
+    return synthetic_hashed(count, gen_seed)
+
+
+def test_search_bruteforce_golden(K):
+    for r in golden("experiments.json")["bruteforce"]:
+        hi, lo = _synthetic_hashed(r["n"], r["gen"])
+        assert K.search_bruteforce(hi, lo, r["n"], r["max_seed"]) == (r["seed"], r["evals"]), r
+
+
+def test_search_bruteforce_vs_oracle(K):
+    """Larger n than the fixtures, several doubling batches deep."""
+    import oracle
+
+    for n, gen in ((17, 5), (18, 6)):
+        hi, lo = _synthetic_hashed(n, gen)
+        assert K.search_bruteforce(hi, lo, n, 1 << 40) == oracle.search_bruteforce(hi, lo, n, 1 << 40)
+
+
+def test_mc_filter_golden(K):
+    for r in golden("experiments.json")["mc_filter"]:
+        assert K.mc_filter_pass_count(r["n"], r["trials"], r["entropy"]) == r["passes"], r
+
+
+def test_enumerate_outcomes_golden(K):
+    for r in golden("experiments.json")["enumerate"]:
+        assert K.enumerate_outcomes(r["n"]) == (r["pf_count"], r["sum_2c"]), r
+    assert K.enumerate_outcomes(0) == (1, 1)
+    with pytest.raises(ValueError):
+        K.enumerate_outcomes(9)
+
+
+@pytest.mark.parametrize("n", [7, 8])
+def test_enumerate_outcomes_closed_form(K, n):
+    """n = 7, 8 ((n^2)^n = 6.8e11 / 2.8e14 tuples) are out of the oracle's
+    reach; they are checked against the closed-form census in
+    tests/enum_census.py, which is itself pinned to the reference's n <= 6
+    outputs by tests/test_oracle.py."""
+    from enum_census import census
+
+    assert K.enumerate_outcomes(n) == (census(n, 1), census(n, 2))

@@ -151,3 +151,28 @@ def test_small_builds_golden():
         assert sha(blob) == r["desc_sha"], r
         out = OH.query(res, r["n"], r["mode"], 8, hi, lo)
         assert sha(out.astype("<u8").tobytes()) == r["query_sha"], r
+
+
+def test_experiments_golden():
+    """search_bruteforce / mc_filter_pass_count / enumerate_outcomes
+    (_core.pyx:337-371, 778-860) against the reference's outputs."""
+    g = golden("experiments.json")
+    for r in g["bruteforce"]:
+        hi, lo = synthetic_hashed(r["n"], r["gen"])
+        assert oracle.search_bruteforce(hi, lo, r["n"], r["max_seed"]) == (r["seed"], r["evals"]), r
+    for r in g["enumerate"]:
+        if r["n"] <= 5:
+            assert oracle.enumerate_outcomes(r["n"]) == (r["pf_count"], r["sum_2c"]), r
+    for r in g["mc_filter"]:
+        if r["n"] * r["trials"] <= 5_000_000:
+            assert oracle.mc_filter_pass_count(r["n"], r["trials"], r["entropy"]) == r["passes"], r
+
+
+def test_enumeration_census_pinned():
+    """The closed form used for the GPU check at n = 7, 8 reproduces the
+    reference's enumerate_outcomes for every n it was run at."""
+    from enum_census import census
+
+    for r in golden("experiments.json")["enumerate"]:
+        assert (census(r["n"], 1), census(r["n"], 2)) == (r["pf_count"], r["sum_2c"])
+    assert census(0, 1) == 1 and census(0, 2) == 1
