@@ -399,6 +399,7 @@ int shk_split_search(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
     RC(h2d(c, th.p, hi, (size_t)m * 8));
     RC(h2d(c, tl.p, lo, (size_t)m * 8));
     RC(shk_launch_interleave(th.as<uint64_t>(), tl.as<uint64_t>(), m, keys.as<uint64_t>(), c->stream));
+    RC(shk_launch_premix(keys.as<uint64_t>(), m, 0, c->stream));
     RC(csync(c));
   }
   ShkSplitTask t{};
@@ -1095,6 +1096,9 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   }
   b->mark(2);
   b->level_reset();
+  // the seed searches take pre-mixed key high words (shk_hash.cuh premix_hi);
+  // undone right after the leaves
+  RC(shk_launch_premix(b->keys.as<uint64_t>(), b->N, 0, c->stream));
   DBuf dnodes(c), dqueue(c), dqctl(c), dpn(c), dpoff(c), dbp(c), dnbase(c), dks(c), droot(c);
   if (use_tree && nn > 0) {
     // ---- node table expanded on the device from the (small) plan tables
@@ -1178,6 +1182,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     p.hi = b->keys.as<uint64_t>();
     p.lo = b->keys.as<uint64_t>() + 1;
     p.stride = 2;
+    p.pre = 1;
     p.off = dloff.as<int64_t>();
     p.L = L;
     p.max_n = max_leaf;
@@ -1202,6 +1207,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     }
     RC(shk_launch_leaf_search(p, c->stream));
   }
+  RC(shk_launch_premix(b->keys.as<uint64_t>(), b->N, 1, c->stream));
   b->mark(4);
   int hex = 0;
   RC(d2h(c, &hex, exh, 4));

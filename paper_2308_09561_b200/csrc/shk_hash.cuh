@@ -148,13 +148,36 @@ SHK_D u2 xorshr_alu(u2 z) {
   return r;
 }
 
-// z * C (mod 2^64) in halves: one IMAD.WIDE.U32 + two IMAD.
+// z * C (mod 2^64) in halves: one IMAD.WIDE.U32 + two chained IMAD (written
+// in PTX: left to itself the compiler sums the cross terms separately and
+// spends a fourth FMA-pipe instruction on the add).
 template <uint64_t C>
 SHK_D u2 mulc(u2 z) {
   constexpr uint32_t cl = (uint32_t)C, ch = (uint32_t)(C >> 32);
-  uint64_t w = (uint64_t)z.lo * cl;
-  u2 r = split64(w);
-  r.hi = r.hi + z.lo * ch + z.hi * cl;
+  u2 r;
+  asm("{\n\t.reg .u64 w;\n\t.reg .u32 wh, t;\n\t"
+      "mul.wide.u32 w, %2, %4;\n\t"
+      "mov.b64 {%0, wh}, w;\n\t"
+      "mad.lo.u32 t, %2, %5, wh;\n\t"
+      "mad.lo.u32 %1, %3, %4, t;\n\t"
+      "}"
+      : "=r"(r.lo), "=r"(r.hi)
+      : "r"(z.lo), "r"(z.hi), "n"(cl), "n"(ch));
+  return r;
+}
+
+// High word of z * C (mod 2^64): IMAD.HI + two chained IMAD.
+template <uint64_t C>
+SHK_D uint32_t mulc_hi(u2 z) {
+  constexpr uint32_t cl = (uint32_t)C, ch = (uint32_t)(C >> 32);
+  uint32_t r;
+  asm("{\n\t.reg .u32 t;\n\t"
+      "mul.hi.u32 t, %1, %3;\n\t"
+      "mad.lo.u32 t, %1, %4, t;\n\t"
+      "mad.lo.u32 %0, %2, %3, t;\n\t"
+      "}"
+      : "=r"(r)
+      : "r"(z.lo), "r"(z.hi), "n"(cl), "n"(ch));
   return r;
 }
 
@@ -184,8 +207,45 @@ SHK_D uint32_t remix_top_d(u2 k_hi, u2 k_lo, u2 x) {
   z.lo ^= k_lo.lo;
   z.hi ^= k_lo.hi;
   z = mulc<MUL1>(xorshr<30>(z));
+  return mulc_hi<MUL2>(xorshr<27>(z)) >> 31;
+}
+
+// ---------------------------------------------------------------------------
+// Pre-mixed keys.  The first xor-shift of remix distributes over the seed
+// xor:  (hi ^ x) ^ ((hi ^ x) >> 30) = (hi ^ (hi >> 30)) ^ (x ^ (x >> 30)),
+// so the seed searches store every key's high word as hp = premix(hi) once
+// and every candidate seed's mixer as xp = premix(x) once, and drop one
+// xor-shift (4 ALU instructions) from every (key, seed) evaluation.  Results
+// are bit-identical to remix(); unpremix inverts premix.
+SHK_HD uint64_t premix_hi(uint64_t h) { return h ^ (h >> 30); }
+SHK_HD uint64_t unpremix_hi(uint64_t h) { return h ^ (h >> 30) ^ (h >> 60); }
+
+SHK_D u2 seed_mixer_pre_d(uint64_t seed, uint64_t tag) { return split64(premix_hi(seed_mixer(seed, tag))); }
+
+// First mix64 from pre-mixed operands, then the second one (full remix).
+SHK_D u2 remix_pre_d(u2 kp, u2 k_lo, u2 xp) {
+  u2 z;
+  z.lo = kp.lo ^ xp.lo;
+  z.hi = kp.hi ^ xp.hi;
+  z = mulc<MUL1>(z);
   z = mulc<MUL2>(xorshr<27>(z));
-  return z.hi >> 31;
+  z = xorshr<31>(z);
+  z.lo ^= k_lo.lo;
+  z.hi ^= k_lo.hi;
+  return mix64_d(z);
+}
+
+SHK_D uint32_t remix_top_pre_d(u2 kp, u2 k_lo, u2 xp) {
+  u2 z;
+  z.lo = kp.lo ^ xp.lo;
+  z.hi = kp.hi ^ xp.hi;
+  z = mulc<MUL1>(z);
+  z = mulc<MUL2>(xorshr<27>(z));
+  z = xorshr<31>(z);
+  z.lo ^= k_lo.lo;
+  z.hi ^= k_lo.hi;
+  z = mulc<MUL1>(xorshr<30>(z));
+  return mulc_hi<MUL2>(xorshr<27>(z)) >> 31;
 }
 
 SHK_D uint32_t range32(uint32_t vhi, uint32_t m) { return __umulhi(vhi, m); }

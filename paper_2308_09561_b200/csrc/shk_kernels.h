@@ -30,6 +30,7 @@ struct ShkLeafLaunch {
   unsigned long long* stats_acc;  // optional [4] totals (evals, passes, checks, a_evals)
   int* exhausted;                 // optional flag
   int64_t* place_out;             // optional [N] global slot per key
+  int pre;                        // keys' high words are already premix_hi'ed
 };
 int shk_launch_leaf_search(const ShkLeafLaunch& p, cudaStream_t st);
 int shk_launch_orient(const uint8_t* eu, const uint8_t* ev, const int64_t* off, int64_t L, uint64_t* fbits, int* ok,
@@ -144,6 +145,10 @@ int shk_launch_split_parts(const uint64_t* hi, const uint64_t* lo, int64_t m, ui
 // Pack separate hi/lo arrays into interleaved pairs.
 int shk_launch_interleave(const uint64_t* hi, const uint64_t* lo, int64_t N, uint64_t* pairs, cudaStream_t st);
 int shk_launch_deinterleave(const uint64_t* pairs, int64_t N, uint64_t* hi, uint64_t* lo, cudaStream_t st);
+// premix_hi (inverse = 0) or unpremix_hi (inverse = 1) of the high words of
+// interleaved key pairs, in place: the build's seed searches (split kernels,
+// tree kernel, build-path leaves) take pre-mixed keys.
+int shk_launch_premix(uint64_t* pairs, int64_t N, int inverse, cudaStream_t st);
 int shk_launch_ribbon_query(const int64_t* starts, const uint64_t* p0, const uint64_t* p1, int64_t N,
                             const uint64_t* words, int64_t nwords, uint8_t* out, cudaStream_t st);
 

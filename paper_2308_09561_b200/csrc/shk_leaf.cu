@@ -77,6 +77,7 @@ int shk_launch_leaf_search(const ShkLeafLaunch& p, cudaStream_t st) {
   a.counter = p.counter;
   a.error = p.error;
   a.stride = p.stride > 0 ? p.stride : 1;
+  a.pre = p.pre;
   a.seed_slot = p.seed_slot;
   a.stats_acc = p.stats_acc;
   a.exhausted = p.exhausted;

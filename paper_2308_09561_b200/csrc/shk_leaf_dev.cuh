@@ -40,13 +40,14 @@ struct LeafArgs {
   unsigned long long* stats_acc;  // optional [4] running totals
   int* exhausted;       // optional: set if a leaf has no seed below max_seed
   int64_t* place_out;   // optional [N]: global slot of each key (leaf start + its cell)
+  int pre;              // hi words are already premix_hi'ed (build path)
 };
 
 // MAXE: most keys per leaf the team's buffers hold (64, or 40 to fit more
 // warps per SM when the build's leaves are small enough).
 template <int TW, int MAXE = 64>
 struct LeafSmem {
-  uint4 keys[MAXE];               // (hi.lo, hi.hi, lo.lo, lo.hi)
+  uint4 keys[MAXE];               // (hp.lo, hp.hi, lo.lo, lo.hi), hp = premix_hi(hi)
   uint16_t edges[TW][MAXE * 32];  // per-lane packed edges, column per lane
   int64_t slot_win[2][TW];        // per-warp lowest accepting candidate (or -1)
   int32_t slot_r[2][TW];          // rotation of that candidate
@@ -81,7 +82,8 @@ struct LeafOut {
 template <int TW, class SM>
 SHK_D void load_leaf_keys(const LeafArgs& a, SM& sm, int64_t k0, int n, int tt) {
   for (int i = tt; i < n; i += TW * 32) {
-    u2 h = split64(a.hi[(k0 + i) * a.stride]), l = split64(a.lo[(k0 + i) * a.stride]);
+    const uint64_t hw = a.hi[(k0 + i) * a.stride];
+    u2 h = split64(a.pre ? hw : premix_hi(hw)), l = split64(a.lo[(k0 + i) * a.stride]);
     sm.keys[i] = make_uint4(h.lo, h.hi, l.lo, l.hi);
   }
 }
@@ -129,13 +131,13 @@ SHK_D void leaf_finish(const LeafArgs& a, SM& sm, int64_t k0, int n, int64_t q, 
 // Plain search body for one candidate seed per lane.
 template <bool WIDE>
 SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
-  u2 x = seed_mixer_d(s, TAG_LEAF);
+  u2 x = seed_mixer_pre_d(s, TAG_LEAF);
   const uint32_t un = (uint32_t)n, unm1 = (uint32_t)(n - 1);
   uint32_t m0 = 0, m1 = 0;
 #pragma unroll 4
   for (int i = 0; i < n; ++i) {
     uint4 k = keys[i];
-    u2 v = remix_d(u2{k.x, k.y}, u2{k.z, k.w}, x);
+    u2 v = remix_pre_d(u2{k.x, k.y}, u2{k.z, k.w}, x);
     uint32_t h0, h1;
     leaf_pair_d(v, un, unm1, h0, h1);
     if (!WIDE) {
@@ -211,10 +213,10 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
   }
   if (warp == 0) {
     if (seed >= 0 && n >= 2) {
-      const u2 x = seed_mixer_d((uint64_t)seed, TAG_LEAF);
+      const u2 x = seed_mixer_pre_d((uint64_t)seed, TAG_LEAF);
       for (int i = lane; i < n; i += 32) {
         uint4 k = sm.keys[i];
-        u2 v = remix_d(u2{k.x, k.y}, u2{k.z, k.w}, x);
+        u2 v = remix_pre_d(u2{k.x, k.y}, u2{k.z, k.w}, x);
         uint32_t h0, h1;
         leaf_pair_d(v, (uint32_t)n, (uint32_t)(n - 1), h0, h1);
         sm.eu[i] = (uint8_t)h0;
@@ -254,19 +256,19 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
       if (valid) {
         const uint64_t sa = ck ? base - base % (uint64_t)ck : base;
         ws = (base == 0) || (ck == 0) || (base % (uint64_t)ck == 0);
-        const u2 xb = seed_mixer_d(sa, TAG_SPLITBIT);
-        const u2 xa = seed_mixer_d(sa, TAG_LEAF);
-        const u2 xg = seed_mixer_d(base, TAG_LEAF);
+        const u2 xb = seed_mixer_pre_d(sa, TAG_SPLITBIT);
+        const u2 xa = seed_mixer_pre_d(sa, TAG_LEAF);
+        const u2 xg = seed_mixer_pre_d(base, TAG_LEAF);
         uint32_t ma0 = 0, ma1 = 0, mb0 = 0, mb1 = 0;
 #pragma unroll 2
         for (int i = 0; i < n; ++i) {
           uint4 k = sm.keys[i];
           u2 kh{k.x, k.y}, kl{k.z, k.w};
-          uint32_t bit = remix_top_d(kh, kl, xb);
+          uint32_t bit = remix_top_pre_d(kh, kl, xb);
           u2 x;
           x.lo = bit ? xg.lo : xa.lo;
           x.hi = bit ? xg.hi : xa.hi;
-          u2 v = remix_d(kh, kl, x);
+          u2 v = remix_pre_d(kh, kl, x);
           uint32_t h0, h1;
           leaf_pair_d(v, un, unm1, h0, h1);
           uint32_t c0, c1 = 0;
@@ -364,12 +366,13 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
       const uint64_t base = (uint64_t)q / (uint64_t)n;
       const int r = (int)((uint64_t)q % (uint64_t)n);
       const uint64_t sa = ck ? base - base % (uint64_t)ck : base;
-      const u2 xb = seed_mixer_d(sa, TAG_SPLITBIT), xa = seed_mixer_d(sa, TAG_LEAF), xg = seed_mixer_d(base, TAG_LEAF);
+      const u2 xb = seed_mixer_pre_d(sa, TAG_SPLITBIT), xa = seed_mixer_pre_d(sa, TAG_LEAF),
+               xg = seed_mixer_pre_d(base, TAG_LEAF);
       for (int i = lane; i < n; i += 32) {
         uint4 k = sm.keys[i];
         u2 kh{k.x, k.y}, kl{k.z, k.w};
-        uint32_t bit = remix_top_d(kh, kl, xb);
-        u2 v = remix_d(kh, kl, bit ? xg : xa);
+        uint32_t bit = remix_top_pre_d(kh, kl, xb);
+        u2 v = remix_pre_d(kh, kl, bit ? xg : xa);
         uint32_t h0, h1;
         leaf_pair_d(v, (uint32_t)n, (uint32_t)(n - 1), h0, h1);
         if (bit) {

@@ -3,6 +3,7 @@
 // Restates _core.pyx:378-428 (split_parts, split_seed_search) and the
 // per-node partition of recsplit.py:553-567 for sm_100a.
 //
+// Keys are interleaved (premix_hi(hi), lo) pairs (shk_hash.cuh).
 // One warp per split node (fetched dynamically).  Lane j tests seed R + j
 // over all m keys of the node: key loads are warp-uniform (LDG.128 broadcast
 // from L1/L2), part counts live in one 64-bit register as four 16-bit
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(256) split_kernel(ShkSplitLaunch a) {
     for (uint64_t R = 0; R < a.max_seed; R += 32) {
       const uint64_t s = R + lane;
       const bool valid = s < a.max_seed;
-      const u2 x = seed_mixer_d(s, TAG_SPLIT);
+      const u2 x = seed_mixer_pre_d(s, TAG_SPLIT);
       uint32_t capl = (uint32_t)cap0, caph = (uint32_t)(cap0 >> 32);
       int fail = valid ? -1 : 0;  // invalid lanes count as failed at key 0
       for (int i0 = 0; i0 < m; i0 += 8) {
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) split_kernel(ShkSplitLaunch a) {
           const int i = i0 + u;
           if (i < m) {
             ulonglong2 k = __ldg(kp + i);
-            u2 v = remix_d(split64(k.x), split64(k.y), x);
+            u2 v = remix_pre_d(split64(k.x), split64(k.y), x);
             uint32_t r = __umulhi(v.hi, um);
             uint32_t sh = part_of(r, b0, b1, b2) << 4;
             uint32_t dl = shl_clamp(1u, sh), dh = shl_clamp(1u, sh - 32u);
@@ -141,6 +142,15 @@ __global__ void deinterleave_kernel(const ulonglong2* in, int64_t N, uint64_t* h
   }
 }
 
+// In-place premix_hi / unpremix_hi of the high words of interleaved pairs.
+__global__ void premix_pairs_kernel(ulonglong2* keys, int64_t N, int inverse) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    ulonglong2 k = keys[i];
+    k.x = inverse ? unpremix_hi(k.x) : premix_hi(k.x);
+    keys[i] = k;
+  }
+}
+
 }  // namespace shk
 
 using namespace shk;
@@ -170,6 +180,13 @@ int shk_launch_interleave(const uint64_t* hi, const uint64_t* lo, int64_t N, uin
 int shk_launch_deinterleave(const uint64_t* pairs, int64_t N, uint64_t* hi, uint64_t* lo, cudaStream_t st) {
   if (N <= 0) return 0;
   deinterleave_kernel<<<grid256(N), 256, 0, st>>>((const ulonglong2*)pairs, N, hi, lo);
+  SHK_LAUNCHED();
+  return 0;
+}
+
+int shk_launch_premix(uint64_t* pairs, int64_t N, int inverse, cudaStream_t st) {
+  if (N <= 0) return 0;
+  premix_pairs_kernel<<<grid256(N), 256, 0, st>>>((ulonglong2*)pairs, N, inverse);
   SHK_LAUNCHED();
   return 0;
 }

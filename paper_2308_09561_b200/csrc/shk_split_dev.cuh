@@ -16,6 +16,8 @@ SHK_D uint32_t part_of(uint32_t r, uint32_t b0, uint32_t b1, uint32_t b2) {
   return (uint32_t)(r >= b0) + (uint32_t)(r >= b1) + (uint32_t)(r >= b2);
 }
 
+// Keys of the split searches are interleaved (premix_hi(hi), lo) pairs.
+
 // Stable partition of a node's keys by part (recsplit.py:558-561): ballots
 // rank every key within its part, keys go to tmp and are copied back.
 SHK_D void split_partition(const ulonglong2* kp, ulonglong2* kw, ulonglong2* tmp, const ShkSplitTask& task,
@@ -32,7 +34,7 @@ SHK_D void split_partition(const ulonglong2* kp, ulonglong2* kw, ulonglong2* tmp
       if (j < 3) b[j] = (j < task.fanout - 1) ? acc : um;
     }
   }
-  const u2 x = seed_mixer_d((uint64_t)seed, TAG_SPLIT);
+  const u2 x = seed_mixer_pre_d((uint64_t)seed, TAG_SPLIT);
   for (int c = 0; c < m; c += 32) {
     const int i = c + lane;
     const bool in = i < m;
@@ -40,7 +42,7 @@ SHK_D void split_partition(const ulonglong2* kp, ulonglong2* kw, ulonglong2* tmp
     uint32_t p = 4;
     if (in) {
       k = kp[i];
-      u2 v = remix_d(split64(k.x), split64(k.y), x);
+      u2 v = remix_pre_d(split64(k.x), split64(k.y), x);
       p = part_of(__umulhi(v.hi, um), b[0], b[1], b[2]);
     }
     uint32_t dst = 0;
@@ -57,19 +59,20 @@ SHK_D void split_partition(const ulonglong2* kp, ulonglong2* kw, ulonglong2* tmp
   __syncwarp();
 }
 
-// High word of remix(hi, lo, seed, tag) (all the split hash needs).
-SHK_D uint32_t remix_hi_d(u2 k_hi, u2 k_lo, u2 x) {
+// High word of remix(hi, lo, seed, tag) (all the split hash needs), from a
+// pre-mixed key high word and seed mixer (shk_hash.cuh, premix_hi).
+SHK_D uint32_t remix_hi_pre_d(u2 kp, u2 k_lo, u2 xp) {
   u2 z;
-  z.lo = k_hi.lo ^ x.lo;
-  z.hi = k_hi.hi ^ x.hi;
-  z = mulc<MUL1>(xorshr_alu<30>(z));
+  z.lo = kp.lo ^ xp.lo;
+  z.hi = kp.hi ^ xp.hi;
+  z = mulc<MUL1>(z);
   z = mulc<MUL2>(xorshr_alu<27>(z));
   z = xorshr_alu<31>(z);
   z.lo ^= k_lo.lo;
   z.hi ^= k_lo.hi;
   z = mulc<MUL1>(xorshr_alu<30>(z));
-  z = mulc<MUL2>(xorshr_alu<27>(z));
-  return z.hi ^ (z.hi >> 31);  // hi word of z ^ (z >> 31)
+  const uint32_t h = mulc_hi<MUL2>(xorshr_alu<27>(z));
+  return h ^ (h >> 31);  // hi word of z ^ (z >> 31)
 }
 
 // Fast minimum-seed search for a node with F parts (build path).
@@ -99,7 +102,7 @@ SHK_D int64_t split_search_fast(const ulonglong2* kp, const ShkSplitTask& task, 
   const int s0 = task.sizes[0], s1 = task.sizes[1], s2 = F > 2 ? task.sizes[2] : 0, s3 = F > 3 ? task.sizes[3] : 0;
   for (uint64_t R = 0; R < max_seed; R += 32) {
     const uint64_t s = R + lane;
-    const u2 x = seed_mixer_d(s, TAG_SPLIT);
+    const u2 x = seed_mixer_pre_d(s, TAG_SPLIT);
     int g1 = 0, g2 = 0, g3 = 0;
     bool fail = !(s < max_seed);
     bool all_failed = false;
@@ -108,7 +111,7 @@ SHK_D int64_t split_search_fast(const ulonglong2* kp, const ShkSplitTask& task, 
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const ulonglong2 k = load_key(kp + i + u);
-        const uint32_t vh = remix_hi_d(split64(k.x), split64(k.y), x);
+        const uint32_t vh = remix_hi_pre_d(split64(k.x), split64(k.y), x);
         g1 += (vh >= T0);
         if (F > 2) g2 += (vh >= T1);
         if (F > 3) g3 += (vh >= T2);
@@ -127,7 +130,7 @@ SHK_D int64_t split_search_fast(const ulonglong2* kp, const ShkSplitTask& task, 
     if (!all_failed) {
       for (; i < m; ++i) {
         const ulonglong2 k = load_key(kp + i);
-        const uint32_t vh = remix_hi_d(split64(k.x), split64(k.y), x);
+        const uint32_t vh = remix_hi_pre_d(split64(k.x), split64(k.y), x);
         g1 += (vh >= T0);
         if (F > 2) g2 += (vh >= T1);
         if (F > 3) g3 += (vh >= T2);

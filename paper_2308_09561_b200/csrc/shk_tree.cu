@@ -169,6 +169,7 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   a.hi = p.keys;
   a.lo = p.keys + 1;
   a.stride = 2;
+  a.pre = 1;
   a.max_seed = p.max_seed;
   a.mode = p.mode;
   a.cache_k = p.cache_k;

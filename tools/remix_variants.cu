@@ -15,7 +15,26 @@ template <uint64_t C> __device__ __forceinline__ u2 mulc2(u2 z) {  // no IMAD.WI
   constexpr uint32_t cl = (uint32_t)C, ch = (uint32_t)(C >> 32);
   u2 r; r.lo = z.lo * cl; r.hi = __umulhi(z.lo, cl) + z.lo * ch + z.hi * cl; return r;
 }
-template <uint64_t C, int W> __device__ __forceinline__ u2 mulv(u2 z) { return W ? mulc2<C>(z) : mulc<C>(z); }
+template <uint64_t C> __device__ __forceinline__ u2 mulc3(u2 z) {  // IMAD.WIDE with the cross terms as addend
+  constexpr uint32_t cl = (uint32_t)C, ch = (uint32_t)(C >> 32);
+  uint32_t t = z.lo * ch + z.hi * cl;
+  uint64_t w = (uint64_t)z.lo * cl + ((uint64_t)t << 32);
+  return u2{(uint32_t)w, (uint32_t)(w >> 32)};
+}
+template <uint64_t C> __device__ __forceinline__ u2 mulc5(u2 z) {
+  constexpr uint32_t cl = (uint32_t)C, ch = (uint32_t)(C >> 32);
+  u2 r;
+  asm("{\n\t.reg .u64 w;\n\t.reg .u32 wh, t;\n\t"
+      "mul.wide.u32 w, %2, %4;\n\t"
+      "mov.b64 {%0, wh}, w;\n\t"
+      "mad.lo.u32 t, %2, %5, wh;\n\t"
+      "mad.lo.u32 %1, %3, %4, t;\n\t"
+      "}" : "=r"(r.lo), "=r"(r.hi) : "r"(z.lo), "r"(z.hi), "n"(cl), "n"(ch));
+  return r;
+}
+template <uint64_t C, int W> __device__ __forceinline__ u2 mulv(u2 z) {
+  return W == 1 ? mulc2<C>(z) : W == 2 ? mulc5<C>(z) : mulc<C>(z);
+}
 template <int S, bool F> __device__ __forceinline__ u2 xs(u2 z) {
   uint32_t lo_sh;
   if (F) lo_sh = __umulhi(z.lo, P2[32 - S]) + z.hi * P2[32 - S];
@@ -32,12 +51,12 @@ template <int S> __device__ __forceinline__ u2 xsa(u2 z) {  // all-ALU variant
 template <int S, int A> __device__ __forceinline__ u2 xsv(u2 z) { return A ? xsa<S>(z) : xs<S, false>(z); }
 template <int M> __device__ __forceinline__ uint32_t remix_hi(u2 h, u2 l, u2 x) {
   u2 z{h.lo ^ x.lo, h.hi ^ x.hi};
-  z = mulv<0xBF58476D1CE4E5B9ull, (M & 64)>(xsv<30, (M & 1)>(z));
-  z = mulv<0x94D049BB133111EBull, (M & 128)>(xsv<27, (M & 2)>(z));
+  z = mulv<0xBF58476D1CE4E5B9ull, (M & 64) ? 1 : (M & 1024) ? 2 : 0>(xsv<30, (M & 1)>(z));
+  z = mulv<0x94D049BB133111EBull, (M & 128) ? 1 : (M & 2048) ? 2 : 0>(xsv<27, (M & 2)>(z));
   z = xsv<31, (M & 4)>(z);
   z.lo ^= l.lo; z.hi ^= l.hi;
-  z = mulv<0xBF58476D1CE4E5B9ull, (M & 256)>(xsv<30, (M & 8)>(z));
-  z = mulv<0x94D049BB133111EBull, (M & 512)>(xsv<27, (M & 16)>(z));
+  z = mulv<0xBF58476D1CE4E5B9ull, (M & 256) ? 1 : (M & 4096) ? 2 : 0>(xsv<30, (M & 8)>(z));
+  z = mulv<0x94D049BB133111EBull, (M & 512) ? 1 : (M & 8192) ? 2 : 0>(xsv<27, (M & 16)>(z));
   uint32_t hs; if (M & 32) asm("shr.b32 %0, %1, 31;" : "=r"(hs) : "r"(z.hi)); else hs = __umulhi(z.hi, 2u);
   return z.hi ^ hs;
 }
@@ -73,6 +92,9 @@ int main() {
   cudaMemcpyToSymbol(P2, p, sizeof p);
   ulonglong2* keys; cudaMalloc(&keys, 4096 * 16); cudaMemset(keys, 7, 4096 * 16);
   int* out; cudaMalloc(&out, 4);
-  run<63>(keys, out); run<63+64>(keys, out); run<63+64+128>(keys, out); run<63+1024-64>(keys, out); run<63+512>(keys, out); run<0>(keys, out); run<960>(keys, out);
+  run<63>(keys, out); run<63+64>(keys, out); run<63+64+128>(keys, out); run<63+512>(keys, out); run<0>(keys, out); run<960>(keys, out);
+  run<63+1024+2048+4096+8192>(keys, out); run<0+1024+2048+4096+8192>(keys, out); run<63+1024+2048+4096>(keys, out);
+  run<63+960>(keys, out); run<31+960>(keys, out); run<32+1+2+4+960>(keys, out); run<32+1+2+4+15360>(keys, out);
+  run<32+8+16+4+15360>(keys, out); run<32+4+15360>(keys, out);
   return 0;
 }
