@@ -65,6 +65,10 @@ enum {
 int shk_ctx_set_option(shk_ctx* ctx, int opt, int64_t value);
 /* Device memory from the context's caching pool (bench / zero-copy users). */
 int shk_dev_alloc(shk_ctx* ctx, size_t bytes, void** out);
+/* Page-locked host memory (host<->device copies at full PCIe/C2C rate, and
+ * asynchronous on the context stream). */
+int shk_host_alloc(shk_ctx* ctx, size_t bytes, void** out);
+int shk_host_free(shk_ctx* ctx, void* p);
 int shk_dev_free(shk_ctx* ctx, void* p);
 int shk_memcpy(shk_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /*0 H2D 1 D2H 2 D2D*/);
 /* Events on the context stream: elapsed milliseconds between two records. */

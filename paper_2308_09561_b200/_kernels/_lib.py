@@ -65,6 +65,8 @@ _SIGS = {
     "shk_ctx_set_option": (_I, [_P, _I, _I64]),
     "shk_dev_alloc": (_I, [_P, ctypes.c_size_t, _P]),
     "shk_dev_free": (_I, [_P, _P]),
+    "shk_host_alloc": (_I, [_P, ctypes.c_size_t, _P]),
+    "shk_host_free": (_I, [_P, _P]),
     "shk_memcpy": (_I, [_P, _P, _P, ctypes.c_size_t, _I]),
     "shk_timer_start": (_I, [_P]),
     "shk_timer_stop": (_I, [_P, _P]),

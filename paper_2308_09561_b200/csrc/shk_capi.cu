@@ -239,6 +239,16 @@ int shk_ctx_set_option(shk_ctx* c, int opt, int64_t value) {
 }
 
 int shk_dev_alloc(shk_ctx* c, size_t bytes, void** out) { return pool_alloc(c, bytes, out); }
+int shk_host_alloc(shk_ctx* c, size_t bytes, void** out) {
+  (void)c;
+  SHK_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+  return 0;
+}
+int shk_host_free(shk_ctx* c, void* p) {
+  (void)c;
+  if (p) SHK_CUDA(cudaFreeHost(p));
+  return 0;
+}
 int shk_dev_free(shk_ctx* c, void* p) {
   pool_free(c, p);
   return 0;

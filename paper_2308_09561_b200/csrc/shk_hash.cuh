@@ -267,6 +267,9 @@ SHK_D uint32_t shl_clamp(uint32_t v, uint32_t s) {
   asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
   return r;
 }
+
+// v << (s mod 32) (SHF.L.W).
+SHK_D uint32_t shl_wrap(uint32_t v, uint32_t s) { return __funnelshift_l(0u, v, s); }
 #endif
 
 }  // namespace shk

@@ -229,6 +229,34 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
   team_sync<TW>(team);
 }
 
+// Cells of one key in the rotation search: OR its two cells into the A or B
+// coverage mask (bit = split bit, 1 = B) and store its packed edge.
+template <bool WIDE>
+SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_t& ma0, uint32_t& ma1,
+                         uint32_t& mb0, uint32_t& mb1, uint32_t& na, uint16_t* e) {
+  uint32_t h0, h1;
+  leaf_pair_d(v, un, unm1, h0, h1);
+  const uint32_t sel = 0u - bit;  // all ones for B
+  uint32_t c0, c1 = 0;
+  if (!WIDE) {
+    c0 = (1u << h0) | (1u << h1);
+  } else {
+    // 64-bit one-hots: low word clamps to 0 for h >= 32, and the wrapped
+    // shift (h mod 32) differs from it exactly when h >= 32
+    const uint32_t l0 = shl_clamp(1u, h0), l1 = shl_clamp(1u, h1);
+    c0 = l0 | l1;
+    c1 = (shl_wrap(1u, h0) ^ l0) | (shl_wrap(1u, h1) ^ l1);
+  }
+  mb0 |= c0 & sel;
+  ma0 |= c0 & ~sel;
+  if (WIDE) {
+    mb1 |= c1 & sel;
+    ma1 |= c1 & ~sel;
+  }
+  na += bit ^ 1u;
+  *e = (uint16_t)(h0 | (h1 << 8) | (bit << 15));
+}
+
 // Rotation fitting of one leaf: lane per base seed.
 template <int TW, bool WIDE, class SM>
 SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafOut& o, int team,
@@ -257,36 +285,28 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
         const uint64_t sa = ck ? base - base % (uint64_t)ck : base;
         ws = (base == 0) || (ck == 0) || (base % (uint64_t)ck == 0);
         const u2 xb = seed_mixer_pre_d(sa, TAG_SPLITBIT);
-        const u2 xa = seed_mixer_pre_d(sa, TAG_LEAF);
         const u2 xg = seed_mixer_pre_d(base, TAG_LEAF);
         uint32_t ma0 = 0, ma1 = 0, mb0 = 0, mb1 = 0;
+        if (ck == 0) {  // A and B keys share the leaf seed (sa == base)
 #pragma unroll 2
-        for (int i = 0; i < n; ++i) {
-          uint4 k = sm.keys[i];
-          u2 kh{k.x, k.y}, kl{k.z, k.w};
-          uint32_t bit = remix_top_pre_d(kh, kl, xb);
-          u2 x;
-          x.lo = bit ? xg.lo : xa.lo;
-          x.hi = bit ? xg.hi : xa.hi;
-          u2 v = remix_pre_d(kh, kl, x);
-          uint32_t h0, h1;
-          leaf_pair_d(v, un, unm1, h0, h1);
-          uint32_t c0, c1 = 0;
-          if (!WIDE) {
-            c0 = (1u << h0) | (1u << h1);
-          } else {
-            c0 = shl_clamp(1u, h0) | shl_clamp(1u, h1);
-            c1 = shl_clamp(1u, h0 - 32u) | shl_clamp(1u, h1 - 32u);
+          for (int i = 0; i < n; ++i) {
+            const uint4 k = sm.keys[i];
+            const u2 kh{k.x, k.y}, kl{k.z, k.w};
+            const uint32_t bit = remix_top_pre_d(kh, kl, xb);
+            rot_key_cells<WIDE>(remix_pre_d(kh, kl, xg), un, unm1, bit, ma0, ma1, mb0, mb1, na, e + i * 32);
           }
-          if (bit) {
-            mb0 |= c0;
-            mb1 |= c1;
-          } else {
-            ma0 |= c0;
-            ma1 |= c1;
+        } else {
+          const u2 xa = seed_mixer_pre_d(sa, TAG_LEAF);
+#pragma unroll 2
+          for (int i = 0; i < n; ++i) {
+            const uint4 k = sm.keys[i];
+            const u2 kh{k.x, k.y}, kl{k.z, k.w};
+            const uint32_t bit = remix_top_pre_d(kh, kl, xb);
+            u2 x;
+            x.lo = bit ? xg.lo : xa.lo;
+            x.hi = bit ? xg.hi : xa.hi;
+            rot_key_cells<WIDE>(remix_pre_d(kh, kl, x), un, unm1, bit, ma0, ma1, mb0, mb1, na, e + i * 32);
           }
-          na += bit ^ 1u;
-          e[i * 32] = (uint16_t)(h0 | (h1 << 8) | (bit << 15));
         }
         // Rotation filter: the set of r with (mask_a | rotl_n(mask_b, r))
         // == full.  Cell j missing from A needs mask_b[(j - r) mod n], i.e.

@@ -61,17 +61,24 @@ SHK_D void split_partition(const ulonglong2* kp, ulonglong2* kw, ulonglong2* tmp
 
 // High word of remix(hi, lo, seed, tag) (all the split hash needs), from a
 // pre-mixed key high word and seed mixer (shk_hash.cuh, premix_hi).
+#ifndef SHK_SPLIT_SHIFT_MASK
+#define SHK_SPLIT_SHIFT_MASK 0  // bit i: xor-shift i of the split hash takes its high-word shift on the FMA pipe
+#endif
+template <int S, int I>
+SHK_D u2 split_xs(u2 z) {
+  return ((SHK_SPLIT_SHIFT_MASK >> I) & 1) ? xorshr<S>(z) : xorshr_alu<S>(z);
+}
 SHK_D uint32_t remix_hi_pre_d(u2 kp, u2 k_lo, u2 xp) {
   u2 z;
   z.lo = kp.lo ^ xp.lo;
   z.hi = kp.hi ^ xp.hi;
   z = mulc<MUL1>(z);
-  z = mulc<MUL2>(xorshr_alu<27>(z));
-  z = xorshr_alu<31>(z);
+  z = mulc<MUL2>(split_xs<27, 0>(z));
+  z = split_xs<31, 1>(z);
   z.lo ^= k_lo.lo;
   z.hi ^= k_lo.hi;
-  z = mulc<MUL1>(xorshr_alu<30>(z));
-  const uint32_t h = mulc_hi<MUL2>(xorshr_alu<27>(z));
+  z = mulc<MUL1>(split_xs<30, 2>(z));
+  const uint32_t h = mulc_hi<MUL2>(split_xs<27, 3>(z));
   return h ^ (h >> 31);  // hi word of z ^ (z >> 31)
 }
 

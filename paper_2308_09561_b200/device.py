@@ -48,6 +48,37 @@ class DeviceBuffer:
             pass
 
 
+class PinnedBuffer:
+    """Page-locked host memory with a numpy view (``.array``)."""
+
+    def __init__(self, nbytes: int, dtype=np.uint8):
+        self.nbytes = int(nbytes)
+        p = ctypes.c_void_p()
+        check(_lib.load_library().shk_host_alloc(ctx(), max(self.nbytes, 1), ctypes.byref(p)), "host alloc")
+        self.ptr = p.value
+        buf = (ctypes.c_uint8 * max(self.nbytes, 1)).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=np.uint8)[: self.nbytes].view(dtype)
+
+    @classmethod
+    def from_array(cls, a: np.ndarray) -> "PinnedBuffer":
+        a = np.ascontiguousarray(a)
+        b = cls(a.nbytes, a.dtype)
+        b.array[...] = a.reshape(-1)
+        return b
+
+    def free(self):
+        if self.ptr and _lib._lib is not None:
+            self.array = None
+            _lib._lib.shk_host_free(ctx(), self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 def sync():
     check(_lib.load_library().shk_ctx_sync(ctx()), "sync")
 
