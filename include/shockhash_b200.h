@@ -220,6 +220,12 @@ int shk_qdesc_create(shk_ctx* ctx, int64_t n_keys, int64_t nbuckets, int mode, i
                      int64_t stream_nwords, int64_t stream_bit_len, const shk_plans* plans, uint64_t rib_seed,
                      int64_t rib_m, const uint64_t* rib_words, int64_t rib_nwords, shk_qdesc** out);
 int shk_query(shk_qdesc* d, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out, int clamp, int flags);
+/* MphfDescriptor.verify (recsplit.py:383-394) on the device: query the Q
+ * hashed keys (clamped) and check the outputs form a bijection onto [0, N).
+ * *ok = 1 iff so; otherwise *offender = the first input index whose output is
+ * out of range or repeats an earlier input's (-1 when Q != N). */
+int shk_verify(shk_qdesc* d, const uint64_t* hi, const uint64_t* lo, int64_t Q, int flags, int* ok,
+               int64_t* offender);
 int shk_qdesc_destroy(shk_qdesc* d);
 
 #ifdef __cplusplus

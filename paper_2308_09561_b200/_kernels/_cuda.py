@@ -428,6 +428,16 @@ class DeviceDescriptor:
             check(_L().shk_query(self.handle, ptr(hi), ptr(lo), len(hi), ptr(out), 1 if clamp else 0, 0), "query")
         return out
 
+    def verify(self, hi, lo):
+        """(ok, offender index or -1): outputs of the hashed keys form a
+        bijection onto [0, N), checked on the device."""
+        hi = u64(hi).ravel()
+        lo = u64(lo).ravel()
+        ok = ctypes.c_int(0)
+        off = ctypes.c_int64(-1)
+        check(_L().shk_verify(self.handle, ptr(hi), ptr(lo), len(hi), 0, ctypes.byref(ok), ctypes.byref(off)), "verify")
+        return bool(ok.value), int(off.value)
+
     def query_device(self, hi_ptr, lo_ptr, Q, out_ptr, clamp=True):
         """Stream-ordered query on device pointers (bench / zero-copy)."""
         check(_L().shk_query(self.handle, hi_ptr, lo_ptr, int(Q), out_ptr, 1 if clamp else 0, SHK_DEVICE), "query")

@@ -1514,6 +1514,46 @@ int shk_query(shk_qdesc* q, const uint64_t* hi, const uint64_t* lo, int64_t Q, u
   return 0;
 }
 
+int shk_verify(shk_qdesc* q, const uint64_t* hi, const uint64_t* lo, int64_t Q, int flags, int* ok,
+               int64_t* offender) {
+  shk_ctx* c = q->c;
+  *ok = 0;
+  *offender = -1;
+  const int64_t N = q->d.n_keys;
+  if (Q != N) return 0;  // not a bijection onto [0, N); no offender (recsplit.py:388-389)
+  if (N <= 0) {
+    *ok = 1;
+    return 0;
+  }
+  DBuf th(c), tl(c), vals(c), first(c), off(c);
+  const void *dh, *dl;
+  RC(stage_in(c, flags, hi, (size_t)Q * 8, th, &dh));
+  RC(stage_in(c, flags, lo, (size_t)Q * 8, tl, &dl));
+  RC(vals.alloc((size_t)Q * 8));
+  RC(first.alloc((size_t)N * 8));
+  RC(off.alloc(8));
+  int* err = c->d_counter + 5;
+  SHK_CUDA(cudaMemsetAsync(err, 0, 4, c->stream));
+  RC(shk_launch_query(q->d, (const uint64_t*)dh, (const uint64_t*)dl, Q, vals.as<uint64_t>(), err, 1, c->stream));
+  RC(shk_launch_bijection(vals.as<uint64_t>(), Q, N, first.as<unsigned long long>(), off.as<unsigned long long>(),
+                          c->stream));
+  int herr = 0;
+  unsigned long long hoff = 0;
+  RC(d2h(c, &herr, err, 4));
+  RC(d2h(c, &hoff, off.p, 8));
+  RC(csync(c));
+  if (herr) {
+    shk_set_error("bit stream overrun");
+    return SHK_FORMAT;
+  }
+  if (hoff == ~0ull) {
+    *ok = 1;
+  } else {
+    *offender = (int64_t)hoff;
+  }
+  return 0;
+}
+
 int shk_qdesc_destroy(shk_qdesc* q) {
   delete q;
   return 0;

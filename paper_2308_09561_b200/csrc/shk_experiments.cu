@@ -83,8 +83,9 @@ __global__ void mc_filter_kernel(const uint64_t* __restrict__ khi, const uint64_
 // is valid (<= one cycle) iff edges <= nodes, and a tuple is a pseudoforest iff
 // every component is valid, the same predicate as the reference's union-find
 // (cycle into a cyclic component, or merging two cyclic ones, fails).
-// Threads own prefixes of n-2 edges, loop over edge n-1 and count edge n in
-// closed form from the component sizes.
+// Threads own prefixes of n-2 edges, loop over the ordered component pairs
+// edge n-1 can join (weighted by their vertex-pair counts) and count edge n
+// in closed form from the component sizes.
 
 SHK_D uint64_t byte_spread(uint32_t mask8) {
   // byte i = 0xFF iff bit i of mask8
@@ -158,11 +159,28 @@ __global__ void enum_kernel(uint64_t nprefix, unsigned long long* out) {
     }
     if (!ok) continue;
     if (LOOP) {
-      for (uint32_t e = 0; e < T; ++e) {
-        uint64_t CM2 = CM;
-        uint32_t EC2 = EC;
-        int c2 = comps;
-        if (add_edge(CM2, EC2, c2, e / N, e % N)) close_last<N>(CM2, EC2, c2, pf, s2);
+      // edge n-1 only matters through the components of its endpoints: loop
+      // over ordered component pairs (C, D), weight |C| |D| vertex pairs
+      uint32_t reps = 0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const uint32_t c = (uint32_t)(CM >> (8 * i)) & 0xFFu;
+        if ((c & ((2u << i) - 1u)) == (1u << i)) reps |= 1u << i;
+      }
+      for (uint32_t ru = reps; ru; ru &= ru - 1) {
+        const uint32_t u = __ffs(ru) - 1, su = __popc((uint32_t)(CM >> (8 * u)) & 0xFFu);
+        for (uint32_t rv = reps; rv; rv &= rv - 1) {
+          const uint32_t v = __ffs(rv) - 1, sv = __popc((uint32_t)(CM >> (8 * v)) & 0xFFu);
+          uint64_t CM2 = CM;
+          uint32_t EC2 = EC;
+          int c2 = comps;
+          if (add_edge(CM2, EC2, c2, u, v)) {
+            unsigned long long p1 = 0, q1 = 0;
+            close_last<N>(CM2, EC2, c2, p1, q1);
+            pf += p1 * (su * sv);
+            s2 += q1 * (su * sv);
+          }
+        }
       }
     } else {
       close_last<N>(CM, EC, comps, pf, s2);

@@ -182,6 +182,11 @@ struct ShkQueryDesc {
 int shk_launch_node_index(const ShkQueryDesc& d, int64_t* node_pos, int32_t* bucket_bad, cudaStream_t st);
 int shk_launch_query(const ShkQueryDesc& d, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out,
                      int* err, int clamp, cudaStream_t st);
+// Bijection check of Q values against [0, N): *offender = first index whose
+// value is out of range or repeats an earlier one (all ones if none).
+// first: N scratch slots.
+int shk_launch_bijection(const uint64_t* v, int64_t Q, int64_t N, unsigned long long* first,
+                         unsigned long long* offender, cudaStream_t st);
 
 // Rice-decode a sequence of codes (test / seam parity).
 int shk_launch_rice_decode(const uint64_t* words, int64_t bit_len, int64_t pos, const int32_t* g, int64_t count,

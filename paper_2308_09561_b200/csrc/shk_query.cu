@@ -122,6 +122,24 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
   }
 }
 
+// Bijection check of query outputs (MphfDescriptor.verify, recsplit.py:383-394):
+// first[v] = first input index mapping to v; the offender is the first input
+// index whose value is out of range or was produced by an earlier index.
+__global__ void first_index_kernel(const uint64_t* v, int64_t Q, int64_t N, unsigned long long* first) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = v[i];
+    if (x < (uint64_t)N) atomicMin(&first[x], (unsigned long long)i);
+  }
+}
+
+__global__ void offender_kernel(const uint64_t* v, int64_t Q, int64_t N, const unsigned long long* first,
+                                unsigned long long* offender) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = v[i];
+    if (x >= (uint64_t)N || first[x] != (unsigned long long)i) atomicMin(offender, (unsigned long long)i);
+  }
+}
+
 }  // namespace shk
 
 using namespace shk;
@@ -140,6 +158,20 @@ int shk_launch_query(const ShkQueryDesc& d, const uint64_t* hi, const uint64_t* 
   int64_t g = (Q + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   query_kernel<<<(unsigned)g, 256, 0, st>>>(d, hi, lo, Q, out, err, clamp);
+  SHK_LAUNCHED();
+  return 0;
+}
+
+int shk_launch_bijection(const uint64_t* v, int64_t Q, int64_t N, unsigned long long* first,
+                         unsigned long long* offender, cudaStream_t st) {
+  SHK_CUDA(cudaMemsetAsync(first, 0xFF, (size_t)N * 8, st));
+  SHK_CUDA(cudaMemsetAsync(offender, 0xFF, 8, st));
+  if (Q <= 0) return 0;
+  int64_t g = (Q + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  first_index_kernel<<<(unsigned)g, 256, 0, st>>>(v, Q, N, first);
+  SHK_LAUNCHED();
+  offender_kernel<<<(unsigned)g, 256, 0, st>>>(v, Q, N, first, offender);
   SHK_LAUNCHED();
   return 0;
 }

@@ -274,7 +274,18 @@ def part_experiments():
     for n, trials, ent in [(1, 1000, 0), (2, 1000, 1), (12, 2000, 42), (16, 300000, 7), (24, 200000, 3),
                            (32, 300000, 5), (40, 100000, 2**64 - 3), (56, 50000, 11), (64, 50000, 13)]:
         mc.append(dict(n=n, trials=trials, entropy=ent, passes=int(K.mc_filter_pass_count(n, trials, ent))))
-    dump("experiments.json", dict(bruteforce=brute, enumerate=enum, mc_filter=mc))
+    from shockhash_ref import experiments as ex
+
+    trials = []
+    for ns, mode, reps, seed in [([4, 8], "plain", 300, 2), ([10], "rotate", 300, 2), ([12, 16], "plain", 200, 7),
+                                 ([24], "rotate", 100, 1), ([36], "rotate-cached", 20, 3), ([6], "bruteforce", 50, 1)]:
+        for r in ex.trial_statistics(ns, mode, reps, seed):
+            trials.append(dict(n=r.n, mode=r.mode, reps=r.reps, seed=seed, mean_seed=r.mean_seed,
+                               mean_log2_seed=r.mean_log2_seed, overhead_bits=r.overhead_bits))
+    comp = [dict(n=n, trials=t, seed=s, value=ex.mc_component_factor(n, t, s)) for n, t, s in [(8, 2000, 5), (16, 500, 1)]]
+    filt = [dict(n=n, trials=t, seed=s, value=ex.mc_filter_pass(n, t, s)) for n, t, s in [(16, 40000, 3), (32, 40000, 3)]]
+    dump("experiments.json", dict(bruteforce=brute, enumerate=enum, mc_filter=mc, trial_statistics=trials,
+                                  component=comp, filter_pass=filt))
 
 
 if __name__ == "__main__":
