@@ -17,7 +17,7 @@
 //      reached; passes repeat until no row overflows;
 //   3. back substitution over back-chunks of CB columns runs in parallel
 //      with the solution of the 127 columns right of each chunk as symbolic
-//      unknowns: a warp carries 128 bit-sliced affine forms (4 per lane), so
+//      unknowns: a CTA carries 128 bit-sliced affine forms (one per lane), so
 //      each chunk yields the affine map from its right neighbour's first 127
 //      bits to its own first 127 bits;
 //   4. a single warp walks the chunks right to left evaluating those maps
@@ -29,7 +29,13 @@
 
 namespace shk {
 
-constexpr int CE = 1024;  // elimination chunk (columns)
+// Elimination chunk (columns).  Measured at C4: 512 -> ribbon 4.9 ms, 1024 ->
+// 5.2, 256 -> 5.6, 2048 -> 7.1 (smaller chunks: more resident warps per SM,
+// more rows overflowing into later passes).
+#ifndef SHK_RIBBON_CE
+#define SHK_RIBBON_CE 512
+#endif
+constexpr int CE = SHK_RIBBON_CE;
 constexpr int CB = 8192;  // back-substitution chunk (columns), multiple of CE and 64
 
 struct RRow {
@@ -159,17 +165,29 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
   uint64_t a0 = 0, a1 = 0;
   uint32_t b = 0;
   int j = 0;
-  auto fetch = [&]() {
-    active = next < nrows;
-    if (active) {
-      const RRow r = rows[r0 + next];
+  // Each lane keeps its following row in registers: the global load is
+  // issued when the current row starts and consumed when it finishes, so its
+  // latency hides behind the current row's elimination steps.
+  RRow pre{0, 0, 0};
+  bool have_pre = false;
+  auto load_pre = [&]() {
+    have_pre = next < nrows;
+    if (have_pre) {
+      pre = rows[r0 + next];
       next += 32;
-      a0 = r.p0;
-      a1 = r.p1;
-      b = (r.s & RHS_BIT) ? 1u : 0u;
-      j = (int)((r.s & S_MASK) - base);
     }
   };
+  auto fetch = [&]() {
+    active = have_pre;
+    if (active) {
+      a0 = pre.p0;
+      a1 = pre.p1;
+      b = (pre.s & RHS_BIT) ? 1u : 0u;
+      j = (int)((pre.s & S_MASK) - base);
+    }
+    load_pre();
+  };
+  load_pre();
   fetch();
   while (__any_sync(FULL_WARP, active)) {
     // phase A: read the slot at the current pivot
@@ -243,86 +261,70 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
 }
 
 // ---------------------------------------------------------------------------
-// Symbolic back substitution (affine forms), one warp per back-chunk.
-// Lane L owns unknowns u = 4L..4L+3 (u = 127 is the constant term); for each
-// it keeps W_u: a 128-bit window whose bit k is the coefficient of u in
-// sol[c + 1 + k].  forms_out[chunk][u] = W_u after the chunk's first column.
-// Every column's own affine form is also written (coef[col], 4 ballots of the
-// new bits: word q bit L = coefficient of unknown 4L + q), so the final pass
-// is a parallel map instead of a second sequential walk.
-__global__ void __launch_bounds__(32) ribbon_forms_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
-                                                          const uint64_t* sp1, const uint32_t* occ,
-                                                          const uint32_t* sbit, uint4* forms, uint4* coef) {
-  __shared__ uint64_t tp0[256], tp1[256];
-  __shared__ uint4 tcoef[256];
-  __shared__ uint32_t tocc[8], tsb[8];
+// Symbolic back substitution (affine forms), one CTA of 4 warps per
+// back-chunk.  Warp q, lane L owns unknown u = 4L + q (u = 127 is the
+// constant term) and keeps W_u: a 128-bit window whose bit k is the
+// coefficient of u in sol[c + 1 + k].  forms_out[chunk][u] = W_u after the
+// chunk's first column.  Every column's own affine form is also written
+// (coef[col], word q = ballot of warp q's new bits: bit L = coefficient of
+// unknown 4L + q), so the final pass is a parallel map instead of a second
+// sequential walk.  The CTA stages 256-column tiles of pivot patterns as
+// (p >> 1) in four words, zero for free columns, so the per-column loop of a
+// warp is branch-free: LDS.128, 4 AND/XOR, POPC, ballot, window shift.
+__global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
+                                                           const uint64_t* sp1, const uint32_t* occ,
+                                                           const uint32_t* sbit, uint4* forms, uint4* coef) {
+  __shared__ uint4 tpw[256];
+  __shared__ uint32_t tcoef[256][4];
+  __shared__ uint32_t tsb[8];
   const int64_t c = blockIdx.x;
   if (c >= nbchunks) return;
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
+  const int u = 4 * lane + q;
   const int64_t s0 = c * CB;
   const int64_t e = (s0 + CB < m) ? s0 + CB : m;
-  uint32_t W[4][4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int u = 4 * lane + q;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) W[q][w] = (u < 127 && (u >> 5) == w) ? (1u << (u & 31)) : 0u;
+  uint32_t W0 = 0, W1 = 0, W2 = 0, W3 = 0;
+  if (u < 127) {
+    const uint32_t b = 1u << (u & 31);
+    W0 = (u >> 5) == 0 ? b : 0u;
+    W1 = (u >> 5) == 1 ? b : 0u;
+    W2 = (u >> 5) == 2 ? b : 0u;
+    W3 = (u >> 5) == 3 ? b : 0u;
   }
+  const bool konst = (u == 127);
   // process columns e-1 down to s0 in tiles of 256 (tile start aligned to 256)
   int64_t col = e - 1;
   while (col >= s0) {
     const int64_t tstart = (col / 256) * 256 > s0 ? (col / 256) * 256 : s0;
     const int ntile = (int)(col - tstart + 1);
-    __syncwarp();
-    for (int j = lane; j < ntile; j += 32) {
-      tp0[j] = sp0[tstart + j];
-      tp1[j] = sp1[tstart + j];
+    for (int j = tid; j < ntile; j += 128) {
+      const int64_t cc = tstart + j;
+      const bool o = (occ[cc >> 5] >> (cc & 31)) & 1u;
+      const uint64_t a0 = o ? sp0[cc] : 0ull, a1 = o ? sp1[cc] : 0ull;
+      // p >> 1 as four 32-bit words
+      tpw[j] = make_uint4((uint32_t)(a0 >> 1) | ((uint32_t)(a0 >> 32) << 31),
+                          (uint32_t)(a0 >> 33) | ((uint32_t)a1 << 31),
+                          (uint32_t)(a1 >> 1) | ((uint32_t)(a1 >> 32) << 31), (uint32_t)(a1 >> 33));
     }
-    if (lane < 8) {
-      int64_t wi = tstart / 32 + lane;
-      bool in = (int64_t)lane * 32 < ntile;
-      tocc[lane] = in ? occ[wi] : 0;
-      tsb[lane] = in ? sbit[wi] : 0;
-    }
-    __syncwarp();
+    if (tid < 8) tsb[tid] = (tid * 32 < ntile) ? sbit[tstart / 32 + tid] : 0u;  // rhs bits (0 on free columns)
+    __syncthreads();
     for (int j = ntile - 1; j >= 0; --j) {
-      const uint32_t o = (tocc[j >> 5] >> (j & 31)) & 1u;
-      uint32_t nb[4] = {0, 0, 0, 0};
-      if (o) {
-        const uint64_t a0 = tp0[j], a1 = tp1[j];
-        // p >> 1 as four 32-bit words
-        const uint32_t pw0 = (uint32_t)(a0 >> 1) | ((uint32_t)(a0 >> 32) << 31);
-        const uint32_t pw1 = (uint32_t)(a0 >> 33) | ((uint32_t)a1 << 31);
-        const uint32_t pw2 = (uint32_t)(a1 >> 1) | ((uint32_t)(a1 >> 32) << 31);
-        const uint32_t pw3 = (uint32_t)(a1 >> 33);
-        const uint32_t b = (tsb[j >> 5] >> (j & 31)) & 1u;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t x = (W[q][0] & pw0) ^ (W[q][1] & pw1) ^ (W[q][2] & pw2) ^ (W[q][3] & pw3);
-          nb[q] = __popc(x) & 1u;
-        }
-        if (lane == 31) nb[3] ^= b;  // u = 127: constant term
-        const uint32_t b0 = __ballot_sync(FULL_WARP, nb[0]), b1 = __ballot_sync(FULL_WARP, nb[1]);
-        const uint32_t b2 = __ballot_sync(FULL_WARP, nb[2]), b3 = __ballot_sync(FULL_WARP, nb[3]);
-        if (lane == 0) tcoef[j] = make_uint4(b0, b1, b2, b3);
-      } else if (lane == 0) {
-        tcoef[j] = make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        W[q][3] = (W[q][3] << 1) | (W[q][2] >> 31);
-        W[q][2] = (W[q][2] << 1) | (W[q][1] >> 31);
-        W[q][1] = (W[q][1] << 1) | (W[q][0] >> 31);
-        W[q][0] = (W[q][0] << 1) | nb[q];
-      }
+      const uint4 p = tpw[j];
+      uint32_t nb = __popc((W0 & p.x) ^ (W1 & p.y) ^ (W2 & p.z) ^ (W3 & p.w)) & 1u;
+      if (konst) nb ^= (tsb[j >> 5] >> (j & 31)) & 1u;
+      const uint32_t bal = __ballot_sync(FULL_WARP, nb);
+      if (lane == 0) tcoef[j][q] = bal;
+      W3 = __funnelshift_l(W2, W3, 1);
+      W2 = __funnelshift_l(W1, W2, 1);
+      W1 = __funnelshift_l(W0, W1, 1);
+      W0 = (W0 << 1) | nb;
     }
-    __syncwarp();
-    for (int j = lane; j < ntile; j += 32) coef[tstart + j] = tcoef[j];
+    __syncthreads();
+    for (int j = tid; j < ntile; j += 128)
+      coef[tstart + j] = make_uint4(tcoef[j][0], tcoef[j][1], tcoef[j][2], tcoef[j][3]);
     col = tstart - 1;
   }
-  uint4* f = forms + c * 128;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) f[4 * lane + q] = make_uint4(W[q][0], W[q][1], W[q][2], W[q][3]);
+  forms[c * 128 + u] = make_uint4(W0, W1, W2, W3);
 }
 
 // Right-to-left chain over back-chunks: y = first 127 solution bits of chunk
@@ -579,7 +581,7 @@ int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_
     return 0;
   }
   *consistent = 1;
-  ribbon_forms_kernel<<<(unsigned)nbc, 32, 0, st>>>(m, nbc, sp0, sp1, occ, sb, forms, coef);
+  ribbon_forms_kernel<<<(unsigned)nbc, 128, 0, st>>>(m, nbc, sp0, sp1, occ, sb, forms, coef);
   SHK_LAUNCHED();
   ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, forms, yb);
   SHK_LAUNCHED();
