@@ -24,6 +24,8 @@
 //      (the only sequential step: 127x128 GF(2) mat-vec per chunk);
 //   5. every column's solution bit is then parity(its affine form & its
 //      chunk's boundary), a fully parallel map (step 3 stored the forms).
+#include <cuda_pipeline.h>
+
 #include "shk_common.cuh"
 #include "shk_kernels.h"
 
@@ -332,19 +334,28 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
 // loaded while the current one is evaluated.  ysel[c] is the boundary in the
 // coef layout (word q bit L = y bit 4L + q; bit 127 = 1 for the constant).
 __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, const uint4* forms, uint4* ysel) {
+  // D-deep cp.async ring: the forms of chunk c - D are in flight while chunk
+  // c is evaluated (each lane copies and later reads only its own 64 bytes).
+  constexpr int D = 8;
+  __shared__ uint4 ring[D][128];
   const int lane = threadIdx.x;
   uint4 y = make_uint4(0, 0, 0, 0);  // boundary right of the last chunk: zero
-  uint4 nxt[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) nxt[q] = forms[(nbchunks - 1) * 128 + 4 * lane + q];
+  for (int k = 0; k < D; ++k) {
+    const int64_t cc = nbchunks - 1 - k;
+    if (cc >= 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        __pipeline_memcpy_async(&ring[k][4 * lane + q], forms + cc * 128 + 4 * lane + q, sizeof(uint4));
+    }
+    __pipeline_commit();
+  }
+  int slot = 0;
   for (int64_t c = nbchunks - 1; c >= 0; --c) {
+    __pipeline_wait_prior(D - 1);
     uint4 w[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) w[q] = nxt[q];
-    if (c > 0) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) nxt[q] = __ldcg(forms + (c - 1) * 128 + 4 * lane + q);
-    }
+    for (int q = 0; q < 4; ++q) w[q] = ring[slot][4 * lane + q];
     uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
     uint32_t sel[4];
 #pragma unroll
@@ -358,6 +369,14 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
       acc2 ^= w[q].z & msk;
       acc3 ^= w[q].w & msk;
     }
+    // refill the slot just consumed (after its values were used)
+    if (c - D >= 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        __pipeline_memcpy_async(&ring[slot][4 * lane + q], forms + (c - D) * 128 + 4 * lane + q, sizeof(uint4));
+    }
+    __pipeline_commit();
+    slot = (slot + 1 == D) ? 0 : slot + 1;
     const uint32_t s0 = __ballot_sync(FULL_WARP, sel[0]), s1 = __ballot_sync(FULL_WARP, sel[1]);
     const uint32_t s2 = __ballot_sync(FULL_WARP, sel[2]), s3 = __ballot_sync(FULL_WARP, sel[3]);
     if (lane == 0) ysel[c] = make_uint4(s0, s1, s2, s3);
