@@ -315,13 +315,38 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
         const uint64_t full = (n == 64) ? ~0ull : ((1ull << n) - 1);
         const uint64_t ma = join64(ma0, ma1), mb = join64(mb0, mb1);
         uint64_t need = ~ma & full;
-        uint64_t rv = __brevll(mb) >> (64 - n);        // bit k = mb[n-1-k]
-        rv = ((rv << 1) | (rv >> (n - 1))) & full;      // bit k = mb[(n-k) mod n]
+        // E (128 bits): bit t = mb[(2n - 1 - t) mod n], the B mask written
+        // twice and reversed.  Cell j is covered after rotation r iff
+        // mb[(j - r) mod n] = E[n - 1 - j + r], so the rotations covering j
+        // are the bits of E >> (n - 1 - j): one funnel shift per missing cell.
+        const uint64_t dl = (n == 64) ? mb : (mb | (mb << n));   // D = mb | mb << n, low word
+        const uint64_t dh = (n == 64) ? mb : (mb >> (64 - n));   // D, high word
+        // E = reverse128(D) >> (128 - 2n)
+        const uint64_t rl = __brevll(dh), rh = __brevll(dl);     // reverse128(D) = (rh:rl)
+        const int sh = 128 - 2 * n;                              // 0 .. 126
+        uint64_t el, eh;
+        if (sh >= 64) {
+          el = rh >> (sh - 64);
+          eh = 0;
+        } else if (sh > 0) {
+          el = (rl >> sh) | (rh << (64 - sh));
+          eh = rh >> sh;
+        } else {
+          el = rl;
+          eh = rh;
+        }
+        // (E >> s) for s in [0, 63] without a select: (eh << 1) << (63 - s)
+        const uint64_t eh1 = eh << 1;
         uint64_t Rm = full;
-        while (need && Rm) {
-          const int j = __ffsll((long long)need) - 1;
-          need &= need - 1;
-          Rm &= j ? (((rv << j) | (rv >> (n - j))) & full) : rv;
+        // missing cells word by word (32-bit lowest-bit extraction is cheap)
+        for (int hw = 0; hw < 2; ++hw) {
+          uint32_t w = hw ? (uint32_t)(need >> 32) : (uint32_t)need;
+          const int nb1 = n - 1 - 32 * hw;
+          while (w && Rm) {
+            const int s = nb1 - (__ffs(w) - 1);  // n - 1 - j, in [0, n - 1]
+            w &= w - 1;
+            Rm &= (el >> s) | (eh1 << (63 - s));
+          }
         }
         passmask = Rm;
       }
