@@ -40,6 +40,10 @@ enum {
   SHK_DUPLICATE = 5   /* equal 128-bit codes in a build */
 };
 #define SHK_DEVICE 1
+/* shk_blake2b128_fixed only: the key blob is host memory (page-locked for
+ * full speed), hi/lo are device pointers; the copy is pipelined in chunks
+ * with the hashing (copy stream + main stream). */
+#define SHK_BLOB_HOST 2
 
 typedef struct shk_ctx shk_ctx;
 typedef struct shk_build shk_build;

@@ -48,6 +48,7 @@ struct shk_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;  // side stream for pipelined host->device copies
   int num_sms = 148;
   std::multimap<size_t, void*> free_blocks;
   std::unordered_map<void*, size_t> live;
@@ -198,6 +199,7 @@ int shk_ctx_create(int device, shk_ctx** out) {
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
   SHK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  SHK_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
   c->stream = c->own;
   SHK_CUDA(cudaMalloc(&c->d_counter, 256));
   SHK_CUDA(cudaEventCreate(&c->t0));
@@ -218,6 +220,7 @@ int shk_ctx_destroy(shk_ctx* c) {
   cudaEventDestroy(c->t0);
   cudaEventDestroy(c->t1);
   cudaStreamDestroy(c->own);
+  cudaStreamDestroy(c->copy);
   delete c;
   return 0;
 }
@@ -739,6 +742,34 @@ int shk_blake2b128_fixed(shk_ctx* c, const uint8_t* blob, int key_len, int64_t N
     return SHK_INVALID;
   }
   DBuf tb(c), th(c), tl(c);
+  if (flags & SHK_BLOB_HOST) {
+    // chunked: the H2D of chunk k+1 (copy stream) overlaps the hashing of
+    // chunk k (context stream); host-blocking, like every host-input call
+    const int64_t nchunk = 8;
+    const int64_t per = (N + nchunk - 1) / nchunk;
+    RC(tb.alloc((size_t)key_len * N));
+    cudaEvent_t ev[8];
+    for (int k = 0; k < nchunk; ++k) SHK_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    int rc = 0;
+    for (int64_t k = 0; k < nchunk && !rc; ++k) {
+      const int64_t a = k * per, b = (a + per < N) ? a + per : N;
+      if (a >= b) break;
+      const size_t off = (size_t)a * key_len, len = (size_t)(b - a) * key_len;
+      cudaError_t e = cudaMemcpyAsync(tb.as<uint8_t>() + off, blob + off, len, cudaMemcpyHostToDevice, c->copy);
+      if (e == cudaSuccess) e = cudaEventRecord(ev[k], c->copy);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, ev[k], 0);
+      if (e != cudaSuccess) {
+        shk_set_error("blake2b chunked copy: %s", cudaGetErrorString(e));
+        rc = -1000 - (int)e;
+        break;
+      }
+      rc = shk_launch_blake2b_fixed(tb.as<uint8_t>() + off, key_len, b - a, salt, hi + a, lo + a, c->stream);
+    }
+    cudaStreamSynchronize(c->copy);
+    cudaStreamSynchronize(c->stream);
+    for (int k = 0; k < nchunk; ++k) cudaEventDestroy(ev[k]);
+    return rc;
+  }
   const void* db;
   void *dh, *dl;
   RC(stage_in(c, flags, blob, (size_t)key_len * N, tb, &db));

@@ -120,6 +120,18 @@ def blake2b_fixed_device(d_blob: DeviceBuffer, key_len: int, N: int, salt: int, 
                                                    d_lo.ptr, SHK_DEVICE), "blake2b")
 
 
+SHK_BLOB_HOST = 2
+
+
+def blake2b_fixed_from_host(blob: np.ndarray, key_len: int, N: int, salt: int, d_hi: DeviceBuffer,
+                            d_lo: DeviceBuffer):
+    """Host key blob (ideally a PinnedBuffer's array) -> device codes; the
+    H2D copy is chunked and overlapped with the hashing."""
+    blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    check(_lib.load_library().shk_blake2b128_fixed(ctx(), blob.ctypes.data, int(key_len), int(N), int(salt), d_hi.ptr,
+                                                   d_lo.ptr, SHK_BLOB_HOST), "blake2b")
+
+
 def blake2b_fixed_host(blob: np.ndarray, key_len: int, salt: int = 0):
     """Host buffers in, host codes out; H2D/D2H inside the call."""
     blob = np.ascontiguousarray(blob, dtype=np.uint8)
