@@ -49,8 +49,11 @@ SHK_D void publish(int64_t* p, int64_t v) {
   asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// MAXE: leaf buffer capacity; MINB: CTAs per SM requested from ptxas (the
-// 40-key variant fits 10 CTAs = 40 warps per SM in registers and smem).
+// MAXE: leaf buffer capacity; MINB: CTAs per SM requested from ptxas (8 = 64
+// registers; see SHK_TREE_MINB).
+#ifndef SHK_TREE_MINB
+#define SHK_TREE_MINB 8
+#endif
 template <bool WIDE, int MODE, int MAXE, int MINB>
 __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
   __shared__ LeafSmem<1, MAXE> sm_all[4];
@@ -184,12 +187,12 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   void (*kfn)(TreeArgs);
   if (p.mode == 0) {
     if (small)
-      kfn = wide ? tree_kernel<true, 0, 40, 8> : tree_kernel<false, 0, 40, 8>;
+      kfn = wide ? tree_kernel<true, 0, 40, SHK_TREE_MINB> : tree_kernel<false, 0, 40, SHK_TREE_MINB>;
     else
       kfn = tree_kernel<true, 0, 64, 8>;
   } else {
     if (small)
-      kfn = wide ? tree_kernel<true, 1, 40, 8> : tree_kernel<false, 1, 40, 8>;
+      kfn = wide ? tree_kernel<true, 1, 40, SHK_TREE_MINB> : tree_kernel<false, 1, 40, SHK_TREE_MINB>;
     else
       kfn = tree_kernel<true, 1, 64, 8>;
   }
