@@ -133,6 +133,29 @@ def input_keys():
     return k, blob
 
 
+NCU_TREE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_tree_latest.csv")
+
+
+def ncu_traffic():
+    """DRAM bytes (read + write) per launch of the tree kernel from the
+    committed `ncu --set full` summary (tools/summarize_ncu.py), or None."""
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    try:
+        import csv
+
+        tot = 0.0
+        seen = 0
+        with open(NCU_TREE_SUMMARY) as f:
+            for r in csv.DictReader(f):
+                if r["kernel"].startswith("void tree_kernel") and r["metric"] in ("dram__bytes_read.sum",
+                                                                                  "dram__bytes_write.sum"):
+                    tot += float(r["value"]) * scale.get(r.get("unit", "byte"), 1)
+                    seen += 1
+        return int(tot) if seen == 2 else None
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def roofline_numbers(prof, hash_evals, n, clock_mhz, sms):
     """Integer-issue roofline of the dominant kernel (split or leaf search)."""
     ph = prof["phase_ms"]
@@ -159,7 +182,8 @@ def roofline_numbers(prof, hash_evals, n, clock_mhz, sms):
         "peak": round(peak, 2),
         "unit": "Tops/s",
         "frac": round(ach / peak, 4),
-        "traffic": None,
+        "traffic": ncu_traffic() if dom.startswith("tree_kernel") else None,
+        "traffic_unit": "bytes per launch (dram read + write, profiles/ncu_tree_latest.csv)",
         "peak_source": "nominal 128 int32 ops/clk/SM x %d SMs x 1965 MHz (no integer peak in MEASURED_PEAKS.json)" % sms,
         "frac_at_run_clock": round(ach / (peak * clock_mhz / 1965.0), 4) if clock_mhz else None,
         "per_kernel": other,

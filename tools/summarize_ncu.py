@@ -69,16 +69,16 @@ def launches(src, out):
 def full(rep, out):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr = rows[0]
+    hdr, units = rows[0], dict(zip(rows[0], rows[1]))
     with open(out, "w", newline="") as f:
         w = csv.writer(f)
-        w.writerow(["kernel", "metric", "value"])
+        w.writerow(["kernel", "metric", "value", "unit"])
         for r in rows[2:]:
             d = dict(zip(hdr, r))
             name = d.get("Kernel Name", "?").split("(")[0]
             for m in FULL_METRICS:
                 if m in d:
-                    w.writerow([name, m, d[m]])
+                    w.writerow([name, m, d[m], units.get(m, "")])
     print(open(out).read())
 
 
