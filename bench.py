@@ -107,15 +107,28 @@ def dist_info():
     return rank, world, local
 
 
-def max_over_ranks(x, world):
+DIST_BACKEND = os.environ.get("SHK_DIST_BACKEND", "nccl")  # gloo: functional runs of N ranks sharing one GPU
+
+
+def coll_device():
+    import torch
+
+    return torch.device("cuda", torch.cuda.current_device()) if DIST_BACKEND == "nccl" else torch.device("cpu")
+
+
+def reduce_over_ranks(x, world, op="max"):
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=coll_device())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def max_over_ranks(x, world):
+    return reduce_over_ranks(x, world, "max")
 
 
 def barrier(world):
@@ -207,8 +220,12 @@ def run_ours(args):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local if DIST_BACKEND == "nccl" else 0)
+        if DIST_BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            os.environ["SHK_DEVICE"] = "0"
+            dist.init_process_group(DIST_BACKEND)
     from paper_2308_09561_b200 import dist as shdist
     from paper_2308_09561_b200 import device as dev
     from paper_2308_09561_b200 import recsplit
@@ -228,8 +245,7 @@ def run_ours(args):
         if not sharded:
             d = recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"])
             return d, d.device_profile
-        d, prof = shdist.build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"],
-                                                     device=__import__("torch").device("cuda", local))
+        d, prof = shdist.build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"], device=coll_device())
         prof = dict(prof)
         prof["phase_ms"] = dict(zip(("bucketize", "split_search", "leaf_search", "rice", "ribbon"), prof["phase_ms"]))
         return d, prof
@@ -272,25 +288,43 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     value = N / (ms_step * 1e-3)
 
-    # e2e through the public API with host buffers (single process view)
-    e2e = None
-    if world == 1:
-        desc_bytes = 0
-        pinned = dev.PinnedBuffer.from_array(blob)  # the caller's key buffer, page-locked
-        dev.sync()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
+    # e2e through the public API with host buffers: the caller's pinned key
+    # blob in, serialized descriptor bytes out (rank 0); max wall over ranks
+    desc_bytes = 0
+    out = None
+    pinned = dev.PinnedBuffer.from_array(blob)  # the caller's key buffer, page-locked
+    dev.sync()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if sharded:
+            d2, _ = shdist.build_blob_sharded(pinned.array, 8, b, n, CFG["mode"], device=coll_device())
+        else:
             d2 = recsplit.build_blob(pinned.array, 8, b, n, CFG["mode"])
+        if d2 is not None:
             out = d2.serialize()
             desc_bytes = len(out)
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        e2e = {"value": round(N / e2e_s, 1), "unit": "keys/s", "h2d_bytes_per_step": int(blob.nbytes),
-               "d2h_bytes_per_step": int(desc_bytes), "ms_per_step": round(e2e_s * 1e3, 3),
-               "path": "recsplit.build_blob(pinned host 8-byte key blob) -> serialize(); "
-                       "H2D+blake2b+build+D2H timed"}
-        pinned.free()
-        if args.check:
-            parity["e2e_desc_matches_reference"] = hashlib.sha256(out).hexdigest() == parity.get("desc_sha256")
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps, world)
+    e2e = {"value": round(N / e2e_s, 1), "unit": "keys/s", "h2d_bytes_per_step": int(blob.nbytes) * world,
+           "d2h_bytes_per_step": int(desc_bytes), "ms_per_step": round(e2e_s * 1e3, 3),
+           "path": ("dist.build_blob_sharded" if sharded else "recsplit.build_blob")
+           + "(pinned host 8-byte key blob) -> serialize(); H2D+blake2b+build+D2H timed"
+           + (", max wall over ranks" if world > 1 else "")}
+    pinned.free()
+    if args.check and out is not None:
+        parity["e2e_desc_matches_reference"] = hashlib.sha256(out).hexdigest() == parity.get("desc_sha256")
+
+    # algorithmic work of the timed step summed over ranks (roofline)
+    hash_evals_local = prof.get("hash_evals")
+    if hash_evals_local is None and desc is not None and desc.build_stats:
+        hash_evals_local = desc.build_stats.get("hash_evals")
+    hash_evals_all = reduce_over_ranks(hash_evals_local or 0, world, "sum")
+    split_evals_all = reduce_over_ranks(split_evals_exact, world, "sum")
+    tree_ms_max = max_over_ranks(prof["phase_ms"]["split_search"] + prof["phase_ms"]["leaf_search"], world)
+    leaf_lines = {}
+    if args.leaf_configs:
+        for cfg in [int(x) for x in args.leaf_configs.split(",") if x]:
+            leaf_lines[f"C{cfg}"] = bench_leaf(cfg, args, dev, sms, None, rank, world)
 
     # queries (C4: 1e8 keys drawn from the set), device-resident
     query = None
@@ -300,8 +334,13 @@ def run_ours(args):
     if rank != 0:
         return
     prof = dict(profs[-1])
-    prof["split_evals"] = split_evals_exact
-    hash_evals = desc.build_stats.get("hash_evals") if desc.build_stats else None
+    # roofline inputs: work summed over ranks, the dominant kernel's time the
+    # max over ranks (at N = 1 these are the rank's own numbers)
+    prof["split_evals"] = split_evals_all
+    prof["phase_ms"] = dict(prof["phase_ms"])
+    if world > 1:
+        prof["phase_ms"]["split_search"], prof["phase_ms"]["leaf_search"] = tree_ms_max, 0.0
+    hash_evals = hash_evals_all if hash_evals_all else None
     clocks = clk.summary()
     line = {
         "metric": "keys/s MPHF build (ShockHash-RS, N=1e7, n=40, b=2000, rotate)",
@@ -328,14 +367,14 @@ def run_ours(args):
     }
     if e2e:
         line["e2e"] = e2e
-    if hash_evals is not None and world == 1:
-        line["roofline"] = roofline_numbers(prof, hash_evals, n, clocks.get("sm_mhz"), sms)
+    if hash_evals is not None:
+        line["roofline"] = roofline_numbers(prof, hash_evals, n, clocks.get("sm_mhz"), sms * world)
+        if world > 1:
+            line["roofline"]["peak_source"] += f" (all {world} GPUs)"
     if query:
         line["query"] = query
-    if world == 1 and args.leaf_configs:
-        line["leaf_search"] = {}
-        for cfg in [int(x) for x in args.leaf_configs.split(",") if x]:
-            line["leaf_search"][f"C{cfg}"] = bench_leaf(cfg, args, dev, sms, clocks.get("sm_mhz"))
+    if leaf_lines:
+        line["leaf_search"] = leaf_lines
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
@@ -380,19 +419,23 @@ def bench_queries(desc, k, args, dev, sms):
     return res
 
 
-def bench_leaf(cfg, args, dev, sms, clock_mhz):
-    """Leaf-search-only configs (BASELINE configs C1/C3/C5): leaf seeds tested/s."""
+def bench_leaf(cfg, args, dev, sms, clock_mhz, rank=0, world=1):
+    """Leaf-search-only configs (BASELINE configs C1/C3/C5): leaf seeds tested/s.
+    At N > 1 rank r searches the contiguous leaf range [L r/N, L (r+1)/N) (no
+    exchange); seeds tested are summed and the time is the max over ranks."""
     from paper_2308_09561_b200 import workloads as W
     from paper_2308_09561_b200._kernels import kernels as K
 
     spec = W.LEAF_CONFIGS[cfg]
-    L, n = spec["leaves"], spec["n"]
+    L_all, n = spec["leaves"], spec["n"]
+    l0, l1 = (L_all * rank) // world, (L_all * (rank + 1)) // world
+    L = l1 - l0
     if cfg == 5:
-        fp = np.random.default_rng(5).integers(0, 2**64, (L, n, 2), dtype=np.uint64)
+        fp = np.random.default_rng(5).integers(0, 2**64, (L_all, n, 2), dtype=np.uint64)[l0:l1]
         d_hi = dev.DeviceBuffer.from_host(np.ascontiguousarray(fp[..., 0]).ravel())
         d_lo = dev.DeviceBuffer.from_host(np.ascontiguousarray(fp[..., 1]).ravel())
     else:
-        k = W.raw_keys(cfg, L * n)
+        k = W.raw_keys(cfg, L_all * n)[l0 * n : l1 * n]
         d_blob = dev.DeviceBuffer.from_host(np.frombuffer(np.ascontiguousarray(k, dtype="<u8").tobytes(), np.uint8))
         d_hi = dev.DeviceBuffer(8 * L * n)
         d_lo = dev.DeviceBuffer(8 * L * n)
@@ -405,28 +448,31 @@ def bench_leaf(cfg, args, dev, sms, clock_mhz):
     if cfg != 5:
         run()  # warm-up
     dev.sync()
+    barrier(world)
     reps = 1 if cfg == 5 else max(1, args.leaf_reps)
     with dev.timer() as tm:
         for _ in range(reps):
             run()
-    ms = tm.ms / reps
+    ms = max_over_ranks(tm.ms / reps, world)
     seeds = d_seed.download(np.int64, L)
-    seeds_tested = float((seeds + 1).sum())
+    seeds_tested = reduce_over_ranks(float((seeds + 1).sum()), world, "sum")
     w_key = 50 if n <= 32 else 53
     ops = seeds_tested * (n * w_key + W_SEED)
-    peak = INT_OPS_PER_CLK_SM * sms * 1965e6 / 1e12
-    res = {"config": f"C{cfg}: {L} leaves x n={n}, plain", "seeds_tested": int(seeds_tested),
-           "mean_seeds_per_leaf": round(seeds_tested / L, 1), "ms": round(ms, 3),
+    peak = INT_OPS_PER_CLK_SM * sms * world * 1965e6 / 1e12
+    res = {"config": f"C{cfg}: {L_all} leaves x n={n}, plain" + (f", {world} GPUs x contiguous leaf ranges"
+                                                                  if world > 1 else ""),
+           "seeds_tested": int(seeds_tested),
+           "mean_seeds_per_leaf": round(seeds_tested / L_all, 1), "ms": round(ms, 3),
            "value": round(seeds_tested / (ms * 1e-3), 1), "unit": "leaf seeds tested/s",
            "roofline": {"bound": "int32-issue", "achieved": round(ops / (ms * 1e-3) / 1e12, 3),
                         "peak": round(peak, 2), "unit": "Tops/s", "frac": round(ops / (ms * 1e-3) / 1e12 / peak, 4),
                         "work": f"(seed+1) x (n x {w_key} + {W_SEED}) int32 ops"}}
     gpath = os.path.join(ROOT, "tests", "golden", f"c{cfg}.json")
-    if os.path.exists(gpath):
+    if os.path.exists(gpath) and rank == 0:
         g = json.load(open(gpath))
-        kk = len(g["seeds"])
-        res["parity"] = {"leaves_checked": kk, "seeds_match_reference": seeds[:kk].tolist() == g["seeds"],
-                         "fbits_match_reference": d_fb.download(np.uint64, kk).tolist() == g["fbits"]}
+        kk = min(len(g["seeds"]), L)  # the golden prefix inside rank 0's leaf range
+        res["parity"] = {"leaves_checked": kk, "seeds_match_reference": seeds[:kk].tolist() == g["seeds"][:kk],
+                         "fbits_match_reference": d_fb.download(np.uint64, kk).tolist() == g["fbits"][:kk]}
     for b_ in (d_hi, d_lo, d_off, d_seed, d_fb):
         b_.free()
     return res

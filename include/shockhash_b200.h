@@ -203,6 +203,16 @@ int shk_build_choice(shk_build* b, uint8_t* choice /* [N] host, sorted key order
  * key as placed at construction time; enable before shk_build_run. */
 int shk_build_set_record_placements(shk_build* b, int on);
 int shk_build_placements(shk_build* b, int64_t* out /* [N] host */);
+/* Sharded builds (dist.py): a rank builds only its bucket range, so only that
+ * range of its key array is permuted into leaf order.  With keep_sorted (set
+ * before shk_build_run) the bucket-sorted keys are kept, choice_sorted returns
+ * the choice bits of key positions [k0, k1) re-ordered to the sorted order,
+ * and shk_build_ribbon with choice_flags & SHK_RIBBON_SORTED_KEYS builds the
+ * ribbon rows from the sorted keys (choice given in sorted order).  The
+ * ribbon solution does not depend on row order. */
+#define SHK_RIBBON_SORTED_KEYS 4
+int shk_build_set_keep_sorted(shk_build* b, int on);
+int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out /* [k1-k0] host */);
 int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int64_t m, int max_tries,
                      uint64_t* seed_out, uint64_t* words_out /* [ceil(m/64)] host */);
 /* Device time of the last phases (CUDA events on the context stream), ms:

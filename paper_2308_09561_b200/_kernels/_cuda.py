@@ -534,12 +534,24 @@ class GpuBuild:
         check(_L().shk_build_choice(self.handle, ptr(out)))
         return out
 
-    def ribbon(self, m, max_tries=64, choice=None):
+    def keep_sorted(self, on=True):
+        """Keep the bucket-sorted keys (before run) for choice_sorted/ribbon(sorted_keys=True)."""
+        check(_L().shk_build_set_keep_sorted(self.handle, 1 if on else 0))
+
+    def choice_sorted(self, k0, k1):
+        """Choice bits of build positions [k0, k1) in bucket-sorted key order."""
+        out = np.zeros(max(int(k1) - int(k0), 0), dtype=np.uint8)
+        check(_L().shk_build_choice_sorted(self.handle, int(k0), int(k1), ptr(out) if len(out) else None),
+              "choice_sorted")
+        return out
+
+    def ribbon(self, m, max_tries=64, choice=None, sorted_keys=False):
         words = np.zeros((int(m) + 63) // 64, dtype=np.uint64)
         seed = ctypes.c_uint64(0)
         ch = None if choice is None else np.ascontiguousarray(choice, dtype=np.uint8)
-        check(_L().shk_build_ribbon(self.handle, ptr(ch), 0, int(m), int(max_tries), ctypes.byref(seed), ptr(words)),
-              "ribbon")
+        flags = 4 if sorted_keys else 0  # SHK_RIBBON_SORTED_KEYS
+        check(_L().shk_build_ribbon(self.handle, ptr(ch), flags, int(m), int(max_tries), ctypes.byref(seed),
+                                    ptr(words)), "ribbon")
         return int(seed.value), words
 
     def phase_ms(self):

@@ -131,9 +131,42 @@ __global__ void max_bucket_kernel(const int64_t* counts, int64_t nb, int64_t* ma
   atomicMax((unsigned long long*)maxv, (unsigned long long)m);
 }
 
+// Choice bits of the keys at positions [k0, k1) of the (partitioned) build
+// array, written at those keys' positions in the bucket-sorted array: the
+// bucket is recomputed from the key, then a binary search by (hi, lo) inside
+// it (codes are distinct).
+__global__ void choice_sorted_kernel(const ulonglong2* keys, const ulonglong2* sorted, const int64_t* prefix,
+                                     uint32_t nb, const uint8_t* choice, int64_t k0, int64_t k1, uint8_t* out) {
+  const u2 x = split64(seed_mixer(0, TAG_BUCKET));
+  for (int64_t i = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k1; i += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 k = keys[i];
+    const uint32_t bu = __umulhi(remix_d(split64(k.x), split64(k.y), x).hi, nb);
+    int64_t lo = prefix[bu], hi = prefix[bu + 1] - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (key_less(sorted[mid], k))
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    out[lo - k0] = choice[i];
+  }
+}
+
 }  // namespace shk
 
 using namespace shk;
+
+int shk_launch_choice_sorted(const uint64_t* keys, const uint64_t* sorted, const int64_t* prefix, int64_t nb,
+                             const uint8_t* choice, int64_t k0, int64_t k1, uint8_t* out, cudaStream_t st) {
+  if (k1 <= k0) return 0;
+  int64_t g = (k1 - k0 + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  choice_sorted_kernel<<<(unsigned)g, 256, 0, st>>>((const ulonglong2*)keys, (const ulonglong2*)sorted, prefix,
+                                                    (uint32_t)nb, choice, k0, k1, out);
+  SHK_LAUNCHED();
+  return 0;
+}
 
 size_t shk_bucketize_scratch(int64_t N, int64_t nb) {
   size_t s = 0;

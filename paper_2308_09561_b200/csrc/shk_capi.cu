@@ -881,13 +881,17 @@ struct shk_build {
   bool ran = false;
   bool record = false;
   DBuf place;
+  // bucket-sorted copy of the keys (kept when a sharded build asks for it:
+  // run() permutes `keys` in place only inside the rank's bucket range)
+  bool keep_sorted = false;
+  DBuf sorted;
   // phase timing (CUDA events on the context stream): 0 bucketize, 1 splits,
   // 2 leaves, 3 rice, 4 ribbon (last run)
   cudaEvent_t ev[12] = {};
   float phase_ms[6] = {0, 0, 0, 0, 0, 0};
   int64_t split_evals = 0;
   explicit shk_build(shk_ctx* ctx)
-      : c(ctx), keys(ctx), tmp(ctx), prefix(ctx), choice(ctx), words(ctx), place(ctx) {}
+      : c(ctx), keys(ctx), tmp(ctx), prefix(ctx), choice(ctx), words(ctx), place(ctx), sorted(ctx) {}
   ~shk_build() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -1135,6 +1139,10 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     RC(h2d(c, dloff.p, leaf_off.data(), (size_t)(L + 1) * 8));
     RC(h2d(c, dlslot.p, leaf_slot.data(), (size_t)L * 8));
   }
+  if (b->keep_sorted && !b->sorted.p) {
+    RC(b->sorted.alloc((size_t)b->N * 16));
+    SHK_CUDA(cudaMemcpyAsync(b->sorted.p, b->keys.p, (size_t)b->N * 16, cudaMemcpyDeviceToDevice, c->stream));
+  }
   b->mark(2);
   b->level_reset();
   // the seed searches take pre-mixed key high words (shk_hash.cuh premix_hi);
@@ -1333,6 +1341,30 @@ int shk_build_set_record_placements(shk_build* b, int on) {
   return 0;
 }
 
+int shk_build_set_keep_sorted(shk_build* b, int on) {
+  b->keep_sorted = on != 0;
+  return 0;
+}
+
+int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out) {
+  shk_ctx* c = b->c;
+  if (!b->sorted.p || !b->ran) {
+    shk_set_error("choice_sorted needs shk_build_set_keep_sorted before shk_build_run");
+    return SHK_INVALID;
+  }
+  if (k0 < 0 || k1 > b->N || k0 > k1) {
+    shk_set_error("bad key range");
+    return SHK_INVALID;
+  }
+  if (k1 == k0) return 0;
+  DBuf d(c);
+  RC(d.alloc((size_t)(k1 - k0)));
+  RC(shk_launch_choice_sorted(b->keys.as<uint64_t>(), b->sorted.as<uint64_t>(), b->prefix.as<int64_t>(), b->nb,
+                              b->choice.as<uint8_t>(), k0, k1, d.as<uint8_t>(), c->stream));
+  RC(d2h(c, out, d.p, (size_t)(k1 - k0)));
+  return csync(c);
+}
+
 int shk_build_placements(shk_build* b, int64_t* out) {
   if (!b->ran || !b->record) {
     shk_set_error("placements were not recorded");
@@ -1364,8 +1396,18 @@ int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int6
   const int64_t nw = (m + 63) / 64;
   DBuf tw(c);
   RC(tw.alloc((size_t)nw * 8));
+  // SHK_RIBBON_SORTED_KEYS: rows from the bucket-sorted copy (choice given in
+  // that order), as a sharded build's rank 0 does
+  const uint64_t* rkeys = b->keys.as<uint64_t>();
+  if (choice_flags & 4) {
+    if (!b->sorted.p) {
+      shk_set_error("sorted keys were not kept (shk_build_set_keep_sorted)");
+      return SHK_INVALID;
+    }
+    rkeys = b->sorted.as<uint64_t>();
+  }
   b->mark(6);
-  RC(ribbon_seed_loop(c, b->keys.as<uint64_t>(), drhs, b->N, m, max_tries, seed_out, tw.as<uint64_t>()));
+  RC(ribbon_seed_loop(c, rkeys, drhs, b->N, m, max_tries, seed_out, tw.as<uint64_t>()));
   b->mark(7);
   RC(d2h(c, words_out, tw.p, (size_t)nw * 8));
   RC(csync(c));

@@ -108,6 +108,11 @@ struct ShkTreeLaunch {
 };
 int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st);
 
+// Choice bits of build positions [k0, k1) moved to the keys' bucket-sorted
+// positions (out[j - k0]); keys/sorted are interleaved pairs.
+int shk_launch_choice_sorted(const uint64_t* keys, const uint64_t* sorted, const int64_t* prefix, int64_t nb,
+                             const uint8_t* choice, int64_t k0, int64_t k1, uint8_t* out, cudaStream_t st);
+
 // Bucketing.
 // skeys: interleaved (hi, lo) pairs [2N], sorted by (bucket, hi, lo).
 int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nbuckets, uint64_t* skeys,

@@ -125,18 +125,42 @@ def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8,
     sizes = np.unique(np.diff(key_prefix[b0 : b1 + 1].astype(np.int64)))
     plans = recsplit.plans_for_sizes(sizes, n, leaf_g)
     ck = cache_k if mode == leaf_mod.MODE_ROTATE_CACHED else 0
-    gb.run(plans, 0 if mode == leaf_mod.MODE_PLAIN else 1, ck, leaf_mod.CACHE_MIN_LEAF, b0, b1, leaf_mod.MAX_SEED)
+    # Only this rank's bucket range gets permuted into leaf order, so choice
+    # bits travel in the (rank-independent) bucket-sorted key order and rank
+    # 0 builds the ribbon rows from its sorted copy of the keys.
+    gb.keep_sorted(True)
+    st = gb.run(plans, 0 if mode == leaf_mod.MODE_PLAIN else 1, ck, leaf_mod.CACHE_MIN_LEAF, b0, b1,
+                leaf_mod.MAX_SEED)
     words, bit_len, bo = gb.stream()
     rel = bo[: b1 - b0 + 1]
-    choice = gb.choice()[int(key_prefix[b0]) : int(key_prefix[b1])]
+    choice = gb.choice_sorted(int(key_prefix[b0]), int(key_prefix[b1]))
     sw, bl, bit_offsets, choice_all = exchange_and_merge(words, bit_len, rel, choice, device)
     desc = None
     if rank == 0:
         m = retrieval._columns(n_keys, epsilon)
-        rseed, rwords = gb.ribbon(m, retrieval.RETRY_CAP, choice=choice_all)
+        rseed, rwords = gb.ribbon(m, retrieval.RETRY_CAP, choice=choice_all, sorted_keys=True)
         ribbon = retrieval.RibbonSystem(epsilon, rseed, m, rwords)
         desc = recsplit.MphfDescriptor(n_keys, b, n, mode, cache_k, 0, leaf_g, key_prefix, bit_offsets, sw, bl, ribbon)
         desc.build_stats = {"build_seconds": time.perf_counter() - t0}
     phase, split_evals = gb.phase_ms()
     gb.close()
-    return desc, {"phase_ms": phase, "split_evals": split_evals, "buckets": (b0, b1)}
+    return desc, {"phase_ms": phase, "split_evals": split_evals, "buckets": (b0, b1),
+                  "hash_evals": int(st[0]), "filter_passes": int(st[1]), "leaf_count": int(st[6])}
+
+
+def build_blob_sharded(blob, key_len, b, n, mode=1, cache_k=8, epsilon=0.05, device=None):
+    """recsplit.build_blob over the process group: every rank fingerprints the
+    host key blob (H2D pipelined with blake2b) and builds its bucket range;
+    rank 0 returns the descriptor (salt 0; a duplicate code raises)."""
+    from . import device as dev
+
+    blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    n_keys = len(blob) // key_len
+    d_hi = dev.DeviceBuffer(8 * n_keys)
+    d_lo = dev.DeviceBuffer(8 * n_keys)
+    try:
+        dev.blake2b_fixed_from_host(blob, key_len, n_keys, 0, d_hi, d_lo)
+        return build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, n_keys, b, n, mode, cache_k, epsilon, device)
+    finally:
+        d_hi.free()
+        d_lo.free()
