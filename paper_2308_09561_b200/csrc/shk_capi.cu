@@ -1541,7 +1541,7 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
   d.key_prefix = q->kp.as<uint64_t>();
   d.bucket_plan = q->bplan.as<int32_t>();
   d.node_base = q->nbase.as<int64_t>();
-  d.node_pos = q->npos.as<int64_t>();
+  d.node_val = q->npos.as<uint64_t>();
   d.bucket_bad = q->bbad.as<int32_t>();
   d.bit_offsets = q->bo.as<uint64_t>();
   d.stream = q->sw.as<uint64_t>();
@@ -1558,7 +1558,7 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
   d.rib_m = rib_m;
   d.rib_words = q->rw.as<uint64_t>();
   d.rib_nwords = rnw;
-  RC(shk_launch_node_index(d, q->npos.as<int64_t>(), q->bbad.as<int32_t>(), c->stream));
+  RC(shk_launch_node_index(d, q->npos.as<uint64_t>(), q->bbad.as<int32_t>(), c->stream));
   RC(csync(c));
   *out = guard.release();
   return 0;

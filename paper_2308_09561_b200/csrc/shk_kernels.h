@@ -166,7 +166,7 @@ struct ShkQueryDesc {
   const uint64_t* key_prefix;   // [nb+1]
   const int32_t* bucket_plan;   // [nb]  plan id (or -1 for empty)
   const int64_t* node_base;     // [nb]  first global node of the bucket
-  const int64_t* node_pos;      // [total nodes] bit position of each node's code
+  const uint64_t* node_val;     // [total nodes] decoded node: split -> premixed seed mixer, leaf -> seed
   const int32_t* bucket_bad;    // [nb]  first node whose decode overran (INT32_MAX none)
   const uint64_t* bit_offsets;  // [nb+1] stream bit offset of each bucket
   const uint64_t* stream;       // words
@@ -184,7 +184,7 @@ struct ShkQueryDesc {
   const uint64_t* rib_words;
   int64_t rib_nwords;
 };
-int shk_launch_node_index(const ShkQueryDesc& d, int64_t* node_pos, int32_t* bucket_bad, cudaStream_t st);
+int shk_launch_node_index(const ShkQueryDesc& d, uint64_t* node_val, int32_t* bucket_bad, cudaStream_t st);
 int shk_launch_query(const ShkQueryDesc& d, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out,
                      int* err, int clamp, cudaStream_t st);
 // Bijection check of Q values against [0, N): *offender = first index whose

@@ -4,9 +4,10 @@
 // recsplit.py:251-275 (clamp to N-1).  The reference walks the preorder plan
 // of the key's bucket and Rice-decodes EVERY node before the key's leaf (the
 // seeds of skipped left subtrees included, ~38 decodes per query at n=40,
-// b=2000).  Here a derived per-node bit-position index is built once per
-// descriptor (one thread per bucket decodes the bucket's nodes in order), so a
-// query decodes only the split nodes on its root-to-leaf path plus its leaf.
+// b=2000).  Here the whole stream is decoded ONCE per descriptor (one thread
+// per bucket decodes the bucket's nodes in order) into a per-node value table
+// (split node: its seed's pre-mixed TAG_SPLIT mixer; leaf: its seed), so a
+// query decodes nothing: it reads the values on its root-to-leaf path.
 // Outputs are identical; so are the FormatError cases: a query fails iff the
 // reference's sequential decode would overrun before reaching the key's leaf,
 // i.e. iff the first undecodable node of its bucket has preorder index <= the
@@ -17,7 +18,7 @@
 
 namespace shk {
 
-__global__ void node_index_kernel(ShkQueryDesc d, int64_t* node_pos, int32_t* bucket_bad) {
+__global__ void node_index_kernel(ShkQueryDesc d, uint64_t* node_val, int32_t* bucket_bad) {
   for (int64_t bu = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bu < d.nbuckets;
        bu += (int64_t)gridDim.x * blockDim.x) {
     const int32_t plan = d.bucket_plan[bu];
@@ -27,25 +28,31 @@ __global__ void node_index_kernel(ShkQueryDesc d, int64_t* node_pos, int32_t* bu
       const int64_t nb = d.node_base[bu];
       int64_t pos = (int64_t)d.bit_offsets[bu];
       for (int64_t j = 0; j < p1 - p0; ++j) {
-        node_pos[nb + j] = pos;
         int64_t v;
         if (rice_decode(d.stream, d.stream_bit_len, &pos, d.pn_g[p0 + j], &v)) {
           bad = (int32_t)j;
           break;
         }
+        node_val[nb + j] =
+            d.pn_kind[p0 + j] == 0 ? premix_hi(seed_mixer((uint64_t)v, TAG_SPLIT)) : (uint64_t)v;
       }
     }
     bucket_bad[bu] = bad;
   }
 }
 
-SHK_D uint64_t rib_choice(const ShkQueryDesc& d, u2 kh, u2 kl) {
+// Pre-mixed per-descriptor mixers of the query (constant over a launch).
+struct QueryMixers {
+  u2 bucket, rstart, rpat0, rpat1;
+};
+
+SHK_D uint64_t rib_choice(const ShkQueryDesc& d, const QueryMixers& mx, u2 kp, u2 kl) {
   if (!d.rib_m) return 0;
   const uint64_t span = (uint64_t)(d.rib_m - RIBBON_W + 1);
-  const u2 vs = remix_d(kh, kl, split64(seed_mixer(d.rib_seed, TAG_RSTART)));
+  const u2 vs = remix_pre_d(kp, kl, mx.rstart);
   const int64_t s = (int64_t)(((uint64_t)vs.hi * span) >> 32);
-  const u2 a = remix_d(kh, kl, split64(seed_mixer(d.rib_seed, TAG_RPAT0)));
-  const u2 b = remix_d(kh, kl, split64(seed_mixer(d.rib_seed, TAG_RPAT1)));
+  const u2 a = remix_pre_d(kp, kl, mx.rpat0);
+  const u2 b = remix_pre_d(kp, kl, mx.rpat1);
   const uint64_t pat0 = join64(a.lo | 1u, a.hi), pat1 = join64(b.lo, b.hi);
   const int64_t wi = s >> 6;
   const int sh = (int)(s & 63);
@@ -64,12 +71,44 @@ SHK_D uint64_t rib_choice(const ShkQueryDesc& d, u2 kh, u2 kl) {
   return (uint64_t)((__popcll(v0 & pat0) + __popcll(v1 & pat1)) & 1);
 }
 
+// Cell of a key inside its leaf (leaf_cell, _core.pyx:751-767) from the
+// pre-mixed key and the leaf's encoded seed q.
+SHK_D uint32_t leaf_cell_pre(u2 kp, u2 kl, uint64_t q, uint32_t n, int mode, int64_t cache_k, int choice) {
+  if (n <= 1) return 0;  // leaf_pair gives (0, 0)
+  uint32_t h0, h1;
+  if (mode == 0) {
+    leaf_pair_d(remix_pre_d(kp, kl, seed_mixer_pre_d(q, TAG_LEAF)), n, n - 1, h0, h1);
+    return choice ? h1 : h0;
+  }
+  uint64_t base, r;
+  if (q >> 32) {
+    base = q / n;
+    r = q - base * n;
+  } else {
+    const uint32_t b32 = (uint32_t)q / n;
+    base = b32;
+    r = (uint32_t)q - b32 * n;
+  }
+  const uint64_t sa = (mode == 2 && cache_k && n > 32) ? base - base % (uint64_t)cache_k : base;
+  if (remix_top_pre_d(kp, kl, seed_mixer_pre_d(sa, TAG_SPLITBIT)) == 0) {
+    leaf_pair_d(remix_pre_d(kp, kl, seed_mixer_pre_d(sa, TAG_LEAF)), n, n - 1, h0, h1);
+    return choice ? h1 : h0;
+  }
+  leaf_pair_d(remix_pre_d(kp, kl, seed_mixer_pre_d(base, TAG_LEAF)), n, n - 1, h0, h1);
+  uint32_t h = (choice ? h1 : h0) + (uint32_t)r;  // < 2n
+  return h >= n ? h - n : h;
+}
+
 __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64_t* hi, const uint64_t* lo, int64_t Q,
                                                     uint64_t* out, int* err, int clamp) {
-  const u2 xb = split64(seed_mixer(0, TAG_BUCKET));
+  QueryMixers mx;
+  mx.bucket = seed_mixer_pre_d(0, TAG_BUCKET);
+  mx.rstart = seed_mixer_pre_d(d.rib_seed, TAG_RSTART);
+  mx.rpat0 = seed_mixer_pre_d(d.rib_seed, TAG_RPAT0);
+  mx.rpat1 = seed_mixer_pre_d(d.rib_seed, TAG_RPAT1);
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (int64_t)gridDim.x * blockDim.x) {
-    const u2 kh = split64(hi[t]), kl = split64(lo[t]);
-    const u2 vb = remix_d(kh, kl, xb);
+    const u2 kp = split64(premix_hi(hi[t])), kl = split64(lo[t]);
+    const u2 vb = remix_pre_d(kp, kl, mx.bucket);
     const int64_t bucket = (int64_t)__umulhi(vb.hi, (uint32_t)d.nbuckets);
     const uint64_t kp0 = d.key_prefix[bucket];
     const int64_t msize = (int64_t)(d.key_prefix[bucket + 1] - kp0);
@@ -86,9 +125,7 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
           fail = true;
           break;
         }
-        int64_t pos = d.node_pos[nbase + idx], seed;
-        rice_decode(d.stream, d.stream_bit_len, &pos, d.pn_g[pb + idx], &seed);
-        const u2 v = remix_d(kh, kl, split64(seed_mixer((uint64_t)seed, TAG_SPLIT)));
+        const u2 v = remix_pre_d(kp, kl, split64(d.node_val[nbase + idx]));
         const uint32_t r = __umulhi(v.hi, (uint32_t)d.pn_m[pb + idx]);
         const int32_t* sz = d.pn_sizes + 4 * (pb + idx);
         const int fan = d.pn_fanout[pb + idx];
@@ -106,12 +143,10 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
         out[t] = 0;
         continue;
       }
-      int64_t pos = d.node_pos[nbase + idx], q;
-      rice_decode(d.stream, d.stream_bit_len, &pos, d.pn_g[pb + idx], &q);
-      const int mleaf = d.pn_m[pb + idx];
-      const int choice = (int)rib_choice(d, kh, kl);
-      const int cell = leaf_cell(hi[t], lo[t], q, mleaf, d.mode, d.cache_k, choice);
-      offset += (uint64_t)cell;
+      const uint64_t q = d.node_val[nbase + idx];
+      const uint32_t mleaf = (uint32_t)d.pn_m[pb + idx];
+      const int choice = (int)rib_choice(d, mx, kp, kl);
+      offset += leaf_cell_pre(kp, kl, q, mleaf, d.mode, d.cache_k, choice);
     }
     uint64_t o = kp0 + offset;
     if (clamp) {
@@ -144,10 +179,10 @@ __global__ void offender_kernel(const uint64_t* v, int64_t Q, int64_t N, const u
 
 using namespace shk;
 
-int shk_launch_node_index(const ShkQueryDesc& d, int64_t* node_pos, int32_t* bucket_bad, cudaStream_t st) {
+int shk_launch_node_index(const ShkQueryDesc& d, uint64_t* node_val, int32_t* bucket_bad, cudaStream_t st) {
   if (d.nbuckets <= 0) return 0;
   int64_t g = (d.nbuckets + 127) / 128;
-  node_index_kernel<<<(unsigned)g, 128, 0, st>>>(d, node_pos, bucket_bad);
+  node_index_kernel<<<(unsigned)g, 128, 0, st>>>(d, node_val, bucket_bad);
   SHK_LAUNCHED();
   return 0;
 }
