@@ -1445,11 +1445,11 @@ int shk_build_destroy(shk_build* b) {
 struct shk_qdesc {
   shk_ctx* c;
   ShkQueryDesc d{};
-  DBuf kp, bo, sw, rw, bplan, nbase, npos, bbad, kind, g, mm, child, sizes, fan, poff;
+  DBuf kp, bo, sw, rw, bplan, nbase, npos, bbad, kind, g, mm, child, sizes, fan, poff, planq, bucketq;
   int64_t nnodes = 0;
   explicit shk_qdesc(shk_ctx* ctx)
       : c(ctx), kp(ctx), bo(ctx), sw(ctx), rw(ctx), bplan(ctx), nbase(ctx), npos(ctx), bbad(ctx), kind(ctx), g(ctx),
-        mm(ctx), child(ctx), sizes(ctx), fan(ctx), poff(ctx) {}
+        mm(ctx), child(ctx), sizes(ctx), fan(ctx), poff(ctx), planq(ctx), bucketq(ctx) {}
 };
 
 extern "C" {
@@ -1492,6 +1492,7 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
   q->nnodes = nn;
   const size_t np = S.nodes.size();
   std::vector<int32_t> kind(np), g(np), mm(np), child(np * 4), sizes(np * 4), fan(np);
+  std::vector<uint32_t> planq(np * 8, 0u);
   for (size_t j = 0; j < np; ++j) {
     kind[j] = S.nodes[j].kind;
     g[j] = S.nodes[j].g;
@@ -1501,6 +1502,26 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
       child[4 * j + k] = S.nodes[j].child[k];
       sizes[4 * j + k] = S.nodes[j].sizes[k];
     }
+    // packed 16-bit fields (m < 32768, plan-local child ids < 65536)
+    auto u16 = [](int32_t v) { return (uint32_t)v & 0xFFFFu; };
+    uint32_t* e = &planq[8 * j];
+    e[0] = ((uint32_t)kind[j] & 0xFFu) | (((uint32_t)fan[j] & 0xFFu) << 8) | (u16(mm[j]) << 16);
+    e[1] = u16(sizes[4 * j]) | (u16(sizes[4 * j + 1]) << 16);
+    e[2] = u16(sizes[4 * j + 2]) | (u16(child[4 * j]) << 16);
+    e[3] = u16(child[4 * j + 1]) | (u16(child[4 * j + 2]) << 16);
+    e[4] = u16(child[4 * j + 3]);
+  }
+  std::vector<uint32_t> bucketq((size_t)nbuckets * 8, 0u);
+  for (int64_t bu = 0; bu < nbuckets; ++bu) {
+    uint32_t* e = &bucketq[8 * bu];
+    const uint64_t kp0 = key_prefix[bu];
+    e[0] = (uint32_t)kp0;
+    e[1] = (uint32_t)(kp0 >> 32);
+    e[2] = (uint32_t)(key_prefix[bu + 1] - kp0);
+    e[3] = 0x7FFFFFFFu;  // first bad node, set on the device by node_index_kernel
+    e[4] = (uint32_t)nbase[bu];
+    e[5] = (uint32_t)((uint64_t)nbase[bu] >> 32);
+    e[6] = bplan[bu] >= 0 ? (uint32_t)S.plan_off[bplan[bu]] : 0u;
   }
   const int64_t rnw = rib_nwords > 0 ? rib_nwords : 0;
   RC(q->kp.alloc((size_t)(nbuckets + 1) * 8));
@@ -1518,6 +1539,10 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
   RC(q->sizes.alloc(np * 16 + 16));
   RC(q->fan.alloc(np * 4 + 4));
   RC(q->poff.alloc(S.plan_off.size() * 8 + 8));
+  RC(q->planq.alloc(np * 32 + 32));
+  RC(q->bucketq.alloc((size_t)nbuckets * 32 + 32));
+  RC(h2d(c, q->planq.p, planq.data(), np * 32));
+  RC(h2d(c, q->bucketq.p, bucketq.data(), (size_t)nbuckets * 32));
   RC(h2d(c, q->kp.p, key_prefix, (size_t)(nbuckets + 1) * 8));
   RC(h2d(c, q->bo.p, bit_offsets, (size_t)(nbuckets + 1) * 8));
   SHK_CUDA(cudaMemsetAsync(q->sw.p, 0, (size_t)(stream_nwords + 1) * 8, c->stream));
@@ -1542,6 +1567,8 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
   d.bucket_plan = q->bplan.as<int32_t>();
   d.node_base = q->nbase.as<int64_t>();
   d.node_val = q->npos.as<uint64_t>();
+  d.planq = q->planq.as<uint4>();
+  d.bucketq = q->bucketq.as<uint4>();
   d.bucket_bad = q->bbad.as<int32_t>();
   d.bit_offsets = q->bo.as<uint64_t>();
   d.stream = q->sw.as<uint64_t>();

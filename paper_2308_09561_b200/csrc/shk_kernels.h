@@ -167,6 +167,11 @@ struct ShkQueryDesc {
   const int32_t* bucket_plan;   // [nb]  plan id (or -1 for empty)
   const int64_t* node_base;     // [nb]  first global node of the bucket
   const uint64_t* node_val;     // [total nodes] decoded node: split -> premixed seed mixer, leaf -> seed
+  // query-side packed tables (2 x uint4 per entry, one 32 B sector):
+  //   bucketq[b]: {kp0 lo, kp0 hi, msize, bad} {node_base lo, node_base hi, plan first node, 0}
+  //   planq[j]:   {kind | fanout << 8 | m << 16, s0 | s1 << 16, s2 | c0 << 16, c1 | c2 << 16} {c3, 0, 0, 0}
+  const uint4* bucketq;
+  const uint4* planq;
   const int32_t* bucket_bad;    // [nb]  first node whose decode overran (INT32_MAX none)
   const uint64_t* bit_offsets;  // [nb+1] stream bit offset of each bucket
   const uint64_t* stream;       // words

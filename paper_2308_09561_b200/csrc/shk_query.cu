@@ -38,6 +38,7 @@ __global__ void node_index_kernel(ShkQueryDesc d, uint64_t* node_val, int32_t* b
       }
     }
     bucket_bad[bu] = bad;
+    reinterpret_cast<uint32_t*>(const_cast<uint4*>(d.bucketq))[8 * bu + 3] = (uint32_t)bad;
   }
 }
 
@@ -110,41 +111,44 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
     const u2 kp = split64(premix_hi(hi[t])), kl = split64(lo[t]);
     const u2 vb = remix_pre_d(kp, kl, mx.bucket);
     const int64_t bucket = (int64_t)__umulhi(vb.hi, (uint32_t)d.nbuckets);
-    const uint64_t kp0 = d.key_prefix[bucket];
-    const int64_t msize = (int64_t)(d.key_prefix[bucket + 1] - kp0);
+    const uint4 b0 = __ldg(d.bucketq + 2 * bucket), b1 = __ldg(d.bucketq + 2 * bucket + 1);
+    const uint64_t kp0 = join64(b0.x, b0.y);
     uint64_t offset = 0;
-    if (msize > 0) {
-      const int32_t plan = d.bucket_plan[bucket];
-      const int64_t pb = d.plan_off[plan];
-      const int64_t nbase = d.node_base[bucket];
-      const int32_t bad = d.bucket_bad[bucket];
+    if (b0.z > 0) {  // msize
+      const int bad = (int)b0.w;
+      const uint64_t* nv = d.node_val + join64(b1.x, b1.y);
+      const uint4* pq = d.planq + 2 * (uint64_t)b1.z;
       int idx = 0;
-      bool fail = false;
-      while (d.pn_kind[pb + idx] == 0) {
-        if (idx >= bad) {
-          fail = true;
-          break;
-        }
-        const u2 v = remix_pre_d(kp, kl, split64(d.node_val[nbase + idx]));
-        const uint32_t r = __umulhi(v.hi, (uint32_t)d.pn_m[pb + idx]);
-        const int32_t* sz = d.pn_sizes + 4 * (pb + idx);
-        const int fan = d.pn_fanout[pb + idx];
-        uint32_t acc = 0;
-        int part = 0;
-        for (; part < fan - 1; ++part) {
-          if (r < acc + (uint32_t)sz[part]) break;
-          acc += (uint32_t)sz[part];
-        }
-        offset += acc;
-        idx = d.pn_child[4 * (pb + idx) + part];
+      uint4 p = __ldg(pq);
+      while ((p.x & 0xFFu) == 0) {  // split node
+        if (idx >= bad) break;
+        const u2 v = remix_pre_d(kp, kl, split64(__ldg(nv + idx)));
+        const uint32_t r = __umulhi(v.hi, p.x >> 16);
+        const uint32_t fan = (p.x >> 8) & 0xFFu;
+        const uint32_t s0 = p.y & 0xFFFFu, s1 = p.y >> 16, s2 = p.z & 0xFFFFu;
+        // part = number of cumulative bounds <= r among the first fan-1
+        const uint32_t c1 = s0, c2 = s0 + s1, c3 = c2 + s2;
+        const uint32_t part = (uint32_t)(r >= c1) + (uint32_t)(fan > 2 && r >= c2) + (uint32_t)(fan > 3 && r >= c3);
+        offset += part == 0 ? 0u : part == 1 ? c1 : part == 2 ? c2 : c3;
+        uint32_t child;
+        if (part == 0)
+          child = p.z >> 16;
+        else if (part == 1)
+          child = p.w & 0xFFFFu;
+        else if (part == 2)
+          child = p.w >> 16;
+        else
+          child = __ldg(pq + 2 * idx + 1).x;
+        idx = (int)child;
+        p = __ldg(pq + 2 * idx);
       }
-      if (fail || idx >= bad) {
+      if (idx >= bad) {
         atomicOr(err, 1);
         out[t] = 0;
         continue;
       }
-      const uint64_t q = d.node_val[nbase + idx];
-      const uint32_t mleaf = (uint32_t)d.pn_m[pb + idx];
+      const uint64_t q = __ldg(nv + idx);
+      const uint32_t mleaf = p.x >> 16;
       const int choice = (int)rib_choice(d, mx, kp, kl);
       offset += leaf_cell_pre(kp, kl, q, mleaf, d.mode, d.cache_k, choice);
     }
