@@ -1492,7 +1492,7 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
   q->nnodes = nn;
   const size_t np = S.nodes.size();
   std::vector<int32_t> kind(np), g(np), mm(np), child(np * 4), sizes(np * 4), fan(np);
-  std::vector<uint32_t> planq(np * 8, 0u);
+  std::vector<uint32_t> planq(np * 4, 0u);
   for (size_t j = 0; j < np; ++j) {
     kind[j] = S.nodes[j].kind;
     g[j] = S.nodes[j].g;
@@ -1502,14 +1502,25 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
       child[4 * j + k] = S.nodes[j].child[k];
       sizes[4 * j + k] = S.nodes[j].sizes[k];
     }
-    // packed 16-bit fields (m < 32768, plan-local child ids < 65536)
+    // one uint4 of 16-bit fields (m < 32768, plan-local child ids < 65536):
+    // {m | leaf << 15 | b1 << 16, b2 | b3 << 16, c0 | c1 << 16, c2 | c3 << 16}
+    // with b_k the cumulative part bounds (0xFFFF past the fanout: r < m
+    // never reaches them), so part = #(b_k <= r), the offset is lane `part`
+    // of (0, b1, b2, b3) and the child is lane `part` of (c0, c1, c2, c3)
     auto u16 = [](int32_t v) { return (uint32_t)v & 0xFFFFu; };
-    uint32_t* e = &planq[8 * j];
-    e[0] = ((uint32_t)kind[j] & 0xFFu) | (((uint32_t)fan[j] & 0xFFu) << 8) | (u16(mm[j]) << 16);
-    e[1] = u16(sizes[4 * j]) | (u16(sizes[4 * j + 1]) << 16);
-    e[2] = u16(sizes[4 * j + 2]) | (u16(child[4 * j]) << 16);
-    e[3] = u16(child[4 * j + 1]) | (u16(child[4 * j + 2]) << 16);
-    e[4] = u16(child[4 * j + 3]);
+    uint32_t bnd[4] = {0, 0xFFFFu, 0xFFFFu, 0xFFFFu};
+    if (kind[j] == 0) {
+      uint32_t acc = 0;
+      for (int k = 1; k < fan[j]; ++k) {
+        acc += (uint32_t)sizes[4 * j + k - 1];
+        bnd[k] = acc;
+      }
+    }
+    uint32_t* e = &planq[4 * j];
+    e[0] = u16(mm[j]) | ((kind[j] != 0 ? 1u : 0u) << 15) | (bnd[1] << 16);
+    e[1] = bnd[2] | (bnd[3] << 16);
+    e[2] = u16(child[4 * j]) | (u16(child[4 * j + 1]) << 16);
+    e[3] = u16(child[4 * j + 2]) | (u16(child[4 * j + 3]) << 16);
   }
   std::vector<uint32_t> bucketq((size_t)nbuckets * 8, 0u);
   for (int64_t bu = 0; bu < nbuckets; ++bu) {
@@ -1539,9 +1550,9 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
   RC(q->sizes.alloc(np * 16 + 16));
   RC(q->fan.alloc(np * 4 + 4));
   RC(q->poff.alloc(S.plan_off.size() * 8 + 8));
-  RC(q->planq.alloc(np * 32 + 32));
+  RC(q->planq.alloc(np * 16 + 16));
   RC(q->bucketq.alloc((size_t)nbuckets * 32 + 32));
-  RC(h2d(c, q->planq.p, planq.data(), np * 32));
+  RC(h2d(c, q->planq.p, planq.data(), np * 16));
   RC(h2d(c, q->bucketq.p, bucketq.data(), (size_t)nbuckets * 32));
   RC(h2d(c, q->kp.p, key_prefix, (size_t)(nbuckets + 1) * 8));
   RC(h2d(c, q->bo.p, bit_offsets, (size_t)(nbuckets + 1) * 8));

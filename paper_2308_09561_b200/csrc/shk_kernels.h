@@ -167,9 +167,10 @@ struct ShkQueryDesc {
   const int32_t* bucket_plan;   // [nb]  plan id (or -1 for empty)
   const int64_t* node_base;     // [nb]  first global node of the bucket
   const uint64_t* node_val;     // [total nodes] decoded node: split -> premixed seed mixer, leaf -> seed
-  // query-side packed tables (2 x uint4 per entry, one 32 B sector):
-  //   bucketq[b]: {kp0 lo, kp0 hi, msize, bad} {node_base lo, node_base hi, plan first node, 0}
-  //   planq[j]:   {kind | fanout << 8 | m << 16, s0 | s1 << 16, s2 | c0 << 16, c1 | c2 << 16} {c3, 0, 0, 0}
+  // query-side packed tables:
+  //   bucketq[2b..2b+1]: {kp0 lo, kp0 hi, msize, bad} {node_base lo, node_base hi, plan first node, 0}
+  //   planq[j]: {m | leaf << 15 | b1 << 16, b2 | b3 << 16, c0 | c1 << 16, c2 | c3 << 16}
+  //             (b_k cumulative part bounds, 0xFFFF past the fanout; c_k plan-local children)
   const uint4* bucketq;
   const uint4* planq;
   const int32_t* bucket_bad;    // [nb]  first node whose decode overran (INT32_MAX none)

@@ -117,30 +117,18 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
     if (b0.z > 0) {  // msize
       const int bad = (int)b0.w;
       const uint64_t* nv = d.node_val + join64(b1.x, b1.y);
-      const uint4* pq = d.planq + 2 * (uint64_t)b1.z;
+      const uint4* pq = d.planq + b1.z;
       int idx = 0;
       uint4 p = __ldg(pq);
-      while ((p.x & 0xFFu) == 0) {  // split node
+      while (!(p.x & 0x8000u)) {  // split node
         if (idx >= bad) break;
         const u2 v = remix_pre_d(kp, kl, split64(__ldg(nv + idx)));
-        const uint32_t r = __umulhi(v.hi, p.x >> 16);
-        const uint32_t fan = (p.x >> 8) & 0xFFu;
-        const uint32_t s0 = p.y & 0xFFFFu, s1 = p.y >> 16, s2 = p.z & 0xFFFFu;
-        // part = number of cumulative bounds <= r among the first fan-1
-        const uint32_t c1 = s0, c2 = s0 + s1, c3 = c2 + s2;
-        const uint32_t part = (uint32_t)(r >= c1) + (uint32_t)(fan > 2 && r >= c2) + (uint32_t)(fan > 3 && r >= c3);
-        offset += part == 0 ? 0u : part == 1 ? c1 : part == 2 ? c2 : c3;
-        uint32_t child;
-        if (part == 0)
-          child = p.z >> 16;
-        else if (part == 1)
-          child = p.w & 0xFFFFu;
-        else if (part == 2)
-          child = p.w >> 16;
-        else
-          child = __ldg(pq + 2 * idx + 1).x;
-        idx = (int)child;
-        p = __ldg(pq + 2 * idx);
+        const uint32_t r = __umulhi(v.hi, p.x & 0x7FFFu);
+        const uint32_t part = (uint32_t)(r >= (p.x >> 16)) + (uint32_t)(r >= (p.y & 0xFFFFu)) + (uint32_t)(r >= (p.y >> 16));
+        const uint32_t sh = 16 * part;
+        offset += (uint32_t)(join64(p.x & 0xFFFF0000u, p.y) >> sh) & 0xFFFFu;  // lane `part` of (0, b1, b2, b3)
+        idx = (int)((uint32_t)(join64(p.z, p.w) >> sh) & 0xFFFFu);          // lane `part` of (c0 .. c3)
+        p = __ldg(pq + idx);
       }
       if (idx >= bad) {
         atomicOr(err, 1);
@@ -148,7 +136,7 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
         continue;
       }
       const uint64_t q = __ldg(nv + idx);
-      const uint32_t mleaf = p.x >> 16;
+      const uint32_t mleaf = p.x & 0x7FFFu;
       const int choice = (int)rib_choice(d, mx, kp, kl);
       offset += leaf_cell_pre(kp, kl, q, mleaf, d.mode, d.cache_k, choice);
     }
