@@ -128,8 +128,28 @@ SHK_D void leaf_finish(const LeafArgs& a, SM& sm, int64_t k0, int n, int64_t q, 
 }
 
 // -------------------------------------------------------------------------
-// Plain search body for one candidate seed per lane.
-template <bool WIDE>
+// Edge columns of the lanes in `lanes` (their seeds s): the warp recomputes
+// them cooperatively (lane i hashes keys i, i+32) instead of every lane
+// storing its edges for every seed; only filter-passing seeds need them.
+SHK_D void plain_fill_edges(const uint4* keys, int n, uint64_t s, unsigned lanes, uint16_t* ew, int lane) {
+  while (lanes) {
+    const int L = __ffs(lanes) - 1;
+    lanes &= lanes - 1;
+    const uint64_t sl = __shfl_sync(FULL_WARP, s, L);
+    const u2 x = seed_mixer_pre_d(sl, TAG_LEAF);
+    for (int i = lane; i < n; i += 32) {
+      const uint4 k = keys[i];
+      uint32_t h0, h1;
+      leaf_pair_d(remix_pre_d(u2{k.x, k.y}, u2{k.z, k.w}, x), (uint32_t)n, (uint32_t)(n - 1), h0, h1);
+      ew[i * 32 + L] = (uint16_t)(h0 | (h1 << 8));
+    }
+  }
+  __syncwarp();
+}
+
+// Plain search body for one candidate seed per lane (STORE: also write the
+// lane's edge column).
+template <bool WIDE, bool STORE = true>
 SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
   u2 x = seed_mixer_pre_d(s, TAG_LEAF);
   const uint32_t un = (uint32_t)n, unm1 = (uint32_t)(n - 1);
@@ -146,7 +166,7 @@ SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
       m0 |= shl_clamp(1u, h0) | shl_clamp(1u, h1);
       m1 |= shl_clamp(1u, h0 - 32u) | shl_clamp(1u, h1 - 32u);
     }
-    e[i * 32] = (uint16_t)(h0 | (h1 << 8));
+    if (STORE) e[i * 32] = (uint16_t)(h0 | (h1 << 8));
   }
   if (!WIDE) {
     uint32_t full = (n == 32) ? 0xFFFFFFFFu : ((1u << n) - 1u);
@@ -178,8 +198,9 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
     for (uint64_t R = 0; R < a.max_seed; R += (uint64_t)TW * 32, par ^= 1) {
       const uint64_t s = R + (uint64_t)warp * 32 + lane;
       const bool valid = s < a.max_seed;
-      bool full = valid && plain_mask_full<WIDE>(sm.keys, n, s, e);
+      bool full = valid && plain_mask_full<WIDE, false>(sm.keys, n, s, e);
       unsigned pb = __ballot_sync(FULL_WARP, full);
+      if (pb) plain_fill_edges(sm.keys, n, s, pb, sm.edges[warp], lane);
       const bool acc = warp_first_accept(sm.edges[warp], full ? 1ull : 0ull, n, lane, sm.chk[warp]) == 0;
       unsigned ab = __ballot_sync(FULL_WARP, acc);
       if (lane == 0) {
