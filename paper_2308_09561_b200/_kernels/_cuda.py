@@ -545,6 +545,35 @@ class GpuBuild:
               "choice_sorted")
         return out
 
+    # column-sharded ribbon (dist.ribbon_sharded drives the exchange)
+    def dribbon_begin(self, choice_sorted, m, seed, c0, c1):
+        ch = np.ascontiguousarray(choice_sorted, dtype=np.uint8)
+        nexp = ctypes.c_int64(0)
+        bad = ctypes.c_int(0)
+        check(_L().shk_build_dribbon_begin(self.handle, ptr(ch), int(m), int(seed), int(c0), int(c1),
+                                           ctypes.byref(nexp), ctypes.byref(bad)), "ribbon (sharded)")
+        return int(nexp.value), bool(bad.value)
+
+    def dribbon_exports(self, n):
+        rows = np.zeros(3 * max(int(n), 0), dtype=np.uint64)
+        check(_L().shk_build_dribbon_exports(self.handle, ptr(rows) if len(rows) else None, int(n)), "ribbon exports")
+        return rows
+
+    def dribbon_import(self, rows):
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        nexp = ctypes.c_int64(0)
+        bad = ctypes.c_int(0)
+        check(_L().shk_build_dribbon_import(self.handle, ptr(rows) if len(rows) else None, len(rows) // 3,
+                                            ctypes.byref(nexp), ctypes.byref(bad)), "ribbon import")
+        return int(nexp.value), bool(bad.value)
+
+    def dribbon_backsub(self, y_in, ncols):
+        y_in = np.ascontiguousarray(y_in, dtype=np.uint32)
+        y_out = np.zeros(4, dtype=np.uint32)
+        words = np.zeros((int(ncols) + 63) // 64, dtype=np.uint64)
+        check(_L().shk_build_dribbon_backsub(self.handle, ptr(y_in), ptr(y_out), ptr(words)), "ribbon backsub")
+        return y_out, words
+
     def ribbon(self, m, max_tries=64, choice=None, sorted_keys=False):
         words = np.zeros((int(m) + 63) // 64, dtype=np.uint64)
         seed = ctypes.c_uint64(0)

@@ -885,13 +885,15 @@ struct shk_build {
   // run() permutes `keys` in place only inside the rank's bucket range)
   bool keep_sorted = false;
   DBuf sorted;
+  DBuf drhs;            // choice bits (sorted order) of a column-sharded ribbon
+  int64_t dcols = 0;    // its local column count
   // phase timing (CUDA events on the context stream): 0 bucketize, 1 splits,
   // 2 leaves, 3 rice, 4 ribbon (last run)
   cudaEvent_t ev[12] = {};
   float phase_ms[6] = {0, 0, 0, 0, 0, 0};
   int64_t split_evals = 0;
   explicit shk_build(shk_ctx* ctx)
-      : c(ctx), keys(ctx), tmp(ctx), prefix(ctx), choice(ctx), words(ctx), place(ctx), sorted(ctx) {}
+      : c(ctx), keys(ctx), tmp(ctx), prefix(ctx), choice(ctx), words(ctx), place(ctx), sorted(ctx), drhs(ctx) {}
   ~shk_build() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -1343,6 +1345,45 @@ int shk_build_set_record_placements(shk_build* b, int on) {
 
 int shk_build_set_keep_sorted(shk_build* b, int on) {
   b->keep_sorted = on != 0;
+  return 0;
+}
+
+// ---- column-sharded ribbon over the build's sorted keys ---------------------
+int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int64_t m, uint64_t seed, int64_t c0,
+                            int64_t c1, int64_t* n_export, int* bad) {
+  shk_ctx* c = b->c;
+  if (!b->sorted.p) {
+    shk_set_error("sorted keys were not kept (shk_build_set_keep_sorted)");
+    return SHK_INVALID;
+  }
+  if (!b->drhs.p) {
+    RC(b->drhs.alloc((size_t)b->N));
+  }
+  RC(h2d(c, b->drhs.p, choice_sorted, (size_t)b->N));
+  b->dcols = c1 - c0;
+  b->mark(6);  // ribbon phase: from here to the end of backsub (exchanges included)
+  return shk_ribbon_dist_begin(c->rib, b->sorted.as<uint64_t>(), b->drhs.as<uint8_t>(), b->N, m, seed, c0, c1,
+                               n_export, bad, c->stream);
+}
+
+int shk_build_dribbon_exports(shk_build* b, void* rows_out, int64_t n) {
+  return shk_ribbon_dist_take_exports(b->c->rib, rows_out, n, b->c->stream);
+}
+
+int shk_build_dribbon_import(shk_build* b, const void* rows_in, int64_t n, int64_t* n_export, int* bad) {
+  return shk_ribbon_dist_import(b->c->rib, rows_in, n, n_export, bad, b->c->stream);
+}
+
+int shk_build_dribbon_backsub(shk_build* b, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out) {
+  shk_ctx* c = b->c;
+  const int64_t nw = (b->dcols + 63) / 64;
+  DBuf tw(c);
+  RC(tw.alloc((size_t)nw * 8));
+  RC(shk_ribbon_dist_backsub(c->rib, y_in, y_out, tw.as<uint64_t>(), c->stream));
+  RC(d2h(c, words_out, tw.p, (size_t)nw * 8));
+  b->mark(7);
+  RC(csync(c));
+  b->phase_ms[4] = b->span(6, 7);
   return 0;
 }
 

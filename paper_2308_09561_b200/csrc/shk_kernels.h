@@ -142,6 +142,14 @@ int shk_ribbon_solve_keys(ShkRibbon* r, const uint64_t* keys, const uint8_t* rhs
 int shk_ribbon_solve_rows(ShkRibbon* r, const int64_t* starts, const uint64_t* p0, const uint64_t* p1,
                           const uint8_t* rhs, int64_t N, int64_t m, uint64_t* words_out, int* consistent,
                           cudaStream_t st);
+// column-sharded solve (shk_ribbon.cu): rows are 24 bytes (p0, p1, start | rhs << 62)
+int shk_ribbon_dist_begin(ShkRibbon* r, const uint64_t* keys, const uint8_t* rhs, int64_t N, int64_t m,
+                          uint64_t seed, int64_t c0, int64_t c1, int64_t* n_export, int* bad, cudaStream_t st);
+int shk_ribbon_dist_take_exports(ShkRibbon* r, void* rows_out, int64_t n, cudaStream_t st);
+int shk_ribbon_dist_import(ShkRibbon* r, const void* rows_in, int64_t n, int64_t* n_export, int* bad,
+                           cudaStream_t st);
+int shk_ribbon_dist_backsub(ShkRibbon* r, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out,
+                            cudaStream_t st);
 int shk_launch_ribbon_rows(const uint64_t* hi, const uint64_t* lo, int stride, int64_t N, int64_t m, uint64_t seed,
                            int64_t* starts, uint64_t* p0, uint64_t* p1, cudaStream_t st);
 // Split-hash part index of every key (split_parts seam).

@@ -67,20 +67,22 @@ __global__ void ribbon_rows_kernel(const uint64_t* hi, const uint64_t* lo, int s
 }
 
 // Rows from keys directly into chunk buckets (fused generation + histogram).
+// Only rows starting in columns [c0, c1) are kept, re-based to c0 (a
+// column-sharded solve; the single-GPU solve passes the whole range).
 __global__ void ribbon_keyrows_hist_kernel(const ulonglong2* keys, int64_t N, int64_t m, uint64_t seed,
-                                           int64_t* hist) {
+                                           int64_t* hist, int64_t c0, int64_t c1) {
   const u2 xs = split64(seed_mixer(seed, TAG_RSTART));
   const uint64_t span = (uint64_t)(m - RIBBON_W + 1);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     const ulonglong2 k = keys[i];
     u2 v = remix_d(split64(k.x), split64(k.y), xs);
     int64_t s = (int64_t)(((uint64_t)v.hi * span) >> 32);
-    atomicAdd((unsigned long long*)&hist[s / CE], 1ull);
+    if (s >= c0 && s < c1) atomicAdd((unsigned long long*)&hist[(s - c0) / CE], 1ull);
   }
 }
 
 __global__ void ribbon_keyrows_scatter_kernel(const ulonglong2* keys, const uint8_t* rhs, int64_t N, int64_t m,
-                                              uint64_t seed, int64_t* cursor, RRow* rows) {
+                                              uint64_t seed, int64_t* cursor, RRow* rows, int64_t c0, int64_t c1) {
   const u2 xs = split64(seed_mixer(seed, TAG_RSTART));
   const u2 x0 = split64(seed_mixer(seed, TAG_RPAT0));
   const u2 x1 = split64(seed_mixer(seed, TAG_RPAT1));
@@ -90,6 +92,8 @@ __global__ void ribbon_keyrows_scatter_kernel(const ulonglong2* keys, const uint
     u2 kh = split64(k.x), kl = split64(k.y);
     u2 v = remix_d(kh, kl, xs);
     int64_t s = (int64_t)(((uint64_t)v.hi * span) >> 32);
+    if (s < c0 || s >= c1) continue;
+    s -= c0;
     u2 a = remix_d(kh, kl, x0);
     u2 b = remix_d(kh, kl, x1);
     int64_t pos = (int64_t)atomicAdd((unsigned long long*)&cursor[s / CE], 1ull);
@@ -333,13 +337,17 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
 // c + 1 (right boundary of chunk c).  One warp; the next chunk's forms are
 // loaded while the current one is evaluated.  ysel[c] is the boundary in the
 // coef layout (word q bit L = y bit 4L + q; bit 127 = 1 for the constant).
-__global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, const uint4* forms, uint4* ysel) {
+// y_io (device, one uint4): in = the 127 solution bits right of the last chunk
+// (zero at the end of the system; the right neighbour's first bits in a
+// column-sharded solve), out = the first 127 solution bits of chunk 0.
+__global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, const uint4* forms, uint4* ysel,
+                                                          uint4* y_io) {
   // D-deep cp.async ring: the forms of chunk c - D are in flight while chunk
   // c is evaluated (each lane copies and later reads only its own 64 bytes).
   constexpr int D = 8;
   __shared__ uint4 ring[D][128];
   const int lane = threadIdx.x;
-  uint4 y = make_uint4(0, 0, 0, 0);  // boundary right of the last chunk: zero
+  uint4 y = *y_io;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     const int64_t cc = nbchunks - 1 - k;
@@ -389,6 +397,7 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
     }
     y = make_uint4(acc0, acc1, acc2, acc3 & 0x7FFFFFFFu);  // 127 bits
   }
+  if (lane == 0) *y_io = y;
 }
 
 // Final back substitution, a parallel map: sol[col] = parity(coef[col] &
@@ -435,15 +444,36 @@ __global__ void ribbon_query_kernel(const int64_t* starts, const uint64_t* p0, c
   }
 }
 
-__global__ void ribbon_ovf_hist_kernel(const RRow* o, int64_t n, int64_t* hist) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd((unsigned long long*)&hist[(o[i].s & S_MASK) / CE], 1ull);
+// Overflow rows of a pass, regrouped by the chunk they reached.  Rows past the
+// local column range [0, M) (a column-sharded solve: they belong to the next
+// rank) are appended to `exp` in global columns (+ c0) instead.
+__global__ void ribbon_ovf_hist_kernel(const RRow* o, int64_t n, int64_t* hist, int64_t M) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = o[i].s & S_MASK;
+    if (s < M) atomicAdd((unsigned long long*)&hist[s / CE], 1ull);
+  }
 }
-__global__ void ribbon_ovf_scatter_kernel(const RRow* o, int64_t n, int64_t* cursor, RRow* out) {
+__global__ void ribbon_ovf_scatter_kernel(const RRow* o, int64_t n, int64_t* cursor, RRow* out, int64_t M,
+                                          RRow* exp, int64_t* exp_count, int64_t c0) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     RRow r = o[i];
-    int64_t p = (int64_t)atomicAdd((unsigned long long*)&cursor[(r.s & S_MASK) / CE], 1ull);
-    out[p] = r;
+    const int64_t s = r.s & S_MASK;
+    if (s < M) {
+      int64_t p = (int64_t)atomicAdd((unsigned long long*)&cursor[s / CE], 1ull);
+      out[p] = r;
+    } else {
+      const int64_t k = (int64_t)atomicAdd((unsigned long long*)exp_count, 1ull);
+      r.s = (s + c0) | (r.s & RHS_BIT);
+      exp[k] = r;
+    }
+  }
+}
+
+// Imported rows (global columns) re-based to this rank's first column.
+__global__ void ribbon_rebase_kernel(RRow* o, int64_t n, int64_t c0) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = o[i].s;
+    o[i].s = ((s & S_MASK) - c0) | (s & RHS_BIT);
   }
 }
 
@@ -451,10 +481,20 @@ __global__ void ribbon_ovf_scatter_kernel(const RRow* o, int64_t n, int64_t* cur
 
 using namespace shk;
 
+// Byte offsets of the solver's buffers inside ShkRibbon::buf.
+struct RibLayout {
+  size_t off_rows, off_rows2, off_ovf, off_exp, off_hist, off_rowoff, off_cursor, off_sp0, off_sp1, off_occ, off_sb,
+      off_forms, off_coef, off_y, off_yio, off_cnt, off_scan, total;
+};
+
 struct ShkRibbon {
   // device buffers, grown on demand
   void* buf = nullptr;
   size_t cap = 0;
+  // column-sharded solve state (shk_ribbon_dist_*): rows capacity, local
+  // column count, first global column
+  RibLayout dL{};
+  int64_t dN = 0, dM = 0, dc0 = 0;
 };
 
 int shk_ribbon_create(ShkRibbon** out) {
@@ -470,11 +510,6 @@ void shk_ribbon_destroy(ShkRibbon* r) {
 
 namespace {
 
-struct RibLayout {
-  size_t off_rows, off_rows2, off_ovf, off_hist, off_rowoff, off_cursor, off_sp0, off_sp1, off_occ, off_sb, off_forms,
-      off_coef, off_y, off_cnt, off_scan, total;
-};
-
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 RibLayout layout(int64_t N, int64_t m) {
@@ -488,6 +523,8 @@ RibLayout layout(int64_t N, int64_t m) {
   L.off_rows2 = o;
   o += al((size_t)(N + 1) * sizeof(RRow));
   L.off_ovf = o;
+  o += al((size_t)(N + 1) * sizeof(RRow));
+  L.off_exp = o;
   o += al((size_t)(N + 1) * sizeof(RRow));
   L.off_hist = o;
   o += al((size_t)(nch + 1) * 8);
@@ -509,6 +546,8 @@ RibLayout layout(int64_t N, int64_t m) {
   o += al((size_t)m * 16);
   L.off_y = o;
   o += al((size_t)nbc * 16);
+  L.off_yio = o;
+  o += 256;
   L.off_cnt = o;
   o += 256;
   L.off_scan = o;
@@ -534,86 +573,171 @@ int grid_for(int64_t n) {
   return (int)g;
 }
 
-// Shared driver once rows are in r->buf at off_rows with the chunk offsets
-// in off_rowoff.
-int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_t* words_out, int* consistent,
-                 cudaStream_t st) {
-  char* B = (char*)R->buf;
-  const int64_t nch = (m + CE - 1) / CE;
-  const int64_t nbc = (m + CB - 1) / CB;
-  const int64_t nw32 = (m + 31) / 32 + CE / 32;
-  RRow* rows = (RRow*)(B + L.off_rows);
-  RRow* rows2 = (RRow*)(B + L.off_rows2);
-  RRow* ovf = (RRow*)(B + L.off_ovf);
-  int64_t* hist = (int64_t*)(B + L.off_hist);
-  int64_t* rowoff = (int64_t*)(B + L.off_rowoff);
-  int64_t* cursor = (int64_t*)(B + L.off_cursor);
-  uint64_t* sp0 = (uint64_t*)(B + L.off_sp0);
-  uint64_t* sp1 = (uint64_t*)(B + L.off_sp1);
-  uint32_t* occ = (uint32_t*)(B + L.off_occ);
-  uint32_t* sb = (uint32_t*)(B + L.off_sb);
-  uint4* forms = (uint4*)(B + L.off_forms);
-  uint4* coef = (uint4*)(B + L.off_coef);
-  uint4* yb = (uint4*)(B + L.off_y);
-  int64_t* cnt = (int64_t*)(B + L.off_cnt);  // [0] ovf count, [1] inconsistent flag (int)
-  void* scan = B + L.off_scan;
+// Views of the solver buffers.
+struct RibBufs {
+  RRow *rows, *rows2, *ovf, *exp;
+  int64_t *hist, *rowoff, *cursor, *cnt;  // cnt: [0] ovf count, [1] inconsistent flag (int), [2] export count
+  uint64_t *sp0, *sp1;
+  uint32_t *occ, *sb;
+  uint4 *forms, *coef, *yb, *yio;
+  void* scan;
+  RibBufs(ShkRibbon* R, const RibLayout& L) {
+    char* B = (char*)R->buf;
+    rows = (RRow*)(B + L.off_rows);
+    rows2 = (RRow*)(B + L.off_rows2);
+    ovf = (RRow*)(B + L.off_ovf);
+    exp = (RRow*)(B + L.off_exp);
+    hist = (int64_t*)(B + L.off_hist);
+    rowoff = (int64_t*)(B + L.off_rowoff);
+    cursor = (int64_t*)(B + L.off_cursor);
+    cnt = (int64_t*)(B + L.off_cnt);
+    sp0 = (uint64_t*)(B + L.off_sp0);
+    sp1 = (uint64_t*)(B + L.off_sp1);
+    occ = (uint32_t*)(B + L.off_occ);
+    sb = (uint32_t*)(B + L.off_sb);
+    forms = (uint4*)(B + L.off_forms);
+    coef = (uint4*)(B + L.off_coef);
+    yb = (uint4*)(B + L.off_y);
+    yio = (uint4*)(B + L.off_yio);
+    scan = B + L.off_scan;
+  }
+};
 
-  SHK_CUDA(cudaMemsetAsync(sp0, 0, (size_t)(m + 64) * 8, st));
-  SHK_CUDA(cudaMemsetAsync(sp1, 0, (size_t)(m + 64) * 8, st));
-  SHK_CUDA(cudaMemsetAsync(occ, 0, (size_t)nw32 * 4, st));
-  SHK_CUDA(cudaMemsetAsync(sb, 0, (size_t)nw32 * 4, st));
-  SHK_CUDA(cudaMemsetAsync(cnt, 0, 256, st));
-  int* bad = (int*)(cnt + 1);
-  int64_t pending = N;
-  RRow* cur = rows;
+// Empty slot table for M columns.
+int rib_clear(ShkRibbon* R, const RibLayout& L, int64_t M, cudaStream_t st) {
+  RibBufs b(R, L);
+  const int64_t nw32 = (M + 31) / 32 + CE / 32;
+  SHK_CUDA(cudaMemsetAsync(b.sp0, 0, (size_t)(M + 64) * 8, st));
+  SHK_CUDA(cudaMemsetAsync(b.sp1, 0, (size_t)(M + 64) * 8, st));
+  SHK_CUDA(cudaMemsetAsync(b.occ, 0, (size_t)nw32 * 4, st));
+  SHK_CUDA(cudaMemsetAsync(b.sb, 0, (size_t)nw32 * 4, st));
+  SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 256, st));
+  return 0;
+}
+
+// Regroup `n` rows at `src` (local columns) by elimination chunk into
+// rows2 / rowoff; rows past column M go to the export buffer (global
+// columns, + c0).
+int rib_regroup(const RibBufs& b, const RRow* src, int64_t n, int64_t M, int64_t c0, cudaStream_t st) {
+  const int64_t nch = (M + CE - 1) / CE;
+  SHK_CUDA(cudaMemsetAsync(b.hist, 0, (size_t)(nch + 1) * 8, st));
+  ribbon_ovf_hist_kernel<<<grid_for(n), 256, 0, st>>>(src, n, b.hist, M);
+  SHK_LAUNCHED();
+  int rc = shk_exclusive_scan_i64(b.hist, b.rowoff, nch, b.scan, shk_scan_scratch(nch), st);
+  if (rc) return rc;
+  SHK_CUDA(cudaMemcpyAsync(b.cursor, b.rowoff, (size_t)nch * 8, cudaMemcpyDeviceToDevice, st));
+  ribbon_ovf_scatter_kernel<<<grid_for(n), 256, 0, st>>>(src, n, b.cursor, b.rows2, M, b.exp, b.cnt + 2, c0);
+  SHK_LAUNCHED();
+  return 0;
+}
+
+// Elimination passes over `pending` chunk-grouped rows at `cur` (offsets in
+// rowoff) into the slot table of M local columns, until no row is left
+// inside the range.  first: the slot table is known empty.  Rows leaving the
+// range accumulate in the export buffer (count cnt[2]).  *bad: inconsistent.
+int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t pending, int64_t M, int64_t c0, int first,
+               int* bad_out, cudaStream_t st) {
+  RibBufs b(R, L);
+  const int64_t nch = (M + CE - 1) / CE;
+  int* bad = (int*)(b.cnt + 1);
+  *bad_out = 0;
   for (int pass = 0; pending > 0; ++pass) {
-    SHK_CUDA(cudaMemsetAsync(cnt, 0, 8, st));
-    ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(cur, rowoff, nch, m, sp0, sp1, occ, sb, ovf, cnt, bad,
-                                                      pass == 0 ? 1 : 0);
+    SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 8, st));
+    ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(cur, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt,
+                                                      bad, (first && pass == 0) ? 1 : 0);
     SHK_LAUNCHED();
-    int64_t h[2];
-    SHK_CUDA(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, st));
+    int64_t h[3];
+    SHK_CUDA(cudaMemcpyAsync(h, b.cnt, 24, cudaMemcpyDeviceToHost, st));
     SHK_CUDA(cudaStreamSynchronize(st));
-    if ((int)h[1]) break;
-    pending = h[0];
-    if (!pending) break;
-    // regroup overflow rows by chunk into rows2
-    SHK_CUDA(cudaMemsetAsync(hist, 0, (size_t)(nch + 1) * 8, st));
-    ribbon_ovf_hist_kernel<<<grid_for(pending), 256, 0, st>>>(ovf, pending, hist);
-    SHK_LAUNCHED();
-    int rc = shk_exclusive_scan_i64(hist, rowoff, nch, scan, shk_scan_scratch(nch), st);
+    if ((int)h[1]) {
+      *bad_out = 1;
+      return 0;
+    }
+    const int64_t novf = h[0];
+    if (!novf) break;
+    int rc = rib_regroup(b, b.ovf, novf, M, c0, st);
     if (rc) return rc;
-    SHK_CUDA(cudaMemcpyAsync(cursor, rowoff, (size_t)nch * 8, cudaMemcpyDeviceToDevice, st));
-    ribbon_ovf_scatter_kernel<<<grid_for(pending), 256, 0, st>>>(ovf, pending, cursor, rows2);
-    SHK_LAUNCHED();
-    cur = rows2;
+    int64_t e1 = 0;
+    SHK_CUDA(cudaMemcpyAsync(&e1, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
+    SHK_CUDA(cudaStreamSynchronize(st));
+    pending = novf - (e1 - h[2]);  // rows still inside the range
+    cur = b.rows2;
     if (pass > 100000) {
       shk_set_error("ribbon elimination did not converge");
       return -1;
     }
   }
-  int hbad = 0;
-  SHK_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
-  SHK_CUDA(cudaStreamSynchronize(st));
-  if (hbad) {
+  return 0;
+}
+
+// Back substitution of the M local columns given the 127 solution bits right
+// of them (y_in, host); y_out (host, may be null) gets the range's first 127
+// bits; words_out (device) gets ceil(M/64) solution words.
+int rib_backsub(ShkRibbon* R, const RibLayout& L, int64_t M, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out,
+                cudaStream_t st) {
+  RibBufs b(R, L);
+  const int64_t nbc = (M + CB - 1) / CB;
+  const uint4 y0 = y_in ? make_uint4(y_in[0], y_in[1], y_in[2], y_in[3]) : make_uint4(0, 0, 0, 0);
+  SHK_CUDA(cudaMemcpyAsync(b.yio, &y0, 16, cudaMemcpyHostToDevice, st));
+  ribbon_forms_kernel<<<(unsigned)nbc, 128, 0, st>>>(M, nbc, b.sp0, b.sp1, b.occ, b.sb, b.forms, b.coef);
+  SHK_LAUNCHED();
+  ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, b.forms, b.yb, b.yio);
+  SHK_LAUNCHED();
+  const int64_t nwords = (M + 63) / 64;
+  int64_t fb = (nwords + 7) / 8;
+  if (fb > 148 * 8) fb = 148 * 8;
+  ribbon_final_kernel<<<(unsigned)fb, 256, 0, st>>>(M, nwords, b.coef, b.yb, words_out);
+  SHK_LAUNCHED();
+  if (y_out) {
+    SHK_CUDA(cudaMemcpyAsync(y_out, b.yio, 16, cudaMemcpyDeviceToHost, st));
+    SHK_CUDA(cudaStreamSynchronize(st));
+  }
+  return 0;
+}
+
+// Shared single-system driver once rows are in r->buf at off_rows with the
+// chunk offsets in off_rowoff.
+int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_t* words_out, int* consistent,
+                 cudaStream_t st) {
+  int rc = rib_clear(R, L, m, st);
+  if (rc) return rc;
+  int bad = 0;
+  rc = rib_passes(R, L, RibBufs(R, L).rows, N, m, 0, 1, &bad, st);
+  if (rc) return rc;
+  if (bad) {
     *consistent = 0;
     return 0;
   }
   *consistent = 1;
-  ribbon_forms_kernel<<<(unsigned)nbc, 128, 0, st>>>(m, nbc, sp0, sp1, occ, sb, forms, coef);
-  SHK_LAUNCHED();
-  ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, forms, yb);
-  SHK_LAUNCHED();
-  const int64_t nwords = (m + 63) / 64;
-  int64_t fb = (nwords + 7) / 8;
-  if (fb > 148 * 8) fb = 148 * 8;
-  ribbon_final_kernel<<<(unsigned)fb, 256, 0, st>>>(m, nwords, coef, yb, words_out);
-  SHK_LAUNCHED();
-  return 0;
+  return rib_backsub(R, L, m, nullptr, nullptr, words_out, st);
 }
 
 }  // namespace
 
+
+namespace {
+// Rows of the keys whose start column lies in [c0, c0 + M), chunk-grouped at
+// off_rows / off_rowoff in local columns.
+int gen_keyrows(ShkRibbon* R, const RibLayout& L, const ulonglong2* keys, const uint8_t* rhs, int64_t N, int64_t m,
+                uint64_t seed, int64_t c0, int64_t M, cudaStream_t st) {
+  RibBufs b(R, L);
+  const int64_t nch = (M + CE - 1) / CE;
+  const int64_t c1 = c0 + M;
+  SHK_CUDA(cudaMemsetAsync(b.hist, 0, (size_t)(nch + 1) * 8, st));
+  if (N > 0) {
+    ribbon_keyrows_hist_kernel<<<grid_for(N), 256, 0, st>>>(keys, N, m, seed, b.hist, c0, c1);
+    SHK_LAUNCHED();
+  }
+  int rc = shk_exclusive_scan_i64(b.hist, b.rowoff, nch, b.scan, shk_scan_scratch(nch), st);
+  if (rc) return rc;
+  SHK_CUDA(cudaMemcpyAsync(b.cursor, b.rowoff, (size_t)nch * 8, cudaMemcpyDeviceToDevice, st));
+  if (N > 0) {
+    ribbon_keyrows_scatter_kernel<<<grid_for(N), 256, 0, st>>>(keys, rhs, N, m, seed, b.cursor, b.rows, c0, c1);
+    SHK_LAUNCHED();
+  }
+  return 0;
+}
+}  // namespace
 
 int shk_ribbon_solve_keys(ShkRibbon* R, const uint64_t* keys_u64, const uint8_t* rhs, int64_t N, int64_t m,
                           uint64_t seed, uint64_t* words_out, int* consistent, cudaStream_t st) {
@@ -625,25 +749,93 @@ int shk_ribbon_solve_keys(ShkRibbon* R, const uint64_t* keys_u64, const uint8_t*
   RibLayout L = layout(N, m);
   int rc = ensure(R, L.total);
   if (rc) return rc;
-  char* B = (char*)R->buf;
-  const int64_t nch = (m + CE - 1) / CE;
-  int64_t* hist = (int64_t*)(B + L.off_hist);
-  int64_t* rowoff = (int64_t*)(B + L.off_rowoff);
-  int64_t* cursor = (int64_t*)(B + L.off_cursor);
-  SHK_CUDA(cudaMemsetAsync(hist, 0, (size_t)(nch + 1) * 8, st));
-  if (N > 0) {
-    ribbon_keyrows_hist_kernel<<<grid_for(N), 256, 0, st>>>(keys, N, m, seed, hist);
-    SHK_LAUNCHED();
-  }
-  rc = shk_exclusive_scan_i64(hist, rowoff, nch, B + L.off_scan, shk_scan_scratch(nch), st);
+  rc = gen_keyrows(R, L, keys, rhs, N, m, seed, 0, m, st);
   if (rc) return rc;
-  SHK_CUDA(cudaMemcpyAsync(cursor, rowoff, (size_t)nch * 8, cudaMemcpyDeviceToDevice, st));
-  if (N > 0) {
-    ribbon_keyrows_scatter_kernel<<<grid_for(N), 256, 0, st>>>(keys, rhs, N, m, seed, cursor,
-                                                               (RRow*)(B + L.off_rows));
-    SHK_LAUNCHED();
-  }
   return solve_sorted(R, L, N, m, words_out, consistent, st);
+}
+
+// ---------------------------------------------------------------------------
+// Column-sharded solve (SURVEY.md §8(e) option B): this rank owns columns
+// [c0, c1) (c0 a multiple of CB).  begin: rows starting in the range,
+// eliminated locally; rows whose pivot walks past c1 are exported (global
+// columns) for the right neighbour, which imports them and may export
+// further.  When no rank exports any more, backsub runs right to left
+// across ranks: each takes the first 127 solution bits of its right
+// neighbour and hands its own first 127 bits to its left neighbour.  The
+// solution is the single-system one.
+int shk_ribbon_dist_begin(ShkRibbon* R, const uint64_t* keys_u64, const uint8_t* rhs, int64_t N, int64_t m,
+                          uint64_t seed, int64_t c0, int64_t c1, int64_t* n_export, int* bad, cudaStream_t st) {
+  if (m < RIBBON_W || c0 < 0 || c1 > m || c0 >= c1 || (c0 % CB) != 0 || (c1 != m && (c1 % CB) != 0)) {
+    shk_set_error("bad column range [%lld, %lld) of %lld", (long long)c0, (long long)c1, (long long)m);
+    return 3;
+  }
+  const int64_t M = c1 - c0;
+  RibLayout L = layout(N, M);
+  int rc = ensure(R, L.total);
+  if (rc) return rc;
+  R->dL = L;
+  R->dN = N;
+  R->dM = M;
+  R->dc0 = c0;
+  rc = rib_clear(R, L, M, st);
+  if (rc) return rc;
+  rc = gen_keyrows(R, L, reinterpret_cast<const ulonglong2*>(keys_u64), rhs, N, m, seed, c0, M, st);
+  if (rc) return rc;
+  RibBufs b(R, L);
+  const int64_t nch = (M + CE - 1) / CE;
+  int64_t nrows = 0;
+  SHK_CUDA(cudaMemcpyAsync(&nrows, b.rowoff + nch, 8, cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaStreamSynchronize(st));
+  rc = rib_passes(R, L, b.rows, nrows, M, c0, 1, bad, st);
+  if (rc) return rc;
+  SHK_CUDA(cudaMemcpyAsync(n_export, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// Copy out (host, 24 bytes per row: p0, p1, start | rhs << 62) and clear the
+// exported rows.
+int shk_ribbon_dist_take_exports(ShkRibbon* R, void* rows_out, int64_t n, cudaStream_t st) {
+  RibBufs b(R, R->dL);
+  if (n > 0) SHK_CUDA(cudaMemcpyAsync(rows_out, b.exp, (size_t)n * sizeof(RRow), cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaMemsetAsync(b.cnt + 2, 0, 8, st));
+  SHK_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// Insert rows exported by the left neighbour (global columns >= c0).
+int shk_ribbon_dist_import(ShkRibbon* R, const void* rows_in, int64_t n, int64_t* n_export, int* bad,
+                           cudaStream_t st) {
+  RibBufs b(R, R->dL);
+  *bad = 0;
+  if (n > R->dN) {
+    shk_set_error("too many imported rows");
+    return 3;
+  }
+  if (n > 0) {
+    SHK_CUDA(cudaMemcpyAsync(b.ovf, rows_in, (size_t)n * sizeof(RRow), cudaMemcpyHostToDevice, st));
+    ribbon_rebase_kernel<<<grid_for(n), 256, 0, st>>>(b.ovf, n, R->dc0);
+    SHK_LAUNCHED();
+    int64_t e0 = 0, e1 = 0;
+    SHK_CUDA(cudaMemcpyAsync(&e0, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
+    int rc = rib_regroup(b, b.ovf, n, R->dM, R->dc0, st);
+    if (rc) return rc;
+    SHK_CUDA(cudaMemcpyAsync(&e1, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
+    SHK_CUDA(cudaStreamSynchronize(st));
+    rc = rib_passes(R, R->dL, b.rows2, n - (e1 - e0), R->dM, R->dc0, 0, bad, st);
+    if (rc) return rc;
+  }
+  SHK_CUDA(cudaMemcpyAsync(n_export, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// y_in: the right neighbour's first 127 solution bits (zero for the last
+// range); y_out: this range's first 127 bits; words_out (device): its
+// (c1 - c0 + 63) / 64 solution words.
+int shk_ribbon_dist_backsub(ShkRibbon* R, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out,
+                            cudaStream_t st) {
+  return rib_backsub(R, R->dL, R->dM, y_in, y_out, words_out, st);
 }
 
 int shk_ribbon_solve_rows(ShkRibbon* R, const int64_t* starts, const uint64_t* p0, const uint64_t* p1,

@@ -100,6 +100,84 @@ def exchange_and_merge(words, bit_len, rel_offsets, choice_slice, device=None):
     return sw, bl, bo, choice
 
 
+import os
+
+RIBBON_CB = 8192  # back-substitution chunk of the ribbon kernels (csrc/shk_ribbon.cu CB)
+# column-sharded ribbon over all ranks (default) or rank 0 alone (SHK_RIBBON_SHARDED=0)
+RIBBON_SHARDED = os.environ.get("SHK_RIBBON_SHARDED", "1") != "0"
+
+
+def column_range(m: int, rank: int, world: int, cb: int = RIBBON_CB) -> Tuple[int, int]:
+    """Columns of the ribbon owned by a rank: whole back-substitution chunks."""
+    nch = (m + cb - 1) // cb
+    a, b = (nch * rank) // world, (nch * (rank + 1)) // world
+    return min(a * cb, m), min(b * cb, m)
+
+
+def _bcast_u32(arr, src, device=None):
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint32).view(np.int32).copy())
+    t = t.to(device) if device is not None else t
+    dist.broadcast(t, src)
+    return t.cpu().numpy().view(np.uint32)
+
+
+def ribbon_sharded(gb, choice_sorted, m, max_tries, device=None):
+    """Column-sharded ribbon solve (SURVEY.md §8(e) option B) over the process
+    group; every rank returns (seed, words of the whole system).
+
+    Rank r owns columns column_range(m, r, W).  Each rank eliminates the rows
+    starting in its range; rows whose pivot leaves it travel to the right
+    neighbour (exchange rounds until no rank exports); then the 127-bit
+    boundary solution travels right to left, each rank back-substitutes its
+    range, and one all-gather joins the words.  The solution is the
+    single-system one."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    c0, c1 = column_range(m, rank, world)
+    own = c1 > c0
+    dev = device if device is not None else torch.device("cpu")
+
+    def reduce(x, op):
+        t = torch.tensor([int(x)], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=op)
+        return int(t.item())
+
+    for seed in range(max_tries):
+        nexp, bad = gb.dribbon_begin(choice_sorted, m, seed, c0, c1) if own else (0, False)
+        passthrough = np.zeros(0, dtype=np.uint64)
+        while True:
+            if reduce(bad, dist.ReduceOp.MAX):
+                break
+            if reduce(nexp, dist.ReduceOp.SUM) == 0:
+                break
+            out = gb.dribbon_exports(nexp) if own else passthrough
+            parts = allgather_arrays(out, device)
+            incoming = parts[rank - 1] if rank > 0 else np.zeros(0, dtype=np.uint64)
+            if own:
+                nexp, bad = gb.dribbon_import(incoming)
+            else:  # an empty range forwards what it receives
+                passthrough, nexp, bad = incoming, len(incoming) // 3, False
+        else:  # pragma: no cover
+            pass
+        if reduce(bad, dist.ReduceOp.MAX):
+            continue
+        y = np.zeros(4, dtype=np.uint32)
+        words = np.zeros(0, dtype=np.uint64)
+        for r in reversed(range(world)):
+            if rank == r and own:
+                y_out, words = gb.dribbon_backsub(y, c1 - c0)
+            else:
+                y_out = y
+            y = _bcast_u32(y_out, r, device)
+        return seed, np.concatenate(allgather_arrays(words, device))
+    raise RuntimeError(f"retrieval system unsolvable after {max_tries} seeds")
+
+
 def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8, epsilon=0.05, device=None):
     """Bucket-range-sharded build over the current torch.distributed group.
 
@@ -136,9 +214,12 @@ def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8,
     choice = gb.choice_sorted(int(key_prefix[b0]), int(key_prefix[b1]))
     sw, bl, bit_offsets, choice_all = exchange_and_merge(words, bit_len, rel, choice, device)
     desc = None
-    if rank == 0:
-        m = retrieval._columns(n_keys, epsilon)
+    m = retrieval._columns(n_keys, epsilon)
+    if RIBBON_SHARDED:
+        rseed, rwords = ribbon_sharded(gb, choice_all, m, retrieval.RETRY_CAP, device)
+    elif rank == 0:
         rseed, rwords = gb.ribbon(m, retrieval.RETRY_CAP, choice=choice_all, sorted_keys=True)
+    if rank == 0:
         ribbon = retrieval.RibbonSystem(epsilon, rseed, m, rwords)
         desc = recsplit.MphfDescriptor(n_keys, b, n, mode, cache_k, 0, leaf_g, key_prefix, bit_offsets, sw, bl, ribbon)
         desc.build_stats = {"build_seconds": time.perf_counter() - t0}

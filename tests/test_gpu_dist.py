@@ -40,6 +40,57 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _worker_small(rank, world, port, q, N, b, n):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["SHK_DEVICE"] = "0"
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_2308_09561_b200 import device as dev
+        from paper_2308_09561_b200 import dist as shdist
+        from paper_2308_09561_b200.keys import synthetic_hashed
+
+        hi, lo = synthetic_hashed(N, 31)
+        d_hi, d_lo = dev.DeviceBuffer.from_host(hi), dev.DeviceBuffer.from_host(lo)
+        desc, _ = shdist.build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, N, b, n, 1)
+        q.put((rank, desc.serialize() if desc is not None else None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(target, world, *args):
+    import torch.multiprocessing as tmp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    return out
+
+
+@pytest.mark.parametrize("world,N", [(2, 5000), (4, 30000)])
+def test_sharded_small_systems_match_oracle(world, N):
+    """Ribbons of one or few 8192-column chunks: some ranks own no columns
+    and forward the rows they receive."""
+    import oracle.host as OH
+    from paper_2308_09561_b200.keys import synthetic_hashed
+
+    hi, lo = synthetic_hashed(N, 31)
+    ref, _ = OH.build_descriptor(hi, lo, 300, 20, 1)
+    out = _spawn(_worker_small, world, N, 300, 20)
+    assert out[0] == ref
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_build_matches_reference(world):
     import torch.multiprocessing as tmp
