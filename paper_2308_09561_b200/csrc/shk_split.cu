@@ -37,9 +37,7 @@ __global__ void __launch_bounds__(256) split_kernel(ShkSplitLaunch a) {
     const ulonglong2* kp = keys + task.start;
     const uint32_t um = (uint32_t)m;
     if (!a.exact_evals && task.fanout >= 2 && task.fanout <= 4) {
-      int64_t seed = task.fanout == 2 ? split_search_fast<2>(kp, task, a.max_seed, lane)
-                     : task.fanout == 3 ? split_search_fast<3>(kp, task, a.max_seed, lane)
-                                        : split_search_fast<4>(kp, task, a.max_seed, lane);
+      int64_t seed = split_search_build(kp, task, a.max_seed, lane);
       if (lane == 0) {
         a.seeds[task.seed_slot] = seed;
         if (seed < 0 && a.exhausted) atomicOr(a.exhausted, 1);

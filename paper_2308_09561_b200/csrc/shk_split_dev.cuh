@@ -154,4 +154,96 @@ SHK_D int64_t split_search_fast(const ulonglong2* kp, const ShkSplitTask& task, 
   return -1;
 }
 
+// Nodes split into F EQUAL parts (the 4 x 40, 3 x 160 and 2 x 480 nodes of
+// C4's plans carry most of the split work).  With s = m / F the part of a key
+// is floor(floor(vh m / 2^32) / s) = floor(F vh / 2^32) exactly, so:
+//   F = 2: part = vh >> 31, counted with one LEA.HI;
+//   F = 3: part = umulhi(vh, 3); a += part, b += part >> 1 give
+//          #part2 = b, #part1 = a - 2b;
+//   F = 4 (m < 172): part = vh >> 30, one byte counter per part in one
+//          register (acc += 1 << 8 part), overflow of any byte past s by one
+//          add-and-mask.
+// Same seeds as split_search_fast (same exact per-part counts).
+#ifndef SHK_SPLIT_EQUAL
+// bit F: equal-part counters for fanout F.  Measured at C4 (tools/ab_bench.sh):
+// F = 4 saves ~3%; the F = 2 / F = 3 variants are neutral (F = 3's IMAD.HI
+// competes for the busy FMA pipe), so only F = 4 is on by default.
+#define SHK_SPLIT_EQUAL 0x10
+#endif
+SHK_D bool equal_split_ok(int F, int m) {
+  if (F < 2 || F > 4 || m % F || !((SHK_SPLIT_EQUAL >> F) & 1)) return false;
+  return F != 4 || m < 172;
+}
+
+template <int F>
+SHK_D int64_t split_search_equal(const ulonglong2* kp, const ShkSplitTask& task, uint64_t max_seed, int lane) {
+  const int m = task.m;
+  const int sz = m / F;
+  const uint32_t K4 = (uint32_t)(127 - sz) * 0x01010101u;  // byte b > sz <=> bit 7 of (b + 127 - sz)
+  for (uint64_t R = 0; R < max_seed; R += 32) {
+    const uint64_t s = R + lane;
+    const u2 x = seed_mixer_pre_d(s, TAG_SPLIT);
+    uint32_t a = 0, b = 0;
+    bool fail = !(s < max_seed);
+    bool all_failed = false;
+    int i = 0;
+    auto count = [&](uint32_t vh) {
+      if (F == 2) {
+        a += vh >> 31;
+      } else if (F == 3) {
+        const uint32_t p = __umulhi(vh, 3u);
+        a += p;
+        b += p >> 1;
+      } else {
+        a += 1u << ((vh >> 27) & 24u);
+      }
+    };
+    auto over = [&](int done) -> bool {
+      if (F == 2) return (done - (int)a > sz) || ((int)a > sz);
+      if (F == 3) {
+        const int c2 = (int)b, c1 = (int)a - 2 * c2;
+        return (done - c1 - c2 > sz) || (c1 > sz) || (c2 > sz);
+      }
+      return ((a + K4) & 0x80808080u) != 0u;
+    };
+    for (; i + 8 <= m; i += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const ulonglong2 k = load_key(kp + i + u);
+        count(remix_hi_pre_d(split64(k.x), split64(k.y), x));
+      }
+      fail |= over(i + 8);
+      if (__all_sync(FULL_WARP, fail)) {
+        all_failed = true;
+        break;
+      }
+    }
+    if (!all_failed) {
+      for (; i < m; ++i) {
+        const ulonglong2 k = load_key(kp + i);
+        count(remix_hi_pre_d(split64(k.x), split64(k.y), x));
+      }
+      fail |= over(m);
+    }
+    const unsigned ab = __ballot_sync(FULL_WARP, !fail);
+    if (ab) return (int64_t)(R + (uint64_t)(__ffs(ab) - 1));
+  }
+  return -1;
+}
+
+// Dispatch: equal-part nodes take the cheaper counters.
+SHK_D int64_t split_search_build(const ulonglong2* kp, const ShkSplitTask& task, uint64_t max_seed, int lane) {
+  const int F = task.fanout;
+  bool eq = SHK_SPLIT_EQUAL && equal_split_ok(F, task.m);
+  for (int j = 1; j < F && eq; ++j) eq = task.sizes[j] == task.sizes[0];
+  if (eq) {
+    return F == 2 ? split_search_equal<2>(kp, task, max_seed, lane)
+           : F == 3 ? split_search_equal<3>(kp, task, max_seed, lane)
+                    : split_search_equal<4>(kp, task, max_seed, lane);
+  }
+  return F == 2 ? split_search_fast<2>(kp, task, max_seed, lane)
+         : F == 3 ? split_search_fast<3>(kp, task, max_seed, lane)
+                  : split_search_fast<4>(kp, task, max_seed, lane);
+}
+
 }  // namespace shk

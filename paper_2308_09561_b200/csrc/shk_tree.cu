@@ -81,9 +81,7 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       for (int k = 0; k < 4; ++k) task.sizes[k] = nd.sizes[k];
       task.seed_slot = id;
       const ulonglong2* kp = t.keys + nd.start;
-      const int64_t seed = nd.fanout == 2 ? split_search_fast<2>(kp, task, t.max_seed, lane)
-                           : nd.fanout == 3 ? split_search_fast<3>(kp, task, t.max_seed, lane)
-                                            : split_search_fast<4>(kp, task, t.max_seed, lane);
+      const int64_t seed = split_search_build(kp, task, t.max_seed, lane);
       if (lane == 0) {
         t.seeds[id] = seed;
         if (seed < 0 && t.exhausted) atomicOr(t.exhausted, 1);
