@@ -38,7 +38,10 @@ namespace shk {
 #define SHK_RIBBON_CE 512
 #endif
 constexpr int CE = SHK_RIBBON_CE;
-constexpr int CB = 8192;  // back-substitution chunk (columns), multiple of CE and 64
+#ifndef SHK_RIBBON_CB
+#define SHK_RIBBON_CB 8192
+#endif
+constexpr int CB = SHK_RIBBON_CB;  // back-substitution chunk (columns), multiple of CE and 64
 
 struct RRow {
   uint64_t p0, p1;

@@ -201,7 +201,7 @@ def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8,
     b0, b1 = shard_range(nb, rank, world)
     leaf_g = recsplit.leaf_g_table(n)
     sizes = np.unique(np.diff(key_prefix[b0 : b1 + 1].astype(np.int64)))
-    plans = recsplit.plans_for_sizes(sizes, n, leaf_g)
+    plans = recsplit.packed_plans_for_sizes(sizes, n, leaf_g)
     ck = cache_k if mode == leaf_mod.MODE_ROTATE_CACHED else 0
     # Only this rank's bucket range gets permuted into leaf order, so choice
     # bits travel in the (rank-independent) bucket-sorted key order and rank
