@@ -64,3 +64,21 @@ def test_duplicates_and_parameters():
             recsplit.build(keys, b, n)
     with pytest.raises(InvalidParameterError):
         recsplit.build([], 10, 4)
+
+
+def test_large_build_is_a_bijection():
+    """10x the C4 key count (N = 1e8): no 32-bit index overflows anywhere on
+    the path; checked by size-independent properties (every key maps into
+    [0, N) exactly once, on the device; the descriptor round-trips)."""
+    from paper_2308_09561_b200 import device as dev
+
+    N = 100_000_000
+    hi, lo = synthetic_hashed(N, 2024)
+    d_hi, d_lo = dev.DeviceBuffer.from_host(hi), dev.DeviceBuffer.from_host(lo)
+    desc = recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, N, 2000, 40, 1)
+    assert desc.n_keys == N
+    ok, off = desc.device().verify(hi, lo)
+    assert ok and off == -1
+    blob = desc.serialize()
+    assert recsplit.MphfDescriptor.deserialize(blob).serialize() == blob
+    assert len(blob) * 8 / N < 1.7  # ~1.61 bits/key at n=40, b=2000
