@@ -198,17 +198,6 @@ SHK_D u2 remix_d(u2 k_hi, u2 k_lo, u2 x) {
   return mix64_d(z);
 }
 
-// Top bit of remix (split_bit): the final xor-shift by 31 cannot touch bit 63.
-SHK_D uint32_t remix_top_d(u2 k_hi, u2 k_lo, u2 x) {
-  u2 z;
-  z.lo = k_hi.lo ^ x.lo;
-  z.hi = k_hi.hi ^ x.hi;
-  z = mix64_d(z);
-  z.lo ^= k_lo.lo;
-  z.hi ^= k_lo.hi;
-  z = mulc<MUL1>(xorshr<30>(z));
-  return mulc_hi<MUL2>(xorshr<27>(z)) >> 31;
-}
 
 // ---------------------------------------------------------------------------
 // Pre-mixed keys.  The first xor-shift of remix distributes over the seed
@@ -248,7 +237,6 @@ SHK_D uint32_t remix_top_pre_d(u2 kp, u2 k_lo, u2 xp) {
   return mulc_hi<MUL2>(xorshr<27>(z)) >> 31;
 }
 
-SHK_D uint32_t range32(uint32_t vhi, uint32_t m) { return __umulhi(vhi, m); }
 
 SHK_D void leaf_pair_d(u2 v, uint32_t n, uint32_t nm1, uint32_t& h0, uint32_t& h1) {
   uint32_t a = __umulhi(v.hi, n);

@@ -88,7 +88,8 @@ SHK_D uint32_t remix_hi_pre_d(u2 kp, u2 k_lo, u2 xp) {
 // thresholds (thermometer counts g_j = #keys with part >= j).  Overflow is
 // checked once per 8 keys (it is monotone, so the seed verdict is exact);
 // the exact first-failing key index (the reference's `evals`) is not tracked
-// here — split_search_exact does that for the seam API.
+// here — the exact path of split_kernel (shk_split.cu) does that for the seam
+// API and the instrumented build.
 template <int F>
 SHK_D int64_t split_search_fast(const ulonglong2* kp, const ShkSplitTask& task, uint64_t max_seed, int lane) {
   const int m = task.m;
