@@ -450,14 +450,16 @@ __global__ void ribbon_query_kernel(const int64_t* starts, const uint64_t* p0, c
 // Overflow rows of a pass, regrouped by the chunk they reached.  Rows past the
 // local column range [0, M) (a column-sharded solve: they belong to the next
 // rank) are appended to `exp` in global columns (+ c0) instead.
-__global__ void ribbon_ovf_hist_kernel(const RRow* o, int64_t n, int64_t* hist, int64_t M) {
+__global__ void ribbon_ovf_hist_kernel(const RRow* o, const int64_t* np, int64_t* hist, int64_t M) {
+  const int64_t n = *np;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = o[i].s & S_MASK;
     if (s < M) atomicAdd((unsigned long long*)&hist[s / CE], 1ull);
   }
 }
-__global__ void ribbon_ovf_scatter_kernel(const RRow* o, int64_t n, int64_t* cursor, RRow* out, int64_t M,
+__global__ void ribbon_ovf_scatter_kernel(const RRow* o, const int64_t* np, int64_t* cursor, RRow* out, int64_t M,
                                           RRow* exp, int64_t* exp_count, int64_t c0) {
+  const int64_t n = *np;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     RRow r = o[i];
     const int64_t s = r.s & S_MASK;
@@ -621,56 +623,56 @@ int rib_clear(ShkRibbon* R, const RibLayout& L, int64_t M, cudaStream_t st) {
 // Regroup `n` rows at `src` (local columns) by elimination chunk into
 // rows2 / rowoff; rows past column M go to the export buffer (global
 // columns, + c0).
-int rib_regroup(const RibBufs& b, const RRow* src, int64_t n, int64_t M, int64_t c0, cudaStream_t st) {
+// Regroups the *np rows (count read on the device) at `src`.
+int rib_regroup(const RibBufs& b, const RRow* src, const int64_t* np, int64_t M, int64_t c0, cudaStream_t st) {
   const int64_t nch = (M + CE - 1) / CE;
   SHK_CUDA(cudaMemsetAsync(b.hist, 0, (size_t)(nch + 1) * 8, st));
-  ribbon_ovf_hist_kernel<<<grid_for(n), 256, 0, st>>>(src, n, b.hist, M);
+  ribbon_ovf_hist_kernel<<<148 * 4, 256, 0, st>>>(src, np, b.hist, M);
   SHK_LAUNCHED();
   int rc = shk_exclusive_scan_i64(b.hist, b.rowoff, nch, b.scan, shk_scan_scratch(nch), st);
   if (rc) return rc;
   SHK_CUDA(cudaMemcpyAsync(b.cursor, b.rowoff, (size_t)nch * 8, cudaMemcpyDeviceToDevice, st));
-  ribbon_ovf_scatter_kernel<<<grid_for(n), 256, 0, st>>>(src, n, b.cursor, b.rows2, M, b.exp, b.cnt + 2, c0);
+  ribbon_ovf_scatter_kernel<<<148 * 4, 256, 0, st>>>(src, np, b.cursor, b.rows2, M, b.exp, b.cnt + 2, c0);
   SHK_LAUNCHED();
   return 0;
 }
 
-// Elimination passes over `pending` chunk-grouped rows at `cur` (offsets in
+// Elimination passes over the chunk-grouped rows at `cur` (offsets in
 // rowoff) into the slot table of M local columns, until no row is left
 // inside the range.  first: the slot table is known empty.  Rows leaving the
 // range accumulate in the export buffer (count cnt[2]).  *bad: inconsistent.
-int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t pending, int64_t M, int64_t c0, int first,
-               int* bad_out, cudaStream_t st) {
+// Passes run in batches without host round trips (every count stays on the
+// device; a pass with nothing pending costs one near-empty launch); the host
+// checks for completion once per batch.
+int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c0, int first, int* bad_out,
+               cudaStream_t st) {
   RibBufs b(R, L);
   const int64_t nch = (M + CE - 1) / CE;
   int* bad = (int*)(b.cnt + 1);
   *bad_out = 0;
-  for (int pass = 0; pending > 0; ++pass) {
-    SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 8, st));
-    ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(cur, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt,
-                                                      bad, (first && pass == 0) ? 1 : 0);
-    SHK_LAUNCHED();
-    int64_t h[3];
-    SHK_CUDA(cudaMemcpyAsync(h, b.cnt, 24, cudaMemcpyDeviceToHost, st));
+  constexpr int BATCH = 6;
+  for (int pass = 0;;) {
+    for (int k = 0; k < BATCH; ++k, ++pass) {
+      SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 8, st));
+      ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(pass == 0 ? cur : b.rows2, b.rowoff, nch, M, b.sp0, b.sp1,
+                                                        b.occ, b.sb, b.ovf, b.cnt, bad, (first && pass == 0) ? 1 : 0);
+      SHK_LAUNCHED();
+      int rc = rib_regroup(b, b.ovf, b.cnt, M, c0, st);
+      if (rc) return rc;
+    }
+    int64_t h[2];
+    SHK_CUDA(cudaMemcpyAsync(h, b.cnt, 16, cudaMemcpyDeviceToHost, st));
     SHK_CUDA(cudaStreamSynchronize(st));
     if ((int)h[1]) {
       *bad_out = 1;
       return 0;
     }
-    const int64_t novf = h[0];
-    if (!novf) break;
-    int rc = rib_regroup(b, b.ovf, novf, M, c0, st);
-    if (rc) return rc;
-    int64_t e1 = 0;
-    SHK_CUDA(cudaMemcpyAsync(&e1, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
-    SHK_CUDA(cudaStreamSynchronize(st));
-    pending = novf - (e1 - h[2]);  // rows still inside the range
-    cur = b.rows2;
+    if (!h[0]) return 0;  // the last pass left nothing to regroup
     if (pass > 100000) {
       shk_set_error("ribbon elimination did not converge");
       return -1;
     }
   }
-  return 0;
 }
 
 // Back substitution of the M local columns given the 127 solution bits right
@@ -705,7 +707,8 @@ int solve_sorted(ShkRibbon* R, const RibLayout& L, int64_t N, int64_t m, uint64_
   int rc = rib_clear(R, L, m, st);
   if (rc) return rc;
   int bad = 0;
-  rc = rib_passes(R, L, RibBufs(R, L).rows, N, m, 0, 1, &bad, st);
+  (void)N;
+  rc = rib_passes(R, L, RibBufs(R, L).rows, m, 0, 1, &bad, st);
   if (rc) return rc;
   if (bad) {
     *consistent = 0;
@@ -785,11 +788,7 @@ int shk_ribbon_dist_begin(ShkRibbon* R, const uint64_t* keys_u64, const uint8_t*
   rc = gen_keyrows(R, L, reinterpret_cast<const ulonglong2*>(keys_u64), rhs, N, m, seed, c0, M, st);
   if (rc) return rc;
   RibBufs b(R, L);
-  const int64_t nch = (M + CE - 1) / CE;
-  int64_t nrows = 0;
-  SHK_CUDA(cudaMemcpyAsync(&nrows, b.rowoff + nch, 8, cudaMemcpyDeviceToHost, st));
-  SHK_CUDA(cudaStreamSynchronize(st));
-  rc = rib_passes(R, L, b.rows, nrows, M, c0, 1, bad, st);
+  rc = rib_passes(R, L, b.rows, M, c0, 1, bad, st);
   if (rc) return rc;
   SHK_CUDA(cudaMemcpyAsync(n_export, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
   SHK_CUDA(cudaStreamSynchronize(st));
@@ -819,13 +818,10 @@ int shk_ribbon_dist_import(ShkRibbon* R, const void* rows_in, int64_t n, int64_t
     SHK_CUDA(cudaMemcpyAsync(b.ovf, rows_in, (size_t)n * sizeof(RRow), cudaMemcpyHostToDevice, st));
     ribbon_rebase_kernel<<<grid_for(n), 256, 0, st>>>(b.ovf, n, R->dc0);
     SHK_LAUNCHED();
-    int64_t e0 = 0, e1 = 0;
-    SHK_CUDA(cudaMemcpyAsync(&e0, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
-    int rc = rib_regroup(b, b.ovf, n, R->dM, R->dc0, st);
+    SHK_CUDA(cudaMemcpyAsync(b.cnt + 3, &n, 8, cudaMemcpyHostToDevice, st));
+    int rc = rib_regroup(b, b.ovf, b.cnt + 3, R->dM, R->dc0, st);
     if (rc) return rc;
-    SHK_CUDA(cudaMemcpyAsync(&e1, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
-    SHK_CUDA(cudaStreamSynchronize(st));
-    rc = rib_passes(R, R->dL, b.rows2, n - (e1 - e0), R->dM, R->dc0, 0, bad, st);
+    rc = rib_passes(R, R->dL, b.rows2, R->dM, R->dc0, 0, bad, st);
     if (rc) return rc;
   }
   SHK_CUDA(cudaMemcpyAsync(n_export, b.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
