@@ -109,6 +109,79 @@ __global__ void bucket_sort_kernel(const ulonglong2* in, const int64_t* prefix, 
   }
 }
 
+// Same result by distribution: a bucket's hi words are uniform 64-bit values,
+// so one counting pass on their top 12 bits (4096 bins, ~0.5 keys per bin at
+// b = 2000) places every key within a few slots of its sorted position; each
+// bin (a contiguous output range) is then insertion-sorted by (hi, lo) by one
+// thread, which also flags equal codes (they share a bin).  O(cnt) work and
+// three block barriers per bucket instead of the bitonic network's 66.
+#ifndef SHK_BUCKET_SORT
+#define SHK_BUCKET_SORT 2  // 2: distribution sort (bins); 1: bitonic network (+ O(m^2) rank past 16384 keys)
+#endif
+constexpr int SORT_BINS = 4096;
+__global__ void __launch_bounds__(256) bucket_sort_bins_kernel(const ulonglong2* in, const int64_t* prefix, int64_t nb,
+                                                               ulonglong2* out, int* dup_flag) {
+  __shared__ int cur[SORT_BINS];
+  __shared__ int wsum[8];
+  for (int64_t bu = blockIdx.x; bu < nb; bu += gridDim.x) {
+    const int64_t s0 = prefix[bu];
+    const int cnt = (int)(prefix[bu + 1] - s0);
+    if (cnt == 0) continue;
+    for (int i = threadIdx.x; i < SORT_BINS; i += blockDim.x) cur[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) atomicAdd(&cur[(int)(in[s0 + i].x >> 52)], 1);
+    __syncthreads();
+    // exclusive scan of the 4096 counts: 16 per thread, then across threads
+    {
+      const int t = threadIdx.x, base = t * (SORT_BINS / 256);
+      int loc[SORT_BINS / 256], run = 0;
+#pragma unroll
+      for (int k = 0; k < SORT_BINS / 256; ++k) {
+        loc[k] = run;
+        run += cur[base + k];
+      }
+      // block scan of the per-thread totals (warp shuffles + 8 warp sums)
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL_WARP, incl, o);
+        if ((t & 31) >= o) incl += v;
+      }
+      if ((t & 31) == 31) wsum[t >> 5] = incl;
+      __syncthreads();
+      int woff = 0;
+      for (int w = 0; w < (t >> 5); ++w) woff += wsum[w];
+      const int excl = woff + incl - run;
+#pragma unroll
+      for (int k = 0; k < SORT_BINS / 256; ++k) cur[base + k] = excl + loc[k];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const ulonglong2 k = in[s0 + i];
+      out[s0 + atomicAdd(&cur[(int)(k.x >> 52)], 1)] = k;
+    }
+    __syncthreads();
+    // cur[bin] is now the end of the bin; its start is the previous bin's end
+    for (int bin = threadIdx.x; bin < SORT_BINS; bin += blockDim.x) {
+      const int a = bin ? cur[bin - 1] : 0, e = cur[bin];
+      for (int x = a + 1; x < e; ++x) {
+        const ulonglong2 v = out[s0 + x];
+        int y = x - 1;
+        while (y >= a && key_less(v, out[s0 + y])) {
+          out[s0 + y + 1] = out[s0 + y];
+          --y;
+        }
+        out[s0 + y + 1] = v;
+      }
+      for (int x = a + 1; x < e; ++x) {
+        const ulonglong2 p = out[s0 + x - 1], q = out[s0 + x];
+        if (p.x == q.x && p.y == q.y) atomicOr(dup_flag, 1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Fallback for buckets larger than the shared-memory sort: rank by counting
 // (O(cnt^2) per bucket, correct for any size; only reached with huge b).
 __global__ void bucket_rank_kernel(const ulonglong2* in, int64_t s0, int cnt, ulonglong2* out, int* dup_flag) {
@@ -232,7 +305,12 @@ int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nb,
   int P = 1;
   while (P < maxb) P <<= 1;
   if (P < 2) P = 2;
-  if (maxb <= 16384) {
+  if (SHK_BUCKET_SORT == 2) {
+    // distribution sort: any bucket size (bins hold cnt / 4096 keys on average)
+    int64_t grid = nb < 148 * 8 ? nb : 148 * 8;
+    bucket_sort_bins_kernel<<<(unsigned)grid, 256, 0, st>>>(unsorted, prefix, nb, out, dup_flag);
+    SHK_LAUNCHED();
+  } else if (maxb <= 16384) {
     size_t sm = (size_t)P * 10;
     if (sm > 48 * 1024)
       SHK_CUDA(cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
