@@ -373,23 +373,36 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
       }
       // exact checks, warp-cooperative, in lexicographic (base, r) order
       const int win_r = warp_first_accept(sm.edges[warp], passmask, n, lane, sm.chk[warp]);
+      // per-lane counters (each < 2^8: 32-bit single-instruction warp sums)
       const uint32_t nb = (uint32_t)n - na;
-      const uint64_t my_ev = valid ? (uint64_t)nb + (ws ? (uint64_t)n + na : 0) : 0;
-      const uint64_t my_aev = (valid && ws) ? na : 0;
-      const uint64_t my_pass = __popcll(passmask);
-      uint64_t my_pass_le = my_pass;
-      if (win_r >= 0) my_pass_le = __popcll(passmask & ((win_r == 63) ? ~0ull : ((2ull << win_r) - 1)));
+      const uint32_t my_ev = valid ? nb + (ws ? (uint32_t)n + na : 0u) : 0u;
+      const uint32_t my_aev = (valid && ws) ? na : 0u;
+      const uint32_t my_pass = __popcll(passmask);
       unsigned ab = __ballot_sync(FULL_WARP, win_r >= 0);
       int wl = ab ? __ffs(ab) - 1 : 32;
-      // sums over lanes <= wl (winner) and over all lanes
-      uint64_t c_ev_le = (lane <= wl) ? my_ev : 0;
-      uint64_t c_aev_le = (lane <= wl) ? my_aev : 0;
-      uint64_t c_pass_le = (lane < wl) ? my_pass : (lane == wl ? my_pass_le : 0);
-      uint64_t t_ev = warp_sum(my_ev), t_aev = warp_sum(my_aev), t_pass = warp_sum(my_pass);
-      c_ev_le = warp_sum(c_ev_le);
-      c_aev_le = warp_sum(c_aev_le);
-      c_pass_le = warp_sum(c_pass_le);
+      // sums over all lanes, and over lanes <= wl (the winner) when there is one
+      const uint32_t t_ev = __reduce_add_sync(FULL_WARP, my_ev), t_aev = __reduce_add_sync(FULL_WARP, my_aev),
+                     t_pass = __reduce_add_sync(FULL_WARP, my_pass);
+      uint32_t c_ev_le = t_ev, c_aev_le = t_aev, c_pass_le = t_pass;
+      if (ab) {
+        uint32_t my_pass_le = my_pass;
+        if (win_r >= 0) my_pass_le = __popcll(passmask & ((win_r == 63) ? ~0ull : ((2ull << win_r) - 1)));
+        c_ev_le = __reduce_add_sync(FULL_WARP, lane <= wl ? my_ev : 0u);
+        c_aev_le = __reduce_add_sync(FULL_WARP, lane <= wl ? my_aev : 0u);
+        c_pass_le = __reduce_add_sync(FULL_WARP, lane < wl ? my_pass : (lane == wl ? my_pass_le : 0u));
+      }
       int wr = __shfl_sync(FULL_WARP, win_r, wl & 31);
+      if (TW == 1) {  // one-warp team: the round's result stays in registers
+        passes += c_pass_le;
+        evals += c_ev_le;
+        aev += c_aev_le;
+        if (ab) {
+          const uint64_t qq = (R + (uint64_t)wl) * (uint64_t)n + (uint64_t)wr;
+          q = (qq >= a.max_seed) ? -1 : (int64_t)qq;
+          break;
+        }
+        continue;
+      }
       if (lane == 0) {
         sm.slot_win[par][warp] = ab ? (int64_t)(R + (uint64_t)warp * 32 + wl) : -1;
         sm.slot_r[par][warp] = wr;
