@@ -15,6 +15,7 @@
 #include "shk_common.cuh"
 #include "shk_kernels.h"
 #include "shk_rice.cuh"
+#include "shk_split_dev.cuh"  // remix_hi_pre_d: the routing hashes only need the high word
 
 namespace shk {
 
@@ -50,8 +51,7 @@ struct QueryMixers {
 SHK_D uint64_t rib_choice(const ShkQueryDesc& d, const QueryMixers& mx, u2 kp, u2 kl) {
   if (!d.rib_m) return 0;
   const uint64_t span = (uint64_t)(d.rib_m - RIBBON_W + 1);
-  const u2 vs = remix_pre_d(kp, kl, mx.rstart);
-  const int64_t s = (int64_t)(((uint64_t)vs.hi * span) >> 32);
+  const int64_t s = (int64_t)(((uint64_t)remix_hi_pre_d(kp, kl, mx.rstart) * span) >> 32);
   const u2 a = remix_pre_d(kp, kl, mx.rpat0);
   const u2 b = remix_pre_d(kp, kl, mx.rpat1);
   const uint64_t pat0 = join64(a.lo | 1u, a.hi), pat1 = join64(b.lo, b.hi);
@@ -109,8 +109,7 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
   mx.rpat1 = seed_mixer_pre_d(d.rib_seed, TAG_RPAT1);
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (int64_t)gridDim.x * blockDim.x) {
     const u2 kp = split64(premix_hi(hi[t])), kl = split64(lo[t]);
-    const u2 vb = remix_pre_d(kp, kl, mx.bucket);
-    const int64_t bucket = (int64_t)__umulhi(vb.hi, (uint32_t)d.nbuckets);
+    const int64_t bucket = (int64_t)__umulhi(remix_hi_pre_d(kp, kl, mx.bucket), (uint32_t)d.nbuckets);
     const uint4 b0 = __ldg(d.bucketq + 2 * bucket), b1 = __ldg(d.bucketq + 2 * bucket + 1);
     const uint64_t kp0 = join64(b0.x, b0.y);
     uint64_t offset = 0;
@@ -122,8 +121,7 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
       uint4 p = __ldg(pq);
       while (!(p.x & 0x8000u)) {  // split node
         if (idx >= bad) break;
-        const u2 v = remix_pre_d(kp, kl, split64(__ldg(nv + idx)));
-        const uint32_t r = __umulhi(v.hi, p.x & 0x7FFFu);
+        const uint32_t r = __umulhi(remix_hi_pre_d(kp, kl, split64(__ldg(nv + idx))), p.x & 0x7FFFu);
         const uint32_t part = (uint32_t)(r >= (p.x >> 16)) + (uint32_t)(r >= (p.y & 0xFFFFu)) + (uint32_t)(r >= (p.y >> 16));
         const uint32_t sh = 16 * part;
         offset += (uint32_t)(join64(p.x & 0xFFFF0000u, p.y) >> sh) & 0xFFFFu;  // lane `part` of (0, b1, b2, b3)
