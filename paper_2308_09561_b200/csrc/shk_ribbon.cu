@@ -283,9 +283,12 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
 __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
                                                            const uint64_t* sp1, const uint32_t* occ,
                                                            const uint32_t* sbit, uint4* forms, uint4* coef) {
-  __shared__ uint4 tpw[256];
-  __shared__ uint32_t tcoef[256][4];
-  __shared__ uint32_t tsb[8];
+  // double-buffered 256-column tiles: while the warps walk tile k, each
+  // thread's global loads for tile k+1 are in flight, and the finished
+  // coefficients of tile k-1 are written out; one barrier per tile
+  __shared__ uint4 tpw[2][256];
+  __shared__ uint32_t tcoef[2][256][4];
+  __shared__ uint32_t tsb[2][8];
   const int64_t c = blockIdx.x;
   if (c >= nbchunks) return;
   const int tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
@@ -301,38 +304,80 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
     W3 = (u >> 5) == 3 ? b : 0u;
   }
   const bool konst = (u == 127);
-  // process columns e-1 down to s0 in tiles of 256 (tile start aligned to 256)
-  int64_t col = e - 1;
-  while (col >= s0) {
-    const int64_t tstart = (col / 256) * 256 > s0 ? (col / 256) * 256 : s0;
-    const int ntile = (int)(col - tstart + 1);
-    for (int j = tid; j < ntile; j += 128) {
-      const int64_t cc = tstart + j;
-      const bool o = (occ[cc >> 5] >> (cc & 31)) & 1u;
-      const uint64_t a0 = o ? sp0[cc] : 0ull, a1 = o ? sp1[cc] : 0ull;
-      // p >> 1 as four 32-bit words
-      tpw[j] = make_uint4((uint32_t)(a0 >> 1) | ((uint32_t)(a0 >> 32) << 31),
-                          (uint32_t)(a0 >> 33) | ((uint32_t)a1 << 31),
-                          (uint32_t)(a1 >> 1) | ((uint32_t)(a1 >> 32) << 31), (uint32_t)(a1 >> 33));
+  // tiles from the top: tile 0 is [tstart(e-1), e), tile k+1 ends where tile k starts
+  auto tile_start = [&](int64_t col) { return (col / 256) * 256 > s0 ? (col / 256) * 256 : s0; };
+  // per-thread prefetch registers: columns tid and tid + 128 of a tile
+  uint64_t pa0[2], pa1[2];
+  uint32_t psb = 0;
+  auto prefetch = [&](int64_t ts, int nt) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = tid + 128 * h;
+      pa0[h] = pa1[h] = 0ull;
+      if (j < nt) {
+        const int64_t cc = ts + j;
+        if ((occ[cc >> 5] >> (cc & 31)) & 1u) {
+          pa0[h] = sp0[cc];
+          pa1[h] = sp1[cc];
+        }
+      }
     }
-    if (tid < 8) tsb[tid] = (tid * 32 < ntile) ? sbit[tstart / 32 + tid] : 0u;  // rhs bits (0 on free columns)
-    __syncthreads();
-    for (int j = ntile - 1; j >= 0; --j) {
-      const uint4 p = tpw[j];
+    if (tid < 8) psb = (tid * 32 < nt) ? sbit[ts / 32 + tid] : 0u;  // rhs bits (0 on free columns)
+  };
+  auto stash = [&](int buf, int nt) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = tid + 128 * h;
+      if (j < nt) {
+        const uint64_t a0 = pa0[h], a1 = pa1[h];
+        // p >> 1 as four 32-bit words
+        tpw[buf][j] = make_uint4((uint32_t)(a0 >> 1) | ((uint32_t)(a0 >> 32) << 31),
+                                 (uint32_t)(a0 >> 33) | ((uint32_t)a1 << 31),
+                                 (uint32_t)(a1 >> 1) | ((uint32_t)(a1 >> 32) << 31), (uint32_t)(a1 >> 33));
+      }
+    }
+    if (tid < 8) tsb[buf][tid] = psb;
+  };
+  int64_t col = e - 1;
+  int64_t ts = tile_start(col);
+  int nt = (int)(col - ts + 1);
+  prefetch(ts, nt);
+  stash(0, nt);
+  __syncthreads();
+  int64_t prev_ts = -1;
+  int prev_nt = 0, buf = 0;
+  for (int k = 0;; ++k) {
+    buf = k & 1;
+    const int64_t nts = ts - 1 >= s0 ? tile_start(ts - 1) : -1;
+    const int nnt = nts >= 0 ? (int)(ts - nts) : 0;
+    if (nnt) prefetch(nts, nnt);
+    for (int j = nt - 1; j >= 0; --j) {
+      const uint4 p = tpw[buf][j];
       uint32_t nb = __popc((W0 & p.x) ^ (W1 & p.y) ^ (W2 & p.z) ^ (W3 & p.w)) & 1u;
-      if (konst) nb ^= (tsb[j >> 5] >> (j & 31)) & 1u;
+      if (konst) nb ^= (tsb[buf][j >> 5] >> (j & 31)) & 1u;
       const uint32_t bal = __ballot_sync(FULL_WARP, nb);
-      if (lane == 0) tcoef[j][q] = bal;
+      if (lane == 0) tcoef[buf][j][q] = bal;
       W3 = __funnelshift_l(W2, W3, 1);
       W2 = __funnelshift_l(W1, W2, 1);
       W1 = __funnelshift_l(W0, W1, 1);
       W0 = (W0 << 1) | nb;
     }
+    if (nnt) stash(buf ^ 1, nnt);
+    // coefficients of the previous tile (complete since the last barrier)
+    if (prev_nt)
+      for (int j = tid; j < prev_nt; j += 128)
+        coef[prev_ts + j] =
+            make_uint4(tcoef[buf ^ 1][j][0], tcoef[buf ^ 1][j][1], tcoef[buf ^ 1][j][2], tcoef[buf ^ 1][j][3]);
     __syncthreads();
-    for (int j = tid; j < ntile; j += 128)
-      coef[tstart + j] = make_uint4(tcoef[j][0], tcoef[j][1], tcoef[j][2], tcoef[j][3]);
-    col = tstart - 1;
+    prev_ts = ts;
+    prev_nt = nt;
+    if (!nnt) break;
+    ts = nts;
+    nt = nnt;
   }
+  // the last tile's coefficients (complete after the final barrier)
+  for (int j = tid; j < prev_nt; j += 128)
+    coef[prev_ts + j] = make_uint4(tcoef[buf][j][0], tcoef[buf][j][1], tcoef[buf][j][2], tcoef[buf][j][3]);
   forms[c * 128 + u] = make_uint4(W0, W1, W2, W3);
 }
 
