@@ -212,19 +212,20 @@ int shk_build_placements(shk_build* b, int64_t* out /* [N] host */);
  * ribbon solution does not depend on row order. */
 #define SHK_RIBBON_SORTED_KEYS 4
 int shk_build_set_keep_sorted(shk_build* b, int on);
-int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out /* [k1-k0] host */);
+int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out /* [k1-k0] */,
+                            int flags /* SHK_DEVICE: out is a device pointer (no sync) */);
 /* Column-sharded ribbon (SURVEY.md §8(e) option B) over the kept sorted keys:
  * this rank owns columns [c0, c1) (multiples of 8192 except c1 = m).
  * begin eliminates the rows that start in the range (choice_sorted: all N
- * choice bits, host, sorted order); rows whose pivot leaves the range are
+ * choice bits in sorted order, host or, with flags & SHK_DEVICE, device); rows whose pivot leaves the range are
  * exported (24 bytes each: p0, p1, start | rhs << 62, global columns) for the
  * right neighbour, which imports them (and may export further).  *bad = 1:
  * the system is inconsistent (next seed).  When no rank exports, backsub runs
  * right to left across ranks: y_in = the right neighbour's first 127 solution
  * bits (4 words, zero for the last range), y_out = this range's, words_out =
  * its (c1 - c0 + 63) / 64 solution words (host). */
-int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int64_t m, uint64_t seed, int64_t c0,
-                            int64_t c1, int64_t* n_export, int* bad);
+int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int flags, int64_t m, uint64_t seed,
+                            int64_t c0, int64_t c1, int64_t* n_export, int* bad);
 int shk_build_dribbon_exports(shk_build* b, void* rows_out, int64_t n);
 int shk_build_dribbon_import(shk_build* b, const void* rows_in, int64_t n, int64_t* n_export, int* bad);
 int shk_build_dribbon_backsub(shk_build* b, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out);

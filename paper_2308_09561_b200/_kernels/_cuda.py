@@ -538,19 +538,30 @@ class GpuBuild:
         """Keep the bucket-sorted keys (before run) for choice_sorted/ribbon(sorted_keys=True)."""
         check(_L().shk_build_set_keep_sorted(self.handle, 1 if on else 0))
 
-    def choice_sorted(self, k0, k1):
-        """Choice bits of build positions [k0, k1) in bucket-sorted key order."""
+    def choice_sorted(self, k0, k1, dev_ptr=None):
+        """Choice bits of build positions [k0, k1) in bucket-sorted key order
+        (host array, or written to the device pointer dev_ptr)."""
+        if dev_ptr is not None:
+            check(_L().shk_build_choice_sorted(self.handle, int(k0), int(k1), int(dev_ptr), SHK_DEVICE),
+                  "choice_sorted")
+            return None
         out = np.zeros(max(int(k1) - int(k0), 0), dtype=np.uint8)
-        check(_L().shk_build_choice_sorted(self.handle, int(k0), int(k1), ptr(out) if len(out) else None),
+        check(_L().shk_build_choice_sorted(self.handle, int(k0), int(k1), ptr(out) if len(out) else None, 0),
               "choice_sorted")
         return out
 
     # column-sharded ribbon (dist.ribbon_sharded drives the exchange)
     def dribbon_begin(self, choice_sorted, m, seed, c0, c1):
-        ch = np.ascontiguousarray(choice_sorted, dtype=np.uint8)
+        """choice_sorted: all N choice bits in sorted order, a host array or
+        an int device pointer."""
+        if isinstance(choice_sorted, int):
+            cp, fl = choice_sorted, SHK_DEVICE
+        else:
+            ch = np.ascontiguousarray(choice_sorted, dtype=np.uint8)
+            cp, fl = ptr(ch), 0
         nexp = ctypes.c_int64(0)
         bad = ctypes.c_int(0)
-        check(_L().shk_build_dribbon_begin(self.handle, ptr(ch), int(m), int(seed), int(c0), int(c1),
+        check(_L().shk_build_dribbon_begin(self.handle, cp, fl, int(m), int(seed), int(c0), int(c1),
                                            ctypes.byref(nexp), ctypes.byref(bad)), "ribbon (sharded)")
         return int(nexp.value), bool(bad.value)
 
@@ -577,9 +588,12 @@ class GpuBuild:
     def ribbon(self, m, max_tries=64, choice=None, sorted_keys=False):
         words = np.zeros((int(m) + 63) // 64, dtype=np.uint64)
         seed = ctypes.c_uint64(0)
-        ch = None if choice is None else np.ascontiguousarray(choice, dtype=np.uint8)
         flags = 4 if sorted_keys else 0  # SHK_RIBBON_SORTED_KEYS
-        check(_L().shk_build_ribbon(self.handle, ptr(ch), flags, int(m), int(max_tries), ctypes.byref(seed),
+        if isinstance(choice, int):  # device pointer
+            ch, flags = choice, flags | SHK_DEVICE
+        else:
+            ch = None if choice is None else ptr(np.ascontiguousarray(choice, dtype=np.uint8))
+        check(_L().shk_build_ribbon(self.handle, ch, flags, int(m), int(max_tries), ctypes.byref(seed),
                                     ptr(words)), "ribbon")
         return int(seed.value), words
 

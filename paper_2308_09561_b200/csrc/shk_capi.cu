@@ -1349,8 +1349,8 @@ int shk_build_set_keep_sorted(shk_build* b, int on) {
 }
 
 // ---- column-sharded ribbon over the build's sorted keys ---------------------
-int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int64_t m, uint64_t seed, int64_t c0,
-                            int64_t c1, int64_t* n_export, int* bad) {
+int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int flags, int64_t m, uint64_t seed,
+                            int64_t c0, int64_t c1, int64_t* n_export, int* bad) {
   shk_ctx* c = b->c;
   if (!b->sorted.p) {
     shk_set_error("sorted keys were not kept (shk_build_set_keep_sorted)");
@@ -1359,7 +1359,10 @@ int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int64_t 
   if (!b->drhs.p) {
     RC(b->drhs.alloc((size_t)b->N));
   }
-  RC(h2d(c, b->drhs.p, choice_sorted, (size_t)b->N));
+  if (flags & SHK_DEVICE)
+    SHK_CUDA(cudaMemcpyAsync(b->drhs.p, choice_sorted, (size_t)b->N, cudaMemcpyDeviceToDevice, c->stream));
+  else
+    RC(h2d(c, b->drhs.p, choice_sorted, (size_t)b->N));
   b->dcols = c1 - c0;
   b->mark(6);  // ribbon phase: from here to the end of backsub (exchanges included)
   return shk_ribbon_dist_begin(c->rib, b->sorted.as<uint64_t>(), b->drhs.as<uint8_t>(), b->N, m, seed, c0, c1,
@@ -1387,7 +1390,7 @@ int shk_build_dribbon_backsub(shk_build* b, const uint32_t* y_in, uint32_t* y_ou
   return 0;
 }
 
-int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out) {
+int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out, int flags) {
   shk_ctx* c = b->c;
   if (!b->sorted.p || !b->ran) {
     shk_set_error("choice_sorted needs shk_build_set_keep_sorted before shk_build_run");
@@ -1398,6 +1401,11 @@ int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out) 
     return SHK_INVALID;
   }
   if (k1 == k0) return 0;
+  if (flags & SHK_DEVICE) {  // straight into the caller's (collective) buffer
+    RC(shk_launch_choice_sorted(b->keys.as<uint64_t>(), b->sorted.as<uint64_t>(), b->prefix.as<int64_t>(), b->nb,
+                                b->choice.as<uint8_t>(), k0, k1, out, c->stream));
+    return csync(c);
+  }
   DBuf d(c);
   RC(d.alloc((size_t)(k1 - k0)));
   RC(shk_launch_choice_sorted(b->keys.as<uint64_t>(), b->sorted.as<uint64_t>(), b->prefix.as<int64_t>(), b->nb,

@@ -84,20 +84,51 @@ def allgather_arrays(arr: np.ndarray, device=None) -> List[np.ndarray]:
     return [o[:s].cpu().numpy().view(arr.dtype) for o, s in zip(outs, sizes)]
 
 
-def exchange_and_merge(words, bit_len, rel_offsets, choice_slice, device=None):
-    """The one exchange step: gather every rank's stream pieces and choice
-    bits; every rank returns (stream words, bit_len, bit_offsets, choice)."""
+def exchange_streams(words, bit_len, rel_offsets, device=None):
+    """Gather every rank's Rice stream piece (~0.7 MB in all at C4); every
+    rank returns (stream words, bit_len, bit_offsets)."""
     meta = np.asarray([int(bit_len)], dtype=np.int64)
     all_meta = allgather_arrays(meta, device)
     all_words = allgather_arrays(np.asarray(words, dtype=np.uint64), device)
     all_rel = allgather_arrays(np.asarray(rel_offsets, dtype=np.uint64), device)
+    parts = [(w, int(m[0]), r) for w, m, r in zip(all_words, all_meta, all_rel)]
+    return merge_streams(parts)
+
+
+def exchange_and_merge(words, bit_len, rel_offsets, choice_slice, device=None):
+    """Host exchange (gloo): stream pieces plus packed choice bits; every rank
+    returns (stream words, bit_len, bit_offsets, choice)."""
+    sw, bl, bo = exchange_streams(words, bit_len, rel_offsets, device)
     packed = np.packbits(np.asarray(choice_slice, dtype=np.uint8), bitorder="little")
     all_choice = allgather_arrays(packed, device)
     lens = allgather_arrays(np.asarray([len(choice_slice)], dtype=np.int64), device)
-    parts = [(w, int(m[0]), r) for w, m, r in zip(all_words, all_meta, all_rel)]
-    sw, bl, bo = merge_streams(parts)
     choice = np.concatenate([np.unpackbits(c, bitorder="little")[: int(n[0])] for c, n in zip(all_choice, lens)])
     return sw, bl, bo, choice
+
+
+def exchange_choice_device(gb, key_prefix, nb, device):
+    """NCCL exchange of the choice bits, device to device: one N-byte buffer in
+    bucket-sorted key order, each rank's kernel writes its own key range in
+    place, then one broadcast per rank range fills the rest.  Returns the
+    tensor (every rank holds all N bits)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n_keys = int(key_prefix[-1])
+    full = torch.empty(max(n_keys, 1), dtype=torch.uint8, device=device)
+    ranges = []
+    for r in range(world):
+        b0, b1 = shard_range(nb, r, world)
+        ranges.append((int(key_prefix[b0]), int(key_prefix[b1])))
+    k0, k1 = ranges[rank]
+    if k1 > k0:
+        gb.choice_sorted(k0, k1, dev_ptr=full.data_ptr() + k0)  # synchronises the library stream
+    for r, (a, z) in enumerate(ranges):
+        if z > a:
+            dist.broadcast(full[a:z], src=r)
+    torch.cuda.current_stream(device).synchronize()  # the library stream reads it next
+    return full
 
 
 import os
@@ -211,8 +242,13 @@ def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8,
                 leaf_mod.MAX_SEED)
     words, bit_len, bo = gb.stream()
     rel = bo[: b1 - b0 + 1]
-    choice = gb.choice_sorted(int(key_prefix[b0]), int(key_prefix[b1]))
-    sw, bl, bit_offsets, choice_all = exchange_and_merge(words, bit_len, rel, choice, device)
+    if device is not None and getattr(device, "type", "cpu") == "cuda":  # NCCL: choice bits stay on the devices
+        choice_t = exchange_choice_device(gb, key_prefix, nb, device)
+        sw, bl, bit_offsets = exchange_streams(words, bit_len, rel, device)
+        choice_all = choice_t.data_ptr()
+    else:
+        choice = gb.choice_sorted(int(key_prefix[b0]), int(key_prefix[b1]))
+        sw, bl, bit_offsets, choice_all = exchange_and_merge(words, bit_len, rel, choice, device)
     desc = None
     m = retrieval._columns(n_keys, epsilon)
     if RIBBON_SHARDED:

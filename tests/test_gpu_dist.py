@@ -60,6 +60,38 @@ def _worker_small(rank, world, port, q, N, b, n):
         dist.destroy_process_group()
 
 
+def _worker_nccl(rank, world, port, q, ribbon_sharded):
+    """One rank over NCCL: the device-side choice exchange (broadcast into one
+    device buffer) and the device-pointer ribbon entry points."""
+    import os
+
+    os.environ["SHK_DEVICE"] = "0"
+    os.environ["SHK_RIBBON_SHARDED"] = ribbon_sharded
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_2308_09561_b200 import device as dev
+        from paper_2308_09561_b200 import dist as shdist
+        from paper_2308_09561_b200 import workloads as W
+
+        keys = W.build_keys(2)
+        blob = np.frombuffer(np.ascontiguousarray(keys, dtype="<u8").tobytes(), dtype=np.uint8)
+        pinned = dev.PinnedBuffer.from_array(blob)
+        desc, prof = shdist.build_blob_sharded(pinned.array, 8, 500, 24, 1, device=torch.device("cuda", 0))
+        q.put((rank, hashlib.sha256(desc.serialize()).hexdigest() if desc is not None else None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ribbon_sharded", ["1", "0"])
+def test_nccl_device_exchange_matches_reference(ribbon_sharded):
+    out = _spawn(_worker_nccl, 1, ribbon_sharded)
+    assert out[0] == golden("c2.json")["desc_sha"]
+
+
 def _spawn(target, world, *args):
     import torch.multiprocessing as tmp
 
