@@ -6,7 +6,8 @@
 // seeds of skipped left subtrees included, ~38 decodes per query at n=40,
 // b=2000).  Here the whole stream is decoded ONCE per descriptor (one thread
 // per bucket decodes the bucket's nodes in order) into a per-node value table
-// (split node: its seed's pre-mixed TAG_SPLIT mixer; leaf: its seed), so a
+// (split node: its seed's pre-mixed TAG_SPLIT mixer; leaf: its seed, as
+// base << 6 | r in the rotate modes), so a
 // query decodes nothing: it reads the values on its root-to-leaf path.
 // Outputs are identical; so are the FormatError cases: a query fails iff the
 // reference's sequential decode would overrun before reaching the key's leaf,
@@ -34,8 +35,17 @@ __global__ void node_index_kernel(ShkQueryDesc d, uint64_t* node_val, int32_t* b
           bad = (int32_t)j;
           break;
         }
-        node_val[nb + j] =
-            d.pn_kind[p0 + j] == 0 ? premix_hi(seed_mixer((uint64_t)v, TAG_SPLIT)) : (uint64_t)v;
+        uint64_t val;
+        if (d.pn_kind[p0 + j] == 0) {
+          val = premix_hi(seed_mixer((uint64_t)v, TAG_SPLIT));
+        } else if (d.mode != 0 && d.pn_m[p0 + j] > 1) {  // rotate: q = base * m + r stored as base << 6 | r
+          const uint64_t m = (uint64_t)d.pn_m[p0 + j], base = (uint64_t)v / m;
+          // (a base too large to pack keeps q, flagged by bit 63)
+          val = (base >> 57) ? ((uint64_t)v | (1ull << 63)) : ((base << 6) | ((uint64_t)v - base * m));
+        } else {
+          val = (uint64_t)v;
+        }
+        node_val[nb + j] = val;
       }
     }
     bucket_bad[bu] = bad;
@@ -73,7 +83,8 @@ SHK_D uint64_t rib_choice(const ShkQueryDesc& d, const QueryMixers& mx, u2 kp, u
 }
 
 // Cell of a key inside its leaf (leaf_cell, _core.pyx:751-767) from the
-// pre-mixed key and the leaf's encoded seed q.
+// pre-mixed key and the leaf's node value q (plain: the seed; rotate: the
+// seed's base << 6 | rotation, split once by node_index_kernel).
 SHK_D uint32_t leaf_cell_pre(u2 kp, u2 kl, uint64_t q, uint32_t n, int mode, int64_t cache_k, int choice) {
   if (n <= 1) return 0;  // leaf_pair gives (0, 0)
   uint32_t h0, h1;
@@ -81,14 +92,11 @@ SHK_D uint32_t leaf_cell_pre(u2 kp, u2 kl, uint64_t q, uint32_t n, int mode, int
     leaf_pair_d(remix_pre_d(kp, kl, seed_mixer_pre_d(q, TAG_LEAF)), n, n - 1, h0, h1);
     return choice ? h1 : h0;
   }
-  uint64_t base, r;
-  if (q >> 32) {
+  uint64_t base = q >> 6, r = q & 63;  // node_index_kernel's packing
+  if (q >> 63) {
+    q &= ~(1ull << 63);
     base = q / n;
     r = q - base * n;
-  } else {
-    const uint32_t b32 = (uint32_t)q / n;
-    base = b32;
-    r = (uint32_t)q - b32 * n;
   }
   const uint64_t sa = (mode == 2 && cache_k && n > 32) ? base - base % (uint64_t)cache_k : base;
   if (remix_top_pre_d(kp, kl, seed_mixer_pre_d(sa, TAG_SPLITBIT)) == 0) {
@@ -111,6 +119,9 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
     const u2 kp = split64(premix_hi(hi[t])), kl = split64(lo[t]);
     const int64_t bucket = (int64_t)__umulhi(remix_hi_pre_d(kp, kl, mx.bucket), (uint32_t)d.nbuckets);
     const uint4 b0 = __ldg(d.bucketq + 2 * bucket), b1 = __ldg(d.bucketq + 2 * bucket + 1);
+    // the ribbon bit depends on the key alone: its three word loads are issued
+    // here and stay in flight across the split-path walk
+    const int choice = (int)rib_choice(d, mx, kp, kl);
     const uint64_t kp0 = join64(b0.x, b0.y);
     uint64_t offset = 0;
     if (b0.z > 0) {  // msize
@@ -135,7 +146,6 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
       }
       const uint64_t q = __ldg(nv + idx);
       const uint32_t mleaf = p.x & 0x7FFFu;
-      const int choice = (int)rib_choice(d, mx, kp, kl);
       offset += leaf_cell_pre(kp, kl, q, mleaf, d.mode, d.cache_k, choice);
     }
     uint64_t o = kp0 + offset;
