@@ -129,22 +129,26 @@ __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64
       const uint64_t* nv = d.node_val + join64(b1.x, b1.y);
       const uint4* pq = d.planq + b1.z;
       int idx = 0;
+      // a node's plan record and value are loaded together (both depend on
+      // idx only): one dependent load round trip per level
       uint4 p = __ldg(pq);
+      uint64_t x = __ldg(nv);
       while (!(p.x & 0x8000u)) {  // split node
         if (idx >= bad) break;
-        const uint32_t r = __umulhi(remix_hi_pre_d(kp, kl, split64(__ldg(nv + idx))), p.x & 0x7FFFu);
+        const uint32_t r = __umulhi(remix_hi_pre_d(kp, kl, split64(x)), p.x & 0x7FFFu);
         const uint32_t part = (uint32_t)(r >= (p.x >> 16)) + (uint32_t)(r >= (p.y & 0xFFFFu)) + (uint32_t)(r >= (p.y >> 16));
         const uint32_t sh = 16 * part;
         offset += (uint32_t)(join64(p.x & 0xFFFF0000u, p.y) >> sh) & 0xFFFFu;  // lane `part` of (0, b1, b2, b3)
         idx = (int)((uint32_t)(join64(p.z, p.w) >> sh) & 0xFFFFu);          // lane `part` of (c0 .. c3)
         p = __ldg(pq + idx);
+        x = __ldg(nv + idx);
       }
       if (idx >= bad) {
         atomicOr(err, 1);
         out[t] = 0;
         continue;
       }
-      const uint64_t q = __ldg(nv + idx);
+      const uint64_t q = x;
       const uint32_t mleaf = p.x & 0x7FFFu;
       offset += leaf_cell_pre(kp, kl, q, mleaf, d.mode, d.cache_k, choice);
     }
