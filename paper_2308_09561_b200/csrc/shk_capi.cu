@@ -1515,6 +1515,10 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
     shk_set_error("stream bit length exceeds the word array");
     return SHK_INVALID;
   }
+  if (rib_m != 0 && (rib_m < shk::RIBBON_W || rib_m > (1ll << 40))) {
+    shk_set_error("invalid retrieval column count %lld", (long long)rib_m);
+    return SHK_INVALID;
+  }
   PlanSet S;
   RC(load_plans(plans, S));
   shk_qdesc* q = new shk_qdesc(c);
@@ -1571,23 +1575,32 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
     e[2] = u16(child[4 * j]) | (u16(child[4 * j + 1]) << 16);
     e[3] = u16(child[4 * j + 2]) | (u16(child[4 * j + 3]) << 16);
   }
-  std::vector<uint32_t> bucketq((size_t)nbuckets * 8, 0u);
+  // one uint4 per bucket (a query's first random load is a single 16-byte
+  // gather): {kp0 lo, kp0 hi8 | node_base hi8 << 8 | bad << 16, node_base lo,
+  // first plan node or 0xFFFFFFFF for an empty bucket}; bad = the first
+  // undecodable plan-local node (0xFFFF: none; plan nodes are < 65535), set on
+  // the device by node_index_kernel.  Key prefixes and node counts < 2^40.
+  if (key_prefix[nbuckets] >= (1ull << 40) || nn >= (1ll << 40) || S.plan_off.back() >= 0xFFFFFFFFll) {
+    shk_set_error("descriptor too large for the query tables");
+    return SHK_INVALID;
+  }
+  std::vector<uint32_t> bucketq((size_t)nbuckets * 4, 0u);
   for (int64_t bu = 0; bu < nbuckets; ++bu) {
-    uint32_t* e = &bucketq[8 * bu];
-    const uint64_t kp0 = key_prefix[bu];
+    uint32_t* e = &bucketq[4 * bu];
+    const uint64_t kp0 = key_prefix[bu], nb0 = (uint64_t)nbase[bu];
     e[0] = (uint32_t)kp0;
-    e[1] = (uint32_t)(kp0 >> 32);
-    e[2] = (uint32_t)(key_prefix[bu + 1] - kp0);
-    e[3] = 0x7FFFFFFFu;  // first bad node, set on the device by node_index_kernel
-    e[4] = (uint32_t)nbase[bu];
-    e[5] = (uint32_t)((uint64_t)nbase[bu] >> 32);
-    e[6] = bplan[bu] >= 0 ? (uint32_t)S.plan_off[bplan[bu]] : 0u;
+    e[1] = (uint32_t)(kp0 >> 32) | ((uint32_t)(nb0 >> 32) << 8) | (0xFFFFu << 16);
+    e[2] = (uint32_t)nb0;
+    e[3] = bplan[bu] >= 0 ? (uint32_t)S.plan_off[bplan[bu]] : 0xFFFFFFFFu;
   }
   const int64_t rnw = rib_nwords > 0 ? rib_nwords : 0;
   RC(q->kp.alloc((size_t)(nbuckets + 1) * 8));
   RC(q->bo.alloc((size_t)(nbuckets + 1) * 8));
   RC(q->sw.alloc((size_t)(stream_nwords + 1) * 8));
-  RC(q->rw.alloc((size_t)(rnw + 1) * 8));
+  // zero padding past the words: the query's paired loads may read up to
+  // word ceil(m / 64) + 1 (the reference reads zeros out of range)
+  const int64_t rnw_alloc = (rnw > (rib_m + 63) / 64 ? rnw : (rib_m + 63) / 64) + 2;
+  RC(q->rw.alloc((size_t)rnw_alloc * 8));
   RC(q->bplan.alloc((size_t)nbuckets * 4));
   RC(q->nbase.alloc((size_t)(nbuckets + 1) * 8));
   RC(q->npos.alloc((size_t)(nn + 1) * 8));
@@ -1600,14 +1613,14 @@ int shk_qdesc_create(shk_ctx* c, int64_t n_keys, int64_t nbuckets, int mode, int
   RC(q->fan.alloc(np * 4 + 4));
   RC(q->poff.alloc(S.plan_off.size() * 8 + 8));
   RC(q->planq.alloc(np * 16 + 16));
-  RC(q->bucketq.alloc((size_t)nbuckets * 32 + 32));
+  RC(q->bucketq.alloc((size_t)nbuckets * 16 + 16));
   RC(h2d(c, q->planq.p, planq.data(), np * 16));
-  RC(h2d(c, q->bucketq.p, bucketq.data(), (size_t)nbuckets * 32));
+  RC(h2d(c, q->bucketq.p, bucketq.data(), (size_t)nbuckets * 16));
   RC(h2d(c, q->kp.p, key_prefix, (size_t)(nbuckets + 1) * 8));
   RC(h2d(c, q->bo.p, bit_offsets, (size_t)(nbuckets + 1) * 8));
   SHK_CUDA(cudaMemsetAsync(q->sw.p, 0, (size_t)(stream_nwords + 1) * 8, c->stream));
   RC(h2d(c, q->sw.p, stream_words, (size_t)stream_nwords * 8));
-  SHK_CUDA(cudaMemsetAsync(q->rw.p, 0, (size_t)(rnw + 1) * 8, c->stream));
+  SHK_CUDA(cudaMemsetAsync(q->rw.p, 0, (size_t)rnw_alloc * 8, c->stream));
   if (rnw) RC(h2d(c, q->rw.p, rib_words, (size_t)rnw * 8));
   RC(h2d(c, q->bplan.p, bplan.data(), (size_t)nbuckets * 4));
   RC(h2d(c, q->nbase.p, nbase.data(), (size_t)(nbuckets + 1) * 8));

@@ -176,7 +176,8 @@ struct ShkQueryDesc {
   const int64_t* node_base;     // [nb]  first global node of the bucket
   const uint64_t* node_val;     // [total nodes] decoded node: split -> premixed seed mixer, leaf -> seed
   // query-side packed tables:
-  //   bucketq[2b..2b+1]: {kp0 lo, kp0 hi, msize, bad} {node_base lo, node_base hi, plan first node, 0}
+  //   bucketq[b]: {kp0 lo, kp0 hi8 | node_base hi8 << 8 | bad16 << 16, node_base lo,
+  //                plan first node (0xFFFFFFFF: empty bucket)}
   //   planq[j]: {m | leaf << 15 | b1 << 16, b2 | b3 << 16, c0 | c1 << 16, c2 | c3 << 16}
   //             (b_k cumulative part bounds, 0xFFFF past the fanout; c_k plan-local children)
   const uint4* bucketq;

@@ -49,7 +49,8 @@ __global__ void node_index_kernel(ShkQueryDesc d, uint64_t* node_val, int32_t* b
       }
     }
     bucket_bad[bu] = bad;
-    reinterpret_cast<uint32_t*>(const_cast<uint4*>(d.bucketq))[8 * bu + 3] = (uint32_t)bad;
+    uint32_t* bq = reinterpret_cast<uint32_t*>(const_cast<uint4*>(d.bucketq)) + 4 * bu + 1;
+    *bq = (*bq & 0xFFFFu) | ((bad < 0xFFFF ? (uint32_t)bad : 0xFFFFu) << 16);
   }
 }
 
@@ -67,10 +68,15 @@ SHK_D uint64_t rib_choice(const ShkQueryDesc& d, const QueryMixers& mx, u2 kp, u
   const uint64_t pat0 = join64(a.lo | 1u, a.hi), pat1 = join64(b.lo, b.hi);
   const int64_t wi = s >> 6;
   const int sh = (int)(s & 63);
-  const int64_t nw = d.rib_nwords;
-  const uint64_t w0 = wi < nw ? d.rib_words[wi] : 0;
-  const uint64_t w1 = wi + 1 < nw ? d.rib_words[wi + 1] : 0;
-  const uint64_t w2 = wi + 2 < nw ? d.rib_words[wi + 2] : 0;
+  // words wi .. wi + 2 in two gathers: the aligned pair holding wi + 1, and
+  // the remaining word (the table is padded with a zero word; words past m
+  // are zero, as the reference's out-of-range reads)
+  const int64_t odd = wi & 1;
+  const ulonglong2 pr = __ldg(reinterpret_cast<const ulonglong2*>(d.rib_words + ((wi + 1) & ~1ll)));
+  const uint64_t ws = __ldg(d.rib_words + (odd ? wi : wi + 2));
+  const uint64_t w0 = odd ? ws : pr.x;
+  const uint64_t w1 = odd ? pr.x : pr.y;
+  const uint64_t w2 = odd ? pr.y : ws;
   uint64_t v0, v1;
   if (sh) {
     v0 = (w0 >> sh) | (w1 << (64 - sh));
@@ -108,56 +114,98 @@ SHK_D uint32_t leaf_cell_pre(u2 kp, u2 kl, uint64_t q, uint32_t n, int mode, int
   return h >= n ? h - n : h;
 }
 
+// SHK_QUERY_ILP queries per thread (t, t + stride, ...), stepped together
+// through their split paths.  The kernel is co-bound by the L1 gather rate
+// (one random 8-16 byte gather per level) and integer issue; two interleaved
+// queries (58 registers, half the resident warps) measured 3% slower than one
+// (profiles/r01_ncu_full_query_v15.csv), so the default is 1.
+#ifndef SHK_QUERY_ILP
+#define SHK_QUERY_ILP 1
+#endif
 __global__ void __launch_bounds__(256) query_kernel(ShkQueryDesc d, const uint64_t* hi, const uint64_t* lo, int64_t Q,
                                                     uint64_t* out, int* err, int clamp) {
+  constexpr int U = SHK_QUERY_ILP;
   QueryMixers mx;
   mx.bucket = seed_mixer_pre_d(0, TAG_BUCKET);
   mx.rstart = seed_mixer_pre_d(d.rib_seed, TAG_RSTART);
   mx.rpat0 = seed_mixer_pre_d(d.rib_seed, TAG_RPAT0);
   mx.rpat1 = seed_mixer_pre_d(d.rib_seed, TAG_RPAT1);
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (int64_t)gridDim.x * blockDim.x) {
-    const u2 kp = split64(premix_hi(hi[t])), kl = split64(lo[t]);
-    const int64_t bucket = (int64_t)__umulhi(remix_hi_pre_d(kp, kl, mx.bucket), (uint32_t)d.nbuckets);
-    const uint4 b0 = __ldg(d.bucketq + 2 * bucket), b1 = __ldg(d.bucketq + 2 * bucket + 1);
-    // the ribbon bit depends on the key alone: its three word loads are issued
-    // here and stay in flight across the split-path walk
-    const int choice = (int)rib_choice(d, mx, kp, kl);
-    const uint64_t kp0 = join64(b0.x, b0.y);
-    uint64_t offset = 0;
-    if (b0.z > 0) {  // msize
-      const int bad = (int)b0.w;
-      const uint64_t* nv = d.node_val + join64(b1.x, b1.y);
-      const uint4* pq = d.planq + b1.z;
-      int idx = 0;
-      // a node's plan record and value are loaded together (both depend on
-      // idx only): one dependent load round trip per level
-      uint4 p = __ldg(pq);
-      uint64_t x = __ldg(nv);
-      while (!(p.x & 0x8000u)) {  // split node
-        if (idx >= bad) break;
-        const uint32_t r = __umulhi(remix_hi_pre_d(kp, kl, split64(x)), p.x & 0x7FFFu);
-        const uint32_t part = (uint32_t)(r >= (p.x >> 16)) + (uint32_t)(r >= (p.y & 0xFFFFu)) + (uint32_t)(r >= (p.y >> 16));
-        const uint32_t sh = 16 * part;
-        offset += (uint32_t)(join64(p.x & 0xFFFF0000u, p.y) >> sh) & 0xFFFFu;  // lane `part` of (0, b1, b2, b3)
-        idx = (int)((uint32_t)(join64(p.z, p.w) >> sh) & 0xFFFFu);          // lane `part` of (c0 .. c3)
-        p = __ldg(pq + idx);
-        x = __ldg(nv + idx);
-      }
-      if (idx >= bad) {
-        atomicOr(err, 1);
-        out[t] = 0;
-        continue;
-      }
-      const uint64_t q = x;
-      const uint32_t mleaf = p.x & 0x7FFFu;
-      offset += leaf_cell_pre(kp, kl, q, mleaf, d.mode, d.cache_k, choice);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < Q; t0 += U * stride) {
+    u2 kp[U], kl[U];
+    uint64_t kp0[U], offset[U], x[U];
+    uint4 p[U];
+    const uint64_t* nv[U];
+    const uint4* pq[U];
+    int idx[U], bad[U], choice[U];
+    bool walk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = t0 + u * stride;
+      const bool in = t < Q;
+      kp[u] = split64(premix_hi(in ? hi[t] : 0ull));
+      kl[u] = split64(in ? lo[t] : 0ull);
     }
-    uint64_t o = kp0 + offset;
-    if (clamp) {
-      const uint64_t mx = d.n_keys > 0 ? (uint64_t)(d.n_keys - 1) : 0;
-      if (o > mx) o = mx;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t bucket = (int64_t)__umulhi(remix_hi_pre_d(kp[u], kl[u], mx.bucket), (uint32_t)d.nbuckets);
+      const uint4 bq = __ldg(d.bucketq + bucket);
+      kp0[u] = join64(bq.x, bq.y & 0xFFu);
+      bad[u] = (int)(bq.y >> 16);  // 0xFFFF: none (plan-local ids are smaller)
+      walk[u] = bq.w != 0xFFFFFFFFu;
+      nv[u] = d.node_val + join64(bq.z, (bq.y >> 8) & 0xFFu);
+      pq[u] = d.planq + (walk[u] ? bq.w : 0u);
     }
-    out[t] = o;
+    // the ribbon bit depends on the key alone: its word loads stay in flight
+    // across the split-path walk
+#pragma unroll
+    for (int u = 0; u < U; ++u) choice[u] = (int)rib_choice(d, mx, kp[u], kl[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      offset[u] = 0;
+      idx[u] = 0;
+      if (walk[u]) {  // a node's plan record and value depend on idx only: loaded together
+        p[u] = __ldg(pq[u]);
+        x[u] = __ldg(nv[u]);
+      }
+    }
+    bool any = true;
+    while (any) {
+      any = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (walk[u] && !(p[u].x & 0x8000u) && idx[u] < bad[u]) {  // split node
+          const uint32_t r = __umulhi(remix_hi_pre_d(kp[u], kl[u], split64(x[u])), p[u].x & 0x7FFFu);
+          const uint32_t part = (uint32_t)(r >= (p[u].x >> 16)) + (uint32_t)(r >= (p[u].y & 0xFFFFu)) +
+                                (uint32_t)(r >= (p[u].y >> 16));
+          const uint32_t sh = 16 * part;
+          offset[u] += (uint32_t)(join64(p[u].x & 0xFFFF0000u, p[u].y) >> sh) & 0xFFFFu;  // lane `part` of (0, b1..b3)
+          idx[u] = (int)((uint32_t)(join64(p[u].z, p[u].w) >> sh) & 0xFFFFu);            // lane `part` of (c0..c3)
+          p[u] = __ldg(pq[u] + idx[u]);
+          x[u] = __ldg(nv[u] + idx[u]);
+          any = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = t0 + u * stride;
+      if (t >= Q) continue;
+      if (walk[u]) {
+        if (idx[u] >= bad[u]) {
+          atomicOr(err, 1);
+          out[t] = 0;
+          continue;
+        }
+        offset[u] += leaf_cell_pre(kp[u], kl[u], x[u], p[u].x & 0x7FFFu, d.mode, d.cache_k, choice[u]);
+      }
+      uint64_t o = kp0[u] + offset[u];
+      if (clamp) {
+        const uint64_t mxk = d.n_keys > 0 ? (uint64_t)(d.n_keys - 1) : 0;
+        if (o > mxk) o = mxk;
+      }
+      out[t] = o;
+    }
   }
 }
 
@@ -194,7 +242,7 @@ int shk_launch_node_index(const ShkQueryDesc& d, uint64_t* node_val, int32_t* bu
 int shk_launch_query(const ShkQueryDesc& d, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out, int* err,
                      int clamp, cudaStream_t st) {
   if (Q <= 0) return 0;
-  int64_t g = (Q + 255) / 256;
+  int64_t g = ((Q + SHK_QUERY_ILP - 1) / SHK_QUERY_ILP + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   query_kernel<<<(unsigned)g, 256, 0, st>>>(d, hi, lo, Q, out, err, clamp);
   SHK_LAUNCHED();

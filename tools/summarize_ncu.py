@@ -24,6 +24,8 @@ FULL_METRICS = [
     "launch__registers_per_thread",
     "launch__occupancy_limit_registers",
     "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__t_sector_hit_rate.pct",
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
     "lts__t_sector_hit_rate.pct",
