@@ -229,6 +229,15 @@ int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int flag
 int shk_build_dribbon_exports(shk_build* b, void* rows_out, int64_t n);
 int shk_build_dribbon_import(shk_build* b, const void* rows_in, int64_t n, int64_t* n_export, int* bad);
 int shk_build_dribbon_backsub(shk_build* b, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out);
+/* Parallel form of the right-to-left pass: map computes this range's
+ * back-substitution forms and returns its boundary map (map_out: 128 rows of
+ * 4 words; row j < 127 = the range's first 127 solution bits when the 127
+ * bits right of it are e_j, row 127 = when they are zero; the map is affine
+ * over GF(2)).  Every rank composes the maps of the ranks to its right into
+ * its own y_in (no serial hand-off), then finish runs the chain and the
+ * final map (words_out as in backsub). */
+int shk_build_dribbon_map(shk_build* b, uint32_t* map_out /* [128][4] host */);
+int shk_build_dribbon_finish(shk_build* b, const uint32_t* y_in, uint64_t* words_out);
 int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int64_t m, int max_tries,
                      uint64_t* seed_out, uint64_t* words_out /* [ceil(m/64)] host */);
 /* Device time of the last phases (CUDA events on the context stream), ms:

@@ -585,6 +585,19 @@ class GpuBuild:
         check(_L().shk_build_dribbon_backsub(self.handle, ptr(y_in), ptr(y_out), ptr(words)), "ribbon backsub")
         return y_out, words
 
+    def dribbon_map(self):
+        """This range's boundary map, uint32[128, 4] (rows j < 127: image of
+        e_j, row 127: image of 0)."""
+        out = np.zeros((128, 4), dtype=np.uint32)
+        check(_L().shk_build_dribbon_map(self.handle, ptr(out)), "ribbon map")
+        return out
+
+    def dribbon_finish(self, y_in, ncols):
+        y_in = np.ascontiguousarray(y_in, dtype=np.uint32)
+        words = np.zeros((int(ncols) + 63) // 64, dtype=np.uint64)
+        check(_L().shk_build_dribbon_finish(self.handle, ptr(y_in), ptr(words)), "ribbon finish")
+        return words
+
     def ribbon(self, m, max_tries=64, choice=None, sorted_keys=False):
         words = np.zeros((int(m) + 63) // 64, dtype=np.uint64)
         seed = ctypes.c_uint64(0)

@@ -102,6 +102,8 @@ _SIGS = {
     "shk_build_set_keep_sorted": (_I, [_P, _I]),
     "shk_build_choice_sorted": (_I, [_P, _I64, _I64, _P, _I]),
     "shk_build_dribbon_begin": (_I, [_P, _P, _I, _I64, _U64, _I64, _I64, _P, _P]),
+    "shk_build_dribbon_map": (_I, [_P, _P]),
+    "shk_build_dribbon_finish": (_I, [_P, _P, _P]),
     "shk_build_dribbon_exports": (_I, [_P, _P, _I64]),
     "shk_build_dribbon_import": (_I, [_P, _P, _I64, _P, _P]),
     "shk_build_dribbon_backsub": (_I, [_P, _P, _P, _P]),

@@ -1390,6 +1390,23 @@ int shk_build_dribbon_backsub(shk_build* b, const uint32_t* y_in, uint32_t* y_ou
   return 0;
 }
 
+int shk_build_dribbon_map(shk_build* b, uint32_t* map_out) {
+  return shk_ribbon_dist_map(b->c->rib, map_out, b->c->stream);
+}
+
+int shk_build_dribbon_finish(shk_build* b, const uint32_t* y_in, uint64_t* words_out) {
+  shk_ctx* c = b->c;
+  const int64_t nw = (b->dcols + 63) / 64;
+  DBuf tw(c);
+  RC(tw.alloc((size_t)nw * 8));
+  RC(shk_ribbon_dist_finish(c->rib, y_in, tw.as<uint64_t>(), c->stream));
+  RC(d2h(c, words_out, tw.p, (size_t)nw * 8));
+  b->mark(7);
+  RC(csync(c));
+  b->phase_ms[4] = b->span(6, 7);
+  return 0;
+}
+
 int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out, int flags) {
   shk_ctx* c = b->c;
   if (!b->sorted.p || !b->ran) {

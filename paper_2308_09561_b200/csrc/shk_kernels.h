@@ -150,6 +150,8 @@ int shk_ribbon_dist_import(ShkRibbon* r, const void* rows_in, int64_t n, int64_t
                            cudaStream_t st);
 int shk_ribbon_dist_backsub(ShkRibbon* r, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out,
                             cudaStream_t st);
+int shk_ribbon_dist_map(ShkRibbon* r, uint32_t* map_out, cudaStream_t st);
+int shk_ribbon_dist_finish(ShkRibbon* r, const uint32_t* y_in, uint64_t* words_out, cudaStream_t st);
 int shk_launch_ribbon_rows(const uint64_t* hi, const uint64_t* lo, int stride, int64_t N, int64_t m, uint64_t seed,
                            int64_t* starts, uint64_t* p0, uint64_t* p1, cudaStream_t st);
 // Split-hash part index of every key (split_parts seam).

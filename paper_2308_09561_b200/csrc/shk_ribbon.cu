@@ -388,6 +388,10 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
 // y_io (device, one uint4): in = the 127 solution bits right of the last chunk
 // (zero at the end of the system; the right neighbour's first bits in a
 // column-sharded solve), out = the first 127 solution bits of chunk 0.
+// Map mode (ysel == nullptr, one block per basis vector): block j < 127 runs
+// the chain from y = e_j, block 127 from y = 0, and writes its result to
+// y_io[j]: the range's first 127 bits as an affine function of the 127 bits
+// right of it (the column-sharded solve composes these maps across ranks).
 __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, const uint4* forms, uint4* ysel,
                                                           uint4* y_io) {
   // D-deep cp.async ring: the forms of chunk c - D are in flight while chunk
@@ -395,7 +399,14 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
   constexpr int D = 8;
   __shared__ uint4 ring[D][128];
   const int lane = threadIdx.x;
-  uint4 y = *y_io;
+  const int j = blockIdx.x;
+  uint4 y;
+  if (ysel) {
+    y = *y_io;
+  } else {
+    const uint32_t b = (j < 127) ? 1u << (j & 31) : 0u;
+    y = make_uint4((j >> 5) == 0 ? b : 0u, (j >> 5) == 1 ? b : 0u, (j >> 5) == 2 ? b : 0u, (j >> 5) == 3 ? b : 0u);
+  }
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     const int64_t cc = nbchunks - 1 - k;
@@ -435,7 +446,7 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
     slot = (slot + 1 == D) ? 0 : slot + 1;
     const uint32_t s0 = __ballot_sync(FULL_WARP, sel[0]), s1 = __ballot_sync(FULL_WARP, sel[1]);
     const uint32_t s2 = __ballot_sync(FULL_WARP, sel[2]), s3 = __ballot_sync(FULL_WARP, sel[3]);
-    if (lane == 0) ysel[c] = make_uint4(s0, s1, s2, s3);
+    if (lane == 0 && ysel) ysel[c] = make_uint4(s0, s1, s2, s3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       acc0 ^= __shfl_xor_sync(FULL_WARP, acc0, o);
@@ -445,7 +456,7 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
     }
     y = make_uint4(acc0, acc1, acc2, acc3 & 0x7FFFFFFFu);  // 127 bits
   }
-  if (lane == 0) *y_io = y;
+  if (lane == 0) y_io[ysel ? 0 : j] = y;
 }
 
 // Final back substitution, a parallel map: sol[col] = parity(coef[col] &
@@ -534,7 +545,7 @@ using namespace shk;
 // Byte offsets of the solver's buffers inside ShkRibbon::buf.
 struct RibLayout {
   size_t off_rows, off_rows2, off_ovf, off_exp, off_hist, off_rowoff, off_cursor, off_sp0, off_sp1, off_occ, off_sb,
-      off_forms, off_coef, off_y, off_yio, off_cnt, off_scan, total;
+      off_forms, off_coef, off_y, off_yio, off_ymap, off_cnt, off_scan, total;
 };
 
 struct ShkRibbon {
@@ -598,6 +609,8 @@ RibLayout layout(int64_t N, int64_t m) {
   o += al((size_t)nbc * 16);
   L.off_yio = o;
   o += 256;
+  L.off_ymap = o;
+  o += 128 * 16;
   L.off_cnt = o;
   o += 256;
   L.off_scan = o;
@@ -629,7 +642,7 @@ struct RibBufs {
   int64_t *hist, *rowoff, *cursor, *cnt;  // cnt: [0] ovf count, [1] inconsistent flag (int), [2] export count
   uint64_t *sp0, *sp1;
   uint32_t *occ, *sb;
-  uint4 *forms, *coef, *yb, *yio;
+  uint4 *forms, *coef, *yb, *yio, *ymap;
   void* scan;
   RibBufs(ShkRibbon* R, const RibLayout& L) {
     char* B = (char*)R->buf;
@@ -649,6 +662,7 @@ struct RibBufs {
     coef = (uint4*)(B + L.off_coef);
     yb = (uint4*)(B + L.off_y);
     yio = (uint4*)(B + L.off_yio);
+    ymap = (uint4*)(B + L.off_ymap);
     scan = B + L.off_scan;
   }
 };
@@ -723,14 +737,21 @@ int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c
 // Back substitution of the M local columns given the 127 solution bits right
 // of them (y_in, host); y_out (host, may be null) gets the range's first 127
 // bits; words_out (device) gets ceil(M/64) solution words.
-int rib_backsub(ShkRibbon* R, const RibLayout& L, int64_t M, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out,
-                cudaStream_t st) {
+int rib_forms(ShkRibbon* R, const RibLayout& L, int64_t M, cudaStream_t st) {
+  RibBufs b(R, L);
+  const int64_t nbc = (M + CB - 1) / CB;
+  ribbon_forms_kernel<<<(unsigned)nbc, 128, 0, st>>>(M, nbc, b.sp0, b.sp1, b.occ, b.sb, b.forms, b.coef);
+  SHK_LAUNCHED();
+  return 0;
+}
+
+// forms must be current; chain from y_in, final map.
+int rib_chain_final(ShkRibbon* R, const RibLayout& L, int64_t M, const uint32_t* y_in, uint32_t* y_out,
+                    uint64_t* words_out, cudaStream_t st) {
   RibBufs b(R, L);
   const int64_t nbc = (M + CB - 1) / CB;
   const uint4 y0 = y_in ? make_uint4(y_in[0], y_in[1], y_in[2], y_in[3]) : make_uint4(0, 0, 0, 0);
   SHK_CUDA(cudaMemcpyAsync(b.yio, &y0, 16, cudaMemcpyHostToDevice, st));
-  ribbon_forms_kernel<<<(unsigned)nbc, 128, 0, st>>>(M, nbc, b.sp0, b.sp1, b.occ, b.sb, b.forms, b.coef);
-  SHK_LAUNCHED();
   ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, b.forms, b.yb, b.yio);
   SHK_LAUNCHED();
   const int64_t nwords = (M + 63) / 64;
@@ -743,6 +764,13 @@ int rib_backsub(ShkRibbon* R, const RibLayout& L, int64_t M, const uint32_t* y_i
     SHK_CUDA(cudaStreamSynchronize(st));
   }
   return 0;
+}
+
+int rib_backsub(ShkRibbon* R, const RibLayout& L, int64_t M, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out,
+                cudaStream_t st) {
+  int rc = rib_forms(R, L, M, st);
+  if (rc) return rc;
+  return rib_chain_final(R, L, M, y_in, y_out, words_out, st);
 }
 
 // Shared single-system driver once rows are in r->buf at off_rows with the
@@ -880,6 +908,26 @@ int shk_ribbon_dist_import(ShkRibbon* R, const void* rows_in, int64_t n, int64_t
 int shk_ribbon_dist_backsub(ShkRibbon* R, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out,
                             cudaStream_t st) {
   return rib_backsub(R, R->dL, R->dM, y_in, y_out, words_out, st);
+}
+
+// Parallel back substitution across ranks, step 1: this range's forms and
+// its boundary map (map_out, host, [128][4] words: rows j < 127 = the first
+// 127 bits for y_in = e_j, row 127 = for y_in = 0).
+int shk_ribbon_dist_map(ShkRibbon* R, uint32_t* map_out, cudaStream_t st) {
+  RibBufs b(R, R->dL);
+  int rc = rib_forms(R, R->dL, R->dM, st);
+  if (rc) return rc;
+  const int64_t nbc = (R->dM + CB - 1) / CB;
+  ribbon_chain_kernel<<<128, 32, 0, st>>>(nbc, b.forms, nullptr, b.ymap);
+  SHK_LAUNCHED();
+  SHK_CUDA(cudaMemcpyAsync(map_out, b.ymap, 128 * 16, cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// Step 2: chain from the composed y_in and the final map (forms from step 1).
+int shk_ribbon_dist_finish(ShkRibbon* R, const uint32_t* y_in, uint64_t* words_out, cudaStream_t st) {
+  return rib_chain_final(R, R->dL, R->dM, y_in, nullptr, words_out, st);
 }
 
 int shk_ribbon_solve_rows(ShkRibbon* R, const int64_t* starts, const uint64_t* p0, const uint64_t* p1,

@@ -145,14 +145,22 @@ def column_range(m: int, rank: int, world: int, cb: int = RIBBON_CB) -> Tuple[in
     return min(a * cb, m), min(b * cb, m)
 
 
-def _bcast_u32(arr, src, device=None):
-    import torch
-    import torch.distributed as dist
+def identity_map() -> np.ndarray:
+    """Boundary map of an empty column range (y passes through)."""
+    m = np.zeros((128, 4), dtype=np.uint32)
+    for j in range(127):
+        m[j, j >> 5] = np.uint32(1 << (j & 31))
+    return m
 
-    t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint32).view(np.int32).copy())
-    t = t.to(device) if device is not None else t
-    dist.broadcast(t, src)
-    return t.cpu().numpy().view(np.uint32)
+
+def apply_map(mp: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Image of the 127-bit boundary y (4 uint32 words) under an affine map
+    (rows j < 127: image of e_j; row 127: image of 0)."""
+    bits = np.unpackbits(np.ascontiguousarray(y, dtype="<u4").view(np.uint8), bitorder="little")[:127].astype(bool)
+    out = mp[127].copy()
+    if bits.any():
+        out ^= np.bitwise_xor.reduce(mp[:127][bits] ^ mp[127], axis=0)
+    return out
 
 
 def ribbon_sharded(gb, choice_sorted, m, max_tries, device=None):
@@ -197,14 +205,16 @@ def ribbon_sharded(gb, choice_sorted, m, max_tries, device=None):
             pass
         if reduce(bad, dist.ReduceOp.MAX):
             continue
+        # back substitution, all ranks at once: each range's first 127
+        # solution bits are an affine GF(2) function of the 127 bits right of
+        # it; one all-gather of those maps lets every rank compose its own
+        # right boundary instead of waiting for a right-to-left hand-off
+        my_map = gb.dribbon_map() if own else identity_map()
+        maps = [m_.reshape(128, 4) for m_ in allgather_arrays(my_map.reshape(-1), device)]
         y = np.zeros(4, dtype=np.uint32)
-        words = np.zeros(0, dtype=np.uint64)
-        for r in reversed(range(world)):
-            if rank == r and own:
-                y_out, words = gb.dribbon_backsub(y, c1 - c0)
-            else:
-                y_out = y
-            y = _bcast_u32(y_out, r, device)
+        for r in reversed(range(rank + 1, world)):
+            y = apply_map(maps[r], y)
+        words = gb.dribbon_finish(y, c1 - c0) if own else np.zeros(0, dtype=np.uint64)
         return seed, np.concatenate(allgather_arrays(words, device))
     raise RuntimeError(f"retrieval system unsolvable after {max_tries} seeds")
 

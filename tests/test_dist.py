@@ -98,3 +98,38 @@ def test_gloo_world2_exchange(c2_parts):
         p.join(timeout=240)
     out = dict(q.get(timeout=5) for _ in range(2))
     assert out == {0: True, 1: True}
+
+
+def test_boundary_maps_compose_like_the_serial_chain():
+    """dist.apply_map: composing affine GF(2) boundary maps right to left
+    equals applying them one by one, and the identity map passes y through."""
+    from paper_2308_09561_b200.dist import apply_map, identity_map
+
+    rng = np.random.default_rng(5)
+    y = rng.integers(0, 2**32, 4, dtype=np.uint64).astype(np.uint32)
+    y[3] &= 0x7FFFFFFF
+    assert (apply_map(identity_map(), y) == y).all()
+
+    def rand_map():
+        m = rng.integers(0, 2**32, (128, 4), dtype=np.uint64).astype(np.uint32)
+        m[:, 3] &= 0x7FFFFFFF
+        return m
+
+    def dense(mp):  # explicit matrix form: y_out = A y ^ c
+        A = np.zeros((127, 127), dtype=np.uint8)
+        for j in range(127):
+            col = np.unpackbits((mp[j] ^ mp[127]).view(np.uint8), bitorder="little")[:127]
+            A[:, j] = col
+        c = np.unpackbits(mp[127].view(np.uint8), bitorder="little")[:127]
+        return A, c
+
+    maps = [rand_map() for _ in range(3)]
+    bits = np.unpackbits(y.view(np.uint8), bitorder="little")[:127]
+    v = bits.copy()
+    for mp in reversed(maps):
+        A, c = dense(mp)
+        v = (A.astype(np.int64) @ v.astype(np.int64) + c) % 2
+    z = y
+    for mp in reversed(maps):
+        z = apply_map(mp, z)
+    assert (np.unpackbits(z.view(np.uint8), bitorder="little")[:127] == v).all()
