@@ -44,6 +44,12 @@ enum {
  * full speed), hi/lo are device pointers; the copy is pipelined in chunks
  * with the hashing (copy stream + main stream). */
 #define SHK_BLOB_HOST 2
+/* shk_build_create only: return as soon as the key prefix is on the host
+ * (*dup = -1, unknown): the scatter and the sort keep running, and the caller
+ * prepares run() meanwhile.  run() then waits for the duplicate flag just
+ * before its first search kernel and returns SHK_DUPLICATE if it is set;
+ * shk_build_duplicate reads it explicitly. */
+#define SHK_BUILD_ASYNC 8
 
 typedef struct shk_ctx shk_ctx;
 typedef struct shk_build shk_build;
@@ -192,6 +198,7 @@ typedef struct shk_plans {
  *   leaf_seed_bits, split_seed_bits, leaf_count (recsplit.py:539-547). */
 int shk_build_create(shk_ctx* ctx, const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nbuckets, int flags,
                      shk_build** out, int* dup, int64_t* max_bucket);
+int shk_build_duplicate(shk_build* b, int* dup /* 0 or 1; waits for the sort */);
 int shk_build_key_prefix(shk_build* b, uint64_t* key_prefix /* [nb+1] host */);
 int shk_build_sorted_keys(shk_build* b, uint64_t* hi, uint64_t* lo /* [N] host */);
 int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, int cache_min_leaf, int64_t b0,

@@ -17,7 +17,7 @@ import numpy as np
 
 from ..errors import FormatError, InvalidParameterError
 from . import _lib
-from ._lib import SHK_DEVICE, check, ctx, i64, load_library, ptr, u64
+from ._lib import SHK_BUILD_ASYNC, SHK_DEVICE, check, ctx, i64, load_library, ptr, u64
 
 NAME = "cuda"
 
@@ -472,11 +472,14 @@ class GpuBuild:
     bucket range) -> ribbon (over all keys).
     """
 
-    def __init__(self, hi, lo, nbuckets, hi_ptr=None, lo_ptr=None, n=None):
+    def __init__(self, hi, lo, nbuckets, hi_ptr=None, lo_ptr=None, n=None, asynchronous=False):
+        """asynchronous (device inputs only): return once the key prefix is
+        on the host, the sort still running; `duplicate` then waits for it,
+        and run() raises HashCollisionError itself on equal codes."""
         self.handle = None
         if hi_ptr is not None:
             N = int(n)
-            src_hi, src_lo, flags = hi_ptr, lo_ptr, SHK_DEVICE
+            src_hi, src_lo, flags = hi_ptr, lo_ptr, SHK_DEVICE | (SHK_BUILD_ASYNC if asynchronous else 0)
         else:
             hi = u64(hi)
             lo = u64(lo)
@@ -490,8 +493,16 @@ class GpuBuild:
         check(_L().shk_build_create(ctx(), src_hi, src_lo, N, self.nbuckets, flags, ctypes.byref(h), ctypes.byref(dup),
                                     ctypes.byref(mb)), "bucketize")
         self.handle = h
-        self.duplicate = bool(dup.value)
+        self._dup = None if dup.value < 0 else bool(dup.value)
         self.max_bucket = int(mb.value)
+
+    @property
+    def duplicate(self):
+        if self._dup is None:
+            d = ctypes.c_int(0)
+            check(_L().shk_build_duplicate(self.handle, ctypes.byref(d)), "bucketize")
+            self._dup = bool(d.value)
+        return self._dup
 
     def key_prefix(self):
         out = np.zeros(self.nbuckets + 1, dtype=np.uint64)

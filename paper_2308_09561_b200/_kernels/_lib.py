@@ -15,6 +15,7 @@ import numpy as np
 from ..errors import (
     ConstructionFailureError,
     FormatError,
+    HashCollisionError,
     InvalidParameterError,
     ShockHashError,
 )
@@ -24,6 +25,7 @@ LIB_PATH = os.environ.get("SHK_LIB_PATH") or os.path.join(
 
 SHK_OK, SHK_EXHAUSTED, SHK_FORMAT, SHK_INVALID, SHK_UNSOLVABLE, SHK_DUPLICATE = range(6)
 SHK_DEVICE = 1
+SHK_BUILD_ASYNC = 8
 
 
 class BackendUnavailableError(ShockHashError, RuntimeError):
@@ -95,6 +97,7 @@ _SIGS = {
     "shk_build_phase_ms": (_I, [_P, _P, _P]),
     "shk_build_level_ms": (_I, [_P, _P, _P, _I]),
     "shk_build_create": (_I, [_P, _P, _P, _I64, _I64, _I, _P, _P, _P]),
+    "shk_build_duplicate": (_I, [_P, _P]),
     "shk_build_key_prefix": (_I, [_P, _P]),
     "shk_build_sorted_keys": (_I, [_P, _P, _P]),
     "shk_build_set_record_placements": (_I, [_P, _I]),
@@ -164,6 +167,8 @@ def check(rc: int, what: str = ""):
         raise InvalidParameterError(msg)
     if rc == SHK_UNSOLVABLE:
         raise ConstructionFailureError(msg)
+    if rc == SHK_DUPLICATE:
+        raise HashCollisionError(msg)
     raise BackendUnavailableError(f"CUDA failure ({rc}) {msg}")
 
 

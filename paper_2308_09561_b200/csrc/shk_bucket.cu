@@ -254,7 +254,7 @@ size_t shk_bucketize_scratch(int64_t N, int64_t nb) {
 
 int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nb, uint64_t* skeys_u64,
                   uint64_t* key_prefix, int* dup_flag, void* scratch, size_t scratch_bytes, int64_t* max_bucket_out,
-                  cudaStream_t st) {
+                  cudaStream_t st, uint64_t* h_prefix) {
   if (scratch_bytes < shk_bucketize_scratch(N, nb)) {
     shk_set_error("bucketize scratch too small");
     return 3;
@@ -292,15 +292,29 @@ int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nb,
   int rc = shk_exclusive_scan_i64(counts, prefix, nb, scan_scratch, shk_scan_scratch(nb), st);
   if (rc) return rc;
   SHK_CUDA(cudaMemcpyAsync(cursor, prefix, (size_t)nb * 8, cudaMemcpyDeviceToDevice, st));
+  int64_t maxb = 0;
+  if (h_prefix) {
+    // the caller wants the key prefix early (to prepare the next phase while
+    // the scatter and the sort run): wait for the scan only, take the
+    // largest bucket from the prefix on the host, and return without waiting
+    // for the sort
+    SHK_CUDA(cudaMemcpyAsync(h_prefix, prefix, (size_t)(nb + 1) * 8, cudaMemcpyDeviceToHost, st));
+    SHK_CUDA(cudaStreamSynchronize(st));
+    for (int64_t bu = 0; bu < nb; ++bu) {
+      const int64_t cnt = (int64_t)(h_prefix[bu + 1] - h_prefix[bu]);
+      if (cnt > maxb) maxb = cnt;
+    }
+  }
   if (N > 0) {
     bucket_scatter_kernel<<<(unsigned)g, T, 0, st>>>(hi, lo, N, bid, cursor, unsorted);
     SHK_LAUNCHED();
   }
-  max_bucket_kernel<<<64, 256, 0, st>>>(counts, nb, maxv);
-  SHK_LAUNCHED();
-  int64_t maxb = 0;
-  SHK_CUDA(cudaMemcpyAsync(&maxb, maxv, 8, cudaMemcpyDeviceToHost, st));
-  SHK_CUDA(cudaStreamSynchronize(st));
+  if (!h_prefix) {
+    max_bucket_kernel<<<64, 256, 0, st>>>(counts, nb, maxv);
+    SHK_LAUNCHED();
+    SHK_CUDA(cudaMemcpyAsync(&maxb, maxv, 8, cudaMemcpyDeviceToHost, st));
+    SHK_CUDA(cudaStreamSynchronize(st));
+  }
   if (max_bucket_out) *max_bucket_out = maxb;
   int P = 1;
   while (P < maxb) P <<= 1;

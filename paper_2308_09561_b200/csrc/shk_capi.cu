@@ -53,6 +53,8 @@ struct shk_ctx {
   std::multimap<size_t, void*> free_blocks;
   std::unordered_map<void*, size_t> live;
   int* d_counter = nullptr;  // scratch ints: [0] counter [1] flag [2] flag
+  int* h_flags = nullptr;    // pinned host ints (a ring of per-build duplicate flags)
+  unsigned flag_next = 0;
   ShkRibbon* rib = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int64_t opt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // shk_ctx_set_option
@@ -202,6 +204,7 @@ int shk_ctx_create(int device, shk_ctx** out) {
   SHK_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
   c->stream = c->own;
   SHK_CUDA(cudaMalloc(&c->d_counter, 256));
+  SHK_CUDA(cudaMallocHost(&c->h_flags, 64 * sizeof(int)));
   SHK_CUDA(cudaEventCreate(&c->t0));
   SHK_CUDA(cudaEventCreate(&c->t1));
   shk_ribbon_create(&c->rib);
@@ -217,6 +220,7 @@ int shk_ctx_destroy(shk_ctx* c) {
   for (auto& kv : c->live) cudaFree(kv.first);
   shk_ribbon_destroy(c->rib);
   cudaFree(c->d_counter);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
   cudaEventDestroy(c->t0);
   cudaEventDestroy(c->t1);
   cudaStreamDestroy(c->own);
@@ -892,9 +896,24 @@ struct shk_build {
   cudaEvent_t ev[12] = {};
   float phase_ms[6] = {0, 0, 0, 0, 0, 0};
   int64_t split_evals = 0;
+  // asynchronous bucketize (SHK_BUILD_ASYNC): the duplicate flag lands in
+  // pinned memory behind the sort; run() (or shk_build_duplicate) reads it
+  int* h_dup = nullptr;
+  bool dup_pending = false;
+  int dup_value = 0;
+  int take_dup() {
+    if (dup_pending) {
+      cudaEventSynchronize(ev[1]);
+      dup_value = *h_dup;
+      dup_pending = false;
+      phase_ms[0] = span(0, 1);
+    }
+    return dup_value;
+  }
   explicit shk_build(shk_ctx* ctx)
       : c(ctx), keys(ctx), tmp(ctx), prefix(ctx), choice(ctx), words(ctx), place(ctx), sorted(ctx), drhs(ctx) {}
   ~shk_build() {
+    if (dup_pending) cudaEventSynchronize(ev[1]);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     level_reset();
@@ -972,17 +991,31 @@ int shk_build_create(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
     if ((rc = scratch.alloc(ss))) break;
     int* ddup = c->d_counter + 3;
     b->mark(0);
-    if ((rc = shk_bucketize((const uint64_t*)dh, (const uint64_t*)dl, N, nbuckets, b->keys.as<uint64_t>(),
-                            b->prefix.as<uint64_t>(), ddup, scratch.p, ss, &b->max_bucket, c->stream)))
-      break;
     b->h_prefix.resize((size_t)nbuckets + 1);
-    if ((rc = d2h(c, b->h_prefix.data(), b->prefix.p, (size_t)(nbuckets + 1) * 8))) break;
-    int hd = 0;
-    if ((rc = d2h(c, &hd, ddup, 4))) break;
-    b->mark(1);
-    if ((rc = csync(c))) break;
-    b->phase_ms[0] = b->span(0, 1);
-    *dup = hd;
+    const bool async = (flags & SHK_BUILD_ASYNC) != 0;
+    if ((rc = shk_bucketize((const uint64_t*)dh, (const uint64_t*)dl, N, nbuckets, b->keys.as<uint64_t>(),
+                            b->prefix.as<uint64_t>(), ddup, scratch.p, ss, &b->max_bucket, c->stream,
+                            async ? b->h_prefix.data() : nullptr)))
+      break;
+    if (async) {
+      // the prefix is on the host already; the scatter and the sort are
+      // still running: the duplicate flag follows them into pinned memory
+      b->h_dup = c->h_flags + (c->flag_next++ & 63u);
+      SHK_CUDA(cudaMemcpyAsync(b->h_dup, ddup, 4, cudaMemcpyDeviceToHost, c->stream));
+      b->mark(1);
+      b->dup_pending = true;
+      *dup = -1;
+      // host inputs were staged into pool buffers freed on return: finish now
+      if (!(flags & SHK_DEVICE)) *dup = b->take_dup();
+    } else {
+      if ((rc = d2h(c, b->h_prefix.data(), b->prefix.p, (size_t)(nbuckets + 1) * 8))) break;
+      int hd = 0;
+      if ((rc = d2h(c, &hd, ddup, 4))) break;
+      b->mark(1);
+      if ((rc = csync(c))) break;
+      b->phase_ms[0] = b->span(0, 1);
+      *dup = hd;
+    }
     if (max_bucket) *max_bucket = b->max_bucket;
   } while (0);
   if (rc) {
@@ -990,6 +1023,11 @@ int shk_build_create(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
     return rc;
   }
   *out = b;
+  return 0;
+}
+
+int shk_build_duplicate(shk_build* b, int* dup) {
+  *dup = b->take_dup();
   return 0;
 }
 
@@ -1147,6 +1185,12 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   }
   b->mark(2);
   b->level_reset();
+  // an asynchronous bucketize is checked here, after the host-side
+  // preparation (which overlapped the sort) and before the first search
+  if (b->take_dup()) {
+    shk_set_error("equal 128-bit codes in the input");
+    return SHK_DUPLICATE;
+  }
   // the seed searches take pre-mixed key high words (shk_hash.cuh premix_hi);
   // undone right after the leaves
   RC(shk_launch_premix(b->keys.as<uint64_t>(), b->N, 0, c->stream));

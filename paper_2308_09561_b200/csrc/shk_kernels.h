@@ -117,7 +117,8 @@ int shk_launch_choice_sorted(const uint64_t* keys, const uint64_t* sorted, const
 // skeys: interleaved (hi, lo) pairs [2N], sorted by (bucket, hi, lo).
 int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nbuckets, uint64_t* skeys,
                   uint64_t* key_prefix /*[nb+1]*/, int* dup_flag, void* scratch, size_t scratch_bytes,
-                  int64_t* max_bucket_out, cudaStream_t st);
+                  int64_t* max_bucket_out, cudaStream_t st,
+                  uint64_t* h_prefix = nullptr /* host [nb+1]: early prefix, no wait for the sort */);
 size_t shk_bucketize_scratch(int64_t N, int64_t nbuckets);
 
 // Generic exclusive scan of int64 (n elements) -> out[n+1] (out[n] = total).

@@ -66,6 +66,32 @@ def test_duplicates_and_parameters():
         recsplit.build([], 10, 4)
 
 
+def test_duplicates_on_the_device_paths():
+    """The asynchronous bucketize reports equal codes from run(): equal master
+    codes -> HashCollisionError (build_hashed_device); a repeated key in a
+    host blob -> DuplicateKeyError (build_blob, after the salt retry)."""
+    import numpy as np
+
+    from paper_2308_09561_b200 import device as dev
+    from paper_2308_09561_b200.errors import HashCollisionError
+
+    hi, lo = synthetic_hashed(3000, 23)
+    hi[2999], lo[2999] = hi[5], lo[5]
+    d_hi, d_lo = dev.DeviceBuffer.from_host(hi), dev.DeviceBuffer.from_host(lo)
+    with pytest.raises(HashCollisionError):
+        recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, 3000, 300, 20, 1)
+    keys = np.arange(4000, dtype="<u8")
+    keys[3999] = keys[123]
+    blob = np.frombuffer(keys.tobytes(), dtype=np.uint8)
+    with pytest.raises(DuplicateKeyError):
+        recsplit.build_blob(blob, 8, 400, 20, 1)
+    # and a clean build through the same path still matches the host path
+    keys[3999] = 10**9
+    blob = np.frombuffer(keys.tobytes(), dtype=np.uint8)
+    assert recsplit.build_blob(blob, 8, 400, 20, 1).serialize() == recsplit.build(
+        [k.tobytes() for k in keys], 400, 20, 1).serialize()
+
+
 def test_large_build_is_a_bijection():
     """10x the C4 key count (N = 1e8): no 32-bit index overflows anywhere on
     the path; checked by size-independent properties (every key maps into
