@@ -48,7 +48,8 @@ enum {
  * (*dup = -1, unknown): the scatter and the sort keep running, and the caller
  * prepares run() meanwhile.  run() then waits for the duplicate flag just
  * before its first search kernel and returns SHK_DUPLICATE if it is set;
- * shk_build_duplicate reads it explicitly. */
+ * shk_build_duplicate reads it explicitly.  Device inputs (hi, lo) must stay
+ * valid until one of those two calls returns (the scatter still reads them). */
 #define SHK_BUILD_ASYNC 8
 
 typedef struct shk_ctx shk_ctx;
