@@ -39,6 +39,11 @@ struct TreeArgs {
   LeafArgs leaf;
 };
 
+#ifdef SHK_TREE_TRACE
+// (analysis builds) start / end globaltimer of every node id < 2^20
+__device__ unsigned long long g_tree_trace[2 << 20];
+#endif
+
 SHK_D int64_t load_published(const int64_t* p) {
   int64_t v;
   asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -72,6 +77,10 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
     }
     id = __shfl_sync(FULL_WARP, id, 0);
     __threadfence();  // acquire side for all lanes; invalidates stale L1 lines
+#ifdef SHK_TREE_TRACE
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
     const ShkTreeNode nd = t.nodes[id];
     if (nd.kind == 0) {
       ShkSplitTask task;
@@ -102,6 +111,14 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       else
         solve_rotate<1, WIDE>(t.leaf, sm, nd.start, nd.m, o, 0, 0, lane, lane);
     }
+#ifdef SHK_TREE_TRACE
+    if (lane == 0 && id < (1 << 20)) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      g_tree_trace[2 * id] = t0;
+      g_tree_trace[2 * id + 1] = now;
+    }
+#endif
   }
 }
 
@@ -202,3 +219,11 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   SHK_LAUNCHED();
   return 0;
 }
+
+#ifdef SHK_TREE_TRACE
+extern "C" int shk_debug_tree_trace(unsigned long long* out, int64_t n) {
+  if (n > (1 << 20)) n = 1 << 20;
+  SHK_CUDA(cudaMemcpyFromSymbol(out, g_tree_trace, (size_t)n * 16));
+  return 0;
+}
+#endif
