@@ -212,16 +212,27 @@ SHK_HD uint64_t unpremix_hi(uint64_t h) { return h ^ (h >> 30) ^ (h >> 60); }
 SHK_D u2 seed_mixer_pre_d(uint64_t seed, uint64_t tag) { return split64(premix_hi(seed_mixer(seed, tag))); }
 
 // First mix64 from pre-mixed operands, then the second one (full remix).
+// AM bit i: xor-shift i (27, 31, 30, 27, 31 in order) takes its high-word
+// shift on the ALU pipe (SHF) instead of the FMA pipe (IMAD.HI), to balance
+// the two pipes per kernel (the plain leaf search is FMA-heavy: ncu
+// profiles/r01_ncu_full_leaf_c3_v17.csv).
+template <int S, int AM, int I>
+SHK_D u2 xs_sel(u2 z) {
+  return ((AM >> I) & 1) ? xorshr_alu<S>(z) : xorshr<S>(z);
+}
+template <int AM = 0>
 SHK_D u2 remix_pre_d(u2 kp, u2 k_lo, u2 xp) {
   u2 z;
   z.lo = kp.lo ^ xp.lo;
   z.hi = kp.hi ^ xp.hi;
   z = mulc<MUL1>(z);
-  z = mulc<MUL2>(xorshr<27>(z));
-  z = xorshr<31>(z);
+  z = mulc<MUL2>(xs_sel<27, AM, 0>(z));
+  z = xs_sel<31, AM, 1>(z);
   z.lo ^= k_lo.lo;
   z.hi ^= k_lo.hi;
-  return mix64_d(z);
+  z = mulc<MUL1>(xs_sel<30, AM, 2>(z));
+  z = mulc<MUL2>(xs_sel<27, AM, 3>(z));
+  return xs_sel<31, AM, 4>(z);
 }
 
 SHK_D uint32_t remix_top_pre_d(u2 kp, u2 k_lo, u2 xp) {

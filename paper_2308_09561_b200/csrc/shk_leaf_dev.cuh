@@ -149,6 +149,17 @@ SHK_D void plain_fill_edges(const uint4* keys, int n, uint64_t s, unsigned lanes
 
 // Plain search body for one candidate seed per lane (STORE: also write the
 // lane's edge column).
+// remix_pre_d's shift placement (AM) in the plain search's filter loop.
+// Masks of <= 32 cells: the loop is FMA-pipe bound (ncu C3: fmaheavy 83%,
+// ALU 63% with every high-word shift on IMAD.HI), so all five shifts go to
+// the ALU pipe (C3 26.0 -> 25.5 ms, tools/ab_leaf.sh).  64-bit masks spend
+// more ALU instructions on the one-hot cells and keep the FMA placement.
+#ifndef SHK_PLAIN_SHIFT_MASK
+#define SHK_PLAIN_SHIFT_MASK 0x1F
+#endif
+#ifndef SHK_PLAIN_SHIFT_MASK_WIDE
+#define SHK_PLAIN_SHIFT_MASK_WIDE 0
+#endif
 template <bool WIDE, bool STORE = true>
 SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
   u2 x = seed_mixer_pre_d(s, TAG_LEAF);
@@ -157,7 +168,7 @@ SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
 #pragma unroll 4
   for (int i = 0; i < n; ++i) {
     uint4 k = keys[i];
-    u2 v = remix_pre_d(u2{k.x, k.y}, u2{k.z, k.w}, x);
+    u2 v = remix_pre_d<WIDE ? SHK_PLAIN_SHIFT_MASK_WIDE : SHK_PLAIN_SHIFT_MASK>(u2{k.x, k.y}, u2{k.z, k.w}, x);
     uint32_t h0, h1;
     leaf_pair_d(v, un, unm1, h0, h1);
     if (!WIDE) {

@@ -42,6 +42,8 @@ struct TreeArgs {
 #ifdef SHK_TREE_TRACE
 // (analysis builds) start / end globaltimer of every node id < 2^20
 __device__ unsigned long long g_tree_trace[2 << 20];
+// node size m << 8 | fanout (0 for a leaf)
+__device__ unsigned int g_tree_trace_m[1 << 20];
 #endif
 
 SHK_D int64_t load_published(const int64_t* p) {
@@ -117,6 +119,7 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       g_tree_trace[2 * id] = t0;
       g_tree_trace[2 * id + 1] = now;
+      g_tree_trace_m[id] = ((unsigned)nd.m << 8) | (nd.kind == 0 ? (unsigned)nd.fanout : 0u);
     }
 #endif
   }
@@ -224,6 +227,11 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
 extern "C" int shk_debug_tree_trace(unsigned long long* out, int64_t n) {
   if (n > (1 << 20)) n = 1 << 20;
   SHK_CUDA(cudaMemcpyFromSymbol(out, g_tree_trace, (size_t)n * 16));
+  return 0;
+}
+extern "C" int shk_debug_tree_trace_m(unsigned int* out, int64_t n) {
+  if (n > (1 << 20)) n = 1 << 20;
+  SHK_CUDA(cudaMemcpyFromSymbol(out, g_tree_trace_m, (size_t)n * 4));
   return 0;
 }
 #endif

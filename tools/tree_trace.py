@@ -41,11 +41,16 @@ lib.shk_debug_tree_trace.restype = ctypes.c_int
 lib.shk_debug_tree_trace.argtypes = [ctypes.c_void_p, ctypes.c_int64]
 tr = np.zeros((1 << 20, 2), dtype=np.uint64)
 lib.shk_debug_tree_trace(tr.ctypes.data, 1 << 20)
+lib.shk_debug_tree_trace_m.restype = ctypes.c_int
+lib.shk_debug_tree_trace_m.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+tm = np.zeros(1 << 20, dtype=np.uint32)
+lib.shk_debug_tree_trace_m(tm.ctypes.data, 1 << 20)
 # nodes of this run: start >= the run's earliest (older entries are from the first rep or stale)
 valid = tr[:, 1] > 0
 t_end_max = tr[valid, 1].max()
 t_first = tr[valid & (tr[:, 0] > t_end_max - np.uint64(int(ms * 1e6 * 1.5))), 0].min()
 sel = valid & (tr[:, 0] >= t_first)
+info = tm[sel]
 st = (tr[sel, 0] - t_first).astype(np.float64) / 1e6
 en = (tr[sel, 1] - t_first).astype(np.float64) / 1e6
 dur = en - st
@@ -61,6 +66,17 @@ for frac in (0.9, 0.5, 0.25, 0.1):
     print(f"busy >= {int(frac*100)}% of peak ({peak} warps) until {last:.2f} ms ({100*last/span:.1f}% of span)")
 work = dur.sum()
 print(f"warp-ms of work {work:.0f}; at peak occupancy the span would be {work / peak:.2f} ms")
-order = np.argsort(-dur)[:8]
+order = np.argsort(-dur)[:12]
 for i in order:
-    print(f"  node: start {st[i]:7.2f} end {en[i]:7.2f} ms, {dur[i]:.2f} ms")
+    print(f"  node m={info[i] >> 8} fanout={info[i] & 255}: start {st[i]:7.2f} end {en[i]:7.2f} ms, {dur[i]:.2f} ms")
+# per node type: count, mean / max duration, share of warp-time
+kinds = {}
+for key in np.unique(info & 255):
+    for big in (False, True):
+        msk = ((info & 255) == key) & (((info >> 8) > 200) == big)
+        if msk.any():
+            kinds[(int(key), big)] = msk
+for (f, big), msk in sorted(kinds.items()):
+    d = dur[msk]
+    print(f"  {'leaf' if f == 0 else f'split F={f}'} {'m>200' if big else 'm<=200'}: {msk.sum()} nodes, "
+          f"mean {d.mean()*1e3:.0f} us, max {d.max():.2f} ms, {100*d.sum()/work:.1f}% of warp-time")
