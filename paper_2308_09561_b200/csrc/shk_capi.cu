@@ -1115,13 +1115,22 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   std::vector<std::vector<ShkSplitTask>> tasks((size_t)S.max_depth + 1);
   std::vector<int64_t> leaf_off, leaf_slot;
   std::vector<int64_t> kstart_v, root_pos;
-  int64_t nroots = 0;
+  // persistent schedule: split roots open the split region [0, nsplit) of the
+  // queue, leaf roots the leaf region [nsplit, nn) (shk_tree.cu)
+  const int64_t nsplit = nn - n_leaves;
+  int64_t nroots_split = 0, nroots_leaf = 0;
   if (use_tree) {
     kstart_v.resize((size_t)nbr);
     root_pos.resize((size_t)nbr);
     for (int64_t i = 0; i < nbr; ++i) {
       kstart_v[i] = (int64_t)b->h_prefix[b0 + i];
-      root_pos[i] = bplan[i] >= 0 ? nroots++ : -1;
+      if (bplan[i] < 0) {
+        root_pos[i] = -1;
+      } else if (S.nodes[S.plan_off[bplan[i]]].kind == 0) {
+        root_pos[i] = nroots_split++;
+      } else {
+        root_pos[i] = nsplit + nroots_leaf++;
+      }
     }
   } else {
     ng.resize((size_t)nn);
@@ -1213,8 +1222,10 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     RC(h2d(c, dks.p, kstart_v.data(), (size_t)nbr * 8));
     RC(h2d(c, droot.p, root_pos.data(), (size_t)nbr * 8));
     SHK_CUDA(cudaMemsetAsync(dqueue.p, 0xFF, (size_t)nn * 8, c->stream));
-    unsigned long long qc[2] = {0ull, (unsigned long long)nroots};
-    RC(h2d(c, dqctl.p, qc, 16));
+    // split head, leaf head, split tail, leaf tail
+    unsigned long long qc[4] = {0ull, (unsigned long long)nsplit, (unsigned long long)nroots_split,
+                                (unsigned long long)(nsplit + nroots_leaf)};
+    RC(h2d(c, dqctl.p, qc, 32));
     RC(shk_launch_expand_nodes(dpn.as<PlanNode>(), dpoff.as<int64_t>(), dbp.as<int32_t>(), dnbase.as<int64_t>(),
                                dks.as<int64_t>(), droot.as<int64_t>(), nbr, dnodes.as<ShkTreeNode>(), dg.as<int32_t>(),
                                dkind.as<uint8_t>(), dqueue.as<int64_t>(), c->stream));
@@ -1226,7 +1237,15 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     p.nnodes = nn;
     p.queue = dqueue.as<int64_t>();
     p.head = dqctl.as<unsigned long long>();
-    p.tail = dqctl.as<unsigned long long>() + 1;
+    p.tail = dqctl.as<unsigned long long>() + 2;
+    p.nsplit = nsplit;
+    {
+      // A/B of the slot-aware schedule: SHK_TREE_SLOT_AWARE=0 lets every warp
+      // take split nodes; SHK_TREE_SLOW_WID=k sets the first leaf-only slot
+      const char* e = getenv("SHK_TREE_SLOT_AWARE");
+      const char* w = getenv("SHK_TREE_SLOW_WID");
+      p.slow_wid = (e && e[0] == '0') ? (1 << 30) : (w ? atoi(w) : 0);
+    }
     p.max_seed = max_seed;
     p.seeds = dseeds.as<int64_t>();
     p.mode = mode;

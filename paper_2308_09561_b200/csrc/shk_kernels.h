@@ -94,9 +94,11 @@ struct ShkTreeLaunch {
   uint64_t* tmp;   // scratch pairs
   const ShkTreeNode* nodes;
   int64_t nnodes;
-  int64_t* queue;  // [nnodes]: roots first, -1 = not yet published
-  unsigned long long* head;
-  unsigned long long* tail;
+  int64_t* queue;  // [nnodes]: split region [0, nsplit) then leaf region; roots first in each; -1 = not yet published
+  unsigned long long* head;  // [2] split head, leaf head
+  unsigned long long* tail;  // [2] split tail, leaf tail
+  int64_t nsplit;            // split nodes (size of the split region)
+  int slow_wid;              // warps with %warpid >= slow_wid take leaves only; 0 = half the resident warps
   uint64_t max_seed;
   int64_t* seeds;  // per node
   int mode, cache_k, cache_min_leaf, max_n;

@@ -19,6 +19,22 @@
 // so a waiting warp always gets its task; warps exit once head >= node count.
 // Results are exactly those of the per-level schedule: every node sees the
 // same keys in the same order and runs the same minimum-seed search.
+//
+// Warp slots are not equal.  The issue arbiter of a sub-partition favours
+// low hardware warp slots (%warpid), so in this issue-bound kernel a warp in
+// the top CTA slot runs ~16x slower than one in the bottom slot
+// (tools/tree_trace.py: mean node time per %warpid at C4, 0.55 ms for slots
+// 0-3, 9 ms for slots 28-31).  A split node that lands on a slow slot gates
+// its whole subtree: the long nodes of a build were 3 x 160 / 4 x 40 splits
+// started in the first milliseconds on slots >= 24 and finished only when
+// the queue drained.  So the queue is split in two regions, split nodes
+// [0, nsplit) and leaves [nsplit, nnodes), each with its own head and tail:
+// warps in the lower half of the slots take split nodes first and leaves
+// once every split has been handed out; warps in the upper half take leaves
+// only (a leaf gates nothing).  Each region hands out tickets as before
+// (atomicAdd on its head, then wait until the slot is published).  A lower
+// slot waiting for a split leaves its issue share to the leaf warps, so the
+// SM stays busy while the splits run on the fast slots.
 #include "shk_kernels.h"
 #include "shk_leaf_dev.cuh"
 #include "shk_split_dev.cuh"
@@ -30,9 +46,11 @@ struct TreeArgs {
   ulonglong2* tmp;
   const ShkTreeNode* nodes;
   int64_t nnodes;
-  int64_t* queue;
-  unsigned long long* head;
-  unsigned long long* tail;
+  int64_t* queue;              // [nnodes]: split region [0, nsplit), leaf region [nsplit, nnodes)
+  unsigned long long* head;    // [2]: split head, leaf head (absolute slot indices)
+  unsigned long long* tail;    // [2]: split tail, leaf tail
+  int64_t nsplit;
+  int slow_wid;                // warps with %warpid >= slow_wid take leaves only
   uint64_t max_seed;
   int64_t* seeds;
   int* exhausted;
@@ -42,7 +60,7 @@ struct TreeArgs {
 #ifdef SHK_TREE_TRACE
 // (analysis builds) start / end globaltimer of every node id < 2^20
 __device__ unsigned long long g_tree_trace[2 << 20];
-// node size m << 8 | fanout (0 for a leaf)
+// node size m << 8 | fanout (0 for a leaf) | %warpid << 24 of the warp that ran it
 __device__ unsigned int g_tree_trace_m[1 << 20];
 #endif
 
@@ -54,6 +72,12 @@ SHK_D int64_t load_published(const int64_t* p) {
 
 SHK_D void publish(int64_t* p, int64_t v) {
   asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+SHK_D unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // MAXE: leaf buffer capacity; MINB: CTAs per SM requested from ptxas (8 = 64
@@ -68,11 +92,23 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
   const int w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   LeafSmem<1, MAXE>& sm = sm_all[w];
+  unsigned wid;
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  // lower slots take split tickets until the split region is used up, then
+  // leaf tickets; upper slots take leaf tickets only
+  bool splits_done = (int)wid >= t.slow_wid;
   for (;;) {
     unsigned long long h = 0;
-    if (lane == 0) h = atomicAdd(t.head, 1ull);
-    h = __shfl_sync(FULL_WARP, h, 0);
-    if (h >= (unsigned long long)t.nnodes) break;
+    if (!splits_done) {
+      if (lane == 0) h = atomicAdd(t.head, 1ull);
+      h = __shfl_sync(FULL_WARP, h, 0);
+      if (h >= (unsigned long long)t.nsplit) splits_done = true;
+    }
+    if (splits_done) {
+      if (lane == 0) h = atomicAdd(t.head + 1, 1ull);
+      h = __shfl_sync(FULL_WARP, h, 0);
+      if (h >= (unsigned long long)t.nnodes) break;
+    }
     int64_t id = -1;
     if (lane == 0) {
       while ((id = load_published(t.queue + h)) < 0) __nanosleep(200);
@@ -103,8 +139,11 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       if (lane == 0) {
         // children are published even after a failed search (the build is
         // flagged exhausted) so that no consumer waits forever
-        const unsigned long long pos = atomicAdd(t.tail, (unsigned long long)nd.fanout);
-        for (int k = 0; k < nd.fanout; ++k) publish(t.queue + pos + k, nd.child[k]);
+        for (int k = 0; k < nd.fanout; ++k) {
+          const int64_t ch = nd.child[k];
+          const int r = t.nodes[ch].kind != 0;  // 0: split region, 1: leaf region
+          publish(t.queue + atomicAdd(t.tail + r, 1ull), ch);
+        }
       }
     } else {
       const LeafOut o{id, -1};
@@ -119,7 +158,9 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       g_tree_trace[2 * id] = t0;
       g_tree_trace[2 * id + 1] = now;
-      g_tree_trace_m[id] = ((unsigned)nd.m << 8) | (nd.kind == 0 ? (unsigned)nd.fanout : 0u);
+      unsigned wid;
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+      g_tree_trace_m[id] = ((unsigned)nd.m << 8) | (nd.kind == 0 ? (unsigned)nd.fanout : 0u) | (wid << 24);
     }
 #endif
   }
@@ -182,6 +223,7 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   t.queue = p.queue;
   t.head = p.head;
   t.tail = p.tail;
+  t.nsplit = p.nsplit;
   t.max_seed = p.max_seed;
   t.seeds = p.seeds;
   t.exhausted = p.exhausted;
@@ -218,6 +260,7 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   SHK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 128, 0));
   if (occ < 1) occ = 1;
   const int sms = p.num_sms > 0 ? p.num_sms : 148;
+  t.slow_wid = p.slow_wid > 0 ? p.slow_wid : (occ * 4) / 2;
   kfn<<<(unsigned)(sms * occ), 128, 0, st>>>(t);
   SHK_LAUNCHED();
   return 0;

@@ -50,7 +50,8 @@ valid = tr[:, 1] > 0
 t_end_max = tr[valid, 1].max()
 t_first = tr[valid & (tr[:, 0] > t_end_max - np.uint64(int(ms * 1e6 * 1.5))), 0].min()
 sel = valid & (tr[:, 0] >= t_first)
-info = tm[sel]
+info = tm[sel] & np.uint32(0xFFFFFF)
+wid = (tm[sel] >> np.uint32(24)).astype(np.int64)
 st = (tr[sel, 0] - t_first).astype(np.float64) / 1e6
 en = (tr[sel, 1] - t_first).astype(np.float64) / 1e6
 dur = en - st
@@ -68,7 +69,7 @@ work = dur.sum()
 print(f"warp-ms of work {work:.0f}; at peak occupancy the span would be {work / peak:.2f} ms")
 order = np.argsort(-dur)[:12]
 for i in order:
-    print(f"  node m={info[i] >> 8} fanout={info[i] & 255}: start {st[i]:7.2f} end {en[i]:7.2f} ms, {dur[i]:.2f} ms")
+    print(f"  node m={info[i] >> 8} fanout={info[i] & 255} warpid={wid[i]}: start {st[i]:7.2f} end {en[i]:7.2f} ms, {dur[i]:.2f} ms")
 # per node type: count, mean / max duration, share of warp-time
 kinds = {}
 for key in np.unique(info & 255):
@@ -80,3 +81,12 @@ for (f, big), msk in sorted(kinds.items()):
     d = dur[msk]
     print(f"  {'leaf' if f == 0 else f'split F={f}'} {'m>200' if big else 'm<=200'}: {msk.sum()} nodes, "
           f"mean {d.mean()*1e3:.0f} us, max {d.max():.2f} ms, {100*d.sum()/work:.1f}% of warp-time")
+# per hardware warp slot (%warpid; the scheduler favours high slots): work done
+# (node count, busy time) and the mean duration of the 4 x 40 split nodes
+print("warpid: nodes, mean node us, mean 4x40-split us")
+f40 = ((info & 255) == 4) & ((info >> 8) <= 200)
+for w_ in range(int(wid.max()) + 1):
+    m_ = wid == w_
+    if m_.any():
+        d40 = dur[m_ & f40]
+        print(f"  {w_:3d}: {m_.sum():7d} {dur[m_].mean()*1e3:9.0f} {d40.mean()*1e3 if len(d40) else 0:9.0f}")
