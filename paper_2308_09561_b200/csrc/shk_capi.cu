@@ -1245,6 +1245,8 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
       const char* e = getenv("SHK_TREE_SLOT_AWARE");
       const char* w = getenv("SHK_TREE_SLOW_WID");
       p.slow_wid = (e && e[0] == '0') ? (1 << 30) : (w ? atoi(w) : 0);
+      const char* iw = getenv("SHK_TREE_IDLE_WID");
+      p.idle_wid = iw ? atoi(iw) : 0;
     }
     p.max_seed = max_seed;
     p.seeds = dseeds.as<int64_t>();

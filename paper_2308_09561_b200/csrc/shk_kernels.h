@@ -99,6 +99,7 @@ struct ShkTreeLaunch {
   unsigned long long* tail;  // [2] split tail, leaf tail
   int64_t nsplit;            // split nodes (size of the split region)
   int slow_wid;              // warps with %warpid >= slow_wid take leaves only; 0 = half the resident warps
+  int idle_wid;              // warps with %warpid >= idle_wid take no work; 0 = none (A/B only)
   uint64_t max_seed;
   int64_t* seeds;  // per node
   int mode, cache_k, cache_min_leaf, max_n;

@@ -51,6 +51,7 @@ struct TreeArgs {
   unsigned long long* tail;    // [2]: split tail, leaf tail
   int64_t nsplit;
   int slow_wid;                // warps with %warpid >= slow_wid take leaves only
+  int idle_wid;                // warps with %warpid >= idle_wid take no work (A/B)
   uint64_t max_seed;
   int64_t* seeds;
   int* exhausted;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
   asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
   // lower slots take split tickets until the split region is used up, then
   // leaf tickets; upper slots take leaf tickets only
+  if ((int)wid >= t.idle_wid) return;
   bool splits_done = (int)wid >= t.slow_wid;
   for (;;) {
     unsigned long long h = 0;
@@ -261,6 +263,7 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   if (occ < 1) occ = 1;
   const int sms = p.num_sms > 0 ? p.num_sms : 148;
   t.slow_wid = p.slow_wid > 0 ? p.slow_wid : (occ * 4) / 2;
+  t.idle_wid = p.idle_wid > 0 ? p.idle_wid : 1 << 30;
   kfn<<<(unsigned)(sms * occ), 128, 0, st>>>(t);
   SHK_LAUNCHED();
   return 0;
