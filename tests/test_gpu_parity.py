@@ -193,6 +193,25 @@ def test_c2_build_golden():
     assert (np.bincount(own.astype(np.int64), minlength=len(keys)) == 1).all()
 
 
+@pytest.mark.parametrize("env", [
+    {"SHK_TREE_SLOT_AWARE": "0"},          # every warp slot takes split nodes
+    {"SHK_TREE_SLOW_WID": "4"},            # splits on the 4 lowest slots only
+    {"SHK_TREE_SLOW_WID": "31", "SHK_TREE_IDLE_WID": "24"},
+])
+def test_c2_build_schedule_independent(monkeypatch, env):
+    """The persistent tree kernel's schedule (which warp slots take split nodes
+    and which take leaves, shk_tree.cu) changes only the order of the work:
+    the C2 descriptor is the reference's bytes under every schedule."""
+    from paper_2308_09561_b200 import recsplit
+    from paper_2308_09561_b200 import workloads as W
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    keys = W.keys_as_bytes(W.build_keys(2))
+    blob = recsplit.build(keys, 500, 24).serialize()
+    assert sha(blob) == golden("c2.json")["desc_sha"]
+
+
 def test_small_builds_golden():
     from paper_2308_09561_b200 import recsplit
     from paper_2308_09561_b200.keys import synthetic_hashed, synthetic_keys
