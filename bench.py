@@ -15,7 +15,9 @@ config is measured after the build steps and reported beside it.
 
 Multi-GPU (torchrun): buckets are sharded by range over ranks (strong
 scaling, total N fixed); one all-gather joins streams and choice bits;
-rank 0 solves the global ribbon.  Time = max over ranks.
+the ranks solve the global ribbon column-sharded (dist.ribbon_sharded).
+Time = max over ranks.  The leaf-only configs C1/C3/C5 are reported beside
+the build (contiguous leaf ranges per rank at N > 1).
 
 ``--impl reference`` times the reference's CPU implementation of the same
 path: its own compiled kernels (oracle/_ref, built from /root/reference by
@@ -533,7 +535,7 @@ def main():
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--leaf-configs", default="1,3", help="leaf-search-only configs to add (C1,C3,C5)")
+    ap.add_argument("--leaf-configs", default="1,3,5", help="leaf-search-only configs to add (C1,C3,C5; C5 is one ~13 s launch)")
     ap.add_argument("--leaf-reps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
