@@ -149,16 +149,17 @@ SHK_D void plain_fill_edges(const uint4* keys, int n, uint64_t s, unsigned lanes
 
 // Plain search body for one candidate seed per lane (STORE: also write the
 // lane's edge column).
-// remix_pre_d's shift placement (AM) in the plain search's filter loop.
-// Masks of <= 32 cells: the loop is FMA-pipe bound (ncu C3: fmaheavy 83%,
-// ALU 63% with every high-word shift on IMAD.HI), so all five shifts go to
-// the ALU pipe (C3 26.0 -> 25.5 ms, tools/ab_leaf.sh).  64-bit masks spend
-// more ALU instructions on the one-hot cells and keep the FMA placement.
+// remix_pre_d's shift placement (AM) in the plain search's filter loop.  The
+// loop is FMA-pipe bound with every high-word shift on IMAD.HI (ncu: C3
+// fmaheavy 83% / ALU 63%, C5 fmaheavy 85% / ALU 63%), so all five shifts go
+// to the ALU pipe (tools/ab_leaf.sh: C3 26.0 -> 25.5 ms; C5 13.03-13.08 ->
+// 12.82-12.92 s).  The rotate search in the build keeps the FMA placement:
+// the tree kernel is ALU-heavier (split hashes), ncu ALU 72% / fmaheavy 65%.
 #ifndef SHK_PLAIN_SHIFT_MASK
 #define SHK_PLAIN_SHIFT_MASK 0x1F
 #endif
 #ifndef SHK_PLAIN_SHIFT_MASK_WIDE
-#define SHK_PLAIN_SHIFT_MASK_WIDE 0
+#define SHK_PLAIN_SHIFT_MASK_WIDE 0x1F
 #endif
 template <bool WIDE, bool STORE = true>
 SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
