@@ -20,8 +20,8 @@
 // Results are exactly those of the per-level schedule: every node sees the
 // same keys in the same order and runs the same minimum-seed search.
 //
-// Warp slots are not equal.  The issue arbiter of a sub-partition favours
-// low hardware warp slots (%warpid), so in this issue-bound kernel a warp in
+// Warp slots are not equal.  The issue arbiter of a sub-partition serves
+// low hardware warp slots (%warpid) first (measured), so in this issue-bound kernel a warp in
 // the top CTA slot runs ~16x slower than one in the bottom slot
 // (tools/tree_trace.py: mean node time per %warpid at C4, 0.55 ms for slots
 // 0-3, 9 ms for slots 28-31).  A split node that lands on a slow slot gates
