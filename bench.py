@@ -4,8 +4,10 @@
 Workload (one step): build the minimal perfect hash function of N=10,000,000
 uniform random 64-bit keys (8-byte little-endian strings, ``default_rng(4)``),
 leaf size n=40, bucket size b=2000, rotation fitting — the largest
-single-GPU configuration of BASELINE.json; the 1e8-query pass of the same
-config is measured after the build steps and reported beside it.
+single-GPU configuration of BASELINE.json.  Reported beside it: the 1e8
+queries of the same config, the leaf-only configs C1/C3/C5, the C2 build and
+its 1e6 queries, the measured integer-issue peak, and the reference's CPU
+path timed on this host.
 
   value : keys/s of the build from master hash codes resident in HBM
           (bucketize -> split searches -> leaf searches + orientation ->
@@ -13,11 +15,14 @@ config is measured after the build steps and reported beside it.
   e2e   : keys/s through the public C-ABI/Python API with HOST buffers:
           8-byte key blob H2D -> blake2b -> build -> descriptor bytes D2H.
 
-Multi-GPU (torchrun): buckets are sharded by range over ranks (strong
-scaling, total N fixed); one all-gather joins streams and choice bits;
-the ranks solve the global ribbon column-sharded (dist.ribbon_sharded).
-Time = max over ranks.  The leaf-only configs C1/C3/C5 are reported beside
-the build (contiguous leaf ranges per rank at N > 1).
+Multi-GPU: ``--gpus N`` with no WORLD_SIZE in the environment re-launches
+itself under ``torch.distributed.run`` with N ranks (one per GPU, NCCL).
+Buckets are sharded by range over ranks (strong scaling, total N fixed); one
+all-gather joins streams and choice bits; the ranks solve the global ribbon
+column-sharded (dist.ribbon_sharded) and every rank ends with the whole
+descriptor.  Queries: replicated descriptor, batch sharded by range.  Leaf
+configs: contiguous leaf ranges per rank.  Time = max over ranks.
+``SHK_DIST_BACKEND=gloo`` runs the N ranks on one GPU (functional check).
 
 ``--impl reference`` times the reference's CPU implementation of the same
 path: its own compiled kernels (oracle/_ref, built from /root/reference by
@@ -30,6 +35,7 @@ import gc
 import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -41,11 +47,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CFG = dict(N=10_000_000, n=40, b=2000, mode=1, queries=100_000_000)
+CFG2 = dict(N=100_000, n=24, b=500, mode=1, queries=1_000_000)
 W_KEY = 53   # int32 ops per key-hash-eval, 64-bit masks
 W_SEED = 22  # per seed mixer + mask compare
 W_ROT = 10   # per rotation test, 64-bit masks
 W_SPLIT = 46  # per split key-eval
+W_QUERY = 620  # int32 ops per query with the derived node index
 INT_OPS_PER_CLK_SM = 128  # 4 SMSPs x 32 lanes, ALU + FMA pipes (one warp-instr/clk/SMSP)
+MAX_MHZ = 1965.0
+HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+C3_FIG2_MEAN = 4023  # PAPER.md:788, plain ShockHash n=32
+C3_RICE_MODEL = 4984  # (e/2)^n * e / sqrt(pi n) at n=32 (recsplit.py:173-184)
 
 
 def log(*a):
@@ -141,12 +153,49 @@ def barrier(world):
         dist.barrier()
 
 
+def sha_rank_order(arr, world):
+    """sha256 of the concatenation of every rank's array in rank order
+    (rank 0 returns it; the slices travel to rank 0 one at a time)."""
+    h = hashlib.sha256()
+    raw = np.ascontiguousarray(arr).view(np.uint8)
+    if world == 1:
+        h.update(raw.tobytes())
+        return h.hexdigest()
+    import torch
+    import torch.distributed as dist
+
+    dev = coll_device()
+    rank = dist.get_rank()
+    n = torch.tensor([raw.size], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    if rank == 0:
+        h.update(raw.tobytes())
+        for r in range(1, world):
+            buf = torch.empty(max(int(sizes[r].item()), 1), dtype=torch.uint8, device=dev)
+            dist.recv(buf, src=r)
+            h.update(buf[: int(sizes[r].item())].cpu().numpy().tobytes())
+        return h.hexdigest()
+    t = torch.from_numpy(raw.copy() if raw.size else np.zeros(1, np.uint8)).to(dev)
+    dist.send(t, dst=0)
+    return None
+
+
 def input_keys():
     from paper_2308_09561_b200 import workloads as W
 
     k = W.build_keys(4)
     blob = np.frombuffer(np.ascontiguousarray(k, dtype="<u8").tobytes(), dtype=np.uint8)
     return k, blob
+
+
+def hbm_peak():
+    """(GB/s, source) — the driver-measured copy bandwidth, else the fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
 NCU_TREE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_tree_latest.csv")
@@ -172,12 +221,27 @@ def ncu_traffic():
         return None
 
 
-def roofline_numbers(prof, hash_evals, n, clock_mhz, sms):
+def measure_int_peak(dev, sms):
+    """The integer-issue microbenchmark (csrc/shk_peak.cu) next to the nominal
+    128 ops/clk/SM: Tops/s per instruction mix, best = the measured peak."""
+    res = {}
+    for kind, name in dev.INT_PEAK_KINDS.items():
+        ms, ops = dev.int_peak(kind, 16384)
+        res[name] = round(ops / (ms * 1e-3) / 1e12, 3)
+    nominal = INT_OPS_PER_CLK_SM * sms * MAX_MHZ * 1e6 / 1e12
+    best = max(res.values())
+    return {"nominal_Tops": round(nominal, 2), "measured_Tops": res, "measured_best_Tops": best,
+            "measured_over_nominal": round(best / nominal, 4),
+            "how": "8 independent 32-bit chains per thread, 64 warps/SM, one timed launch per mix "
+                   "(inline PTX: lop3.b32 -> LOP3, mad.lo.u32 -> IMAD, shf.r.wrap -> SHF)"}
+
+
+def roofline_numbers(prof, hash_evals, n, clock_mhz, sms, int_peak=None):
     """Integer-issue roofline of the dominant kernel (split or leaf search)."""
     ph = prof["phase_ms"]
     leaf_ops = hash_evals * W_KEY + (hash_evals / 2) * W_ROT + (hash_evals / (2 * n)) * 2 * W_SEED
     split_ops = prof["split_evals"] * W_SPLIT
-    peak = INT_OPS_PER_CLK_SM * sms * 1965e6 / 1e12  # Tops/s at max clock
+    peak = INT_OPS_PER_CLK_SM * sms * MAX_MHZ * 1e6 / 1e12  # Tops/s at max clock
     if ph["leaf_search"] < 0.05 * ph["split_search"]:
         # persistent schedule: split and leaf searches share one kernel launch
         kern = {"tree_kernel(split+leaf search)": (leaf_ops + split_ops, ph["split_search"] + ph["leaf_search"])}
@@ -191,7 +255,7 @@ def roofline_numbers(prof, hash_evals, n, clock_mhz, sms):
     ach = ops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
     other = {k: {"achieved": round(v[0] / (v[1] * 1e-3) / 1e12, 3) if v[1] > 0 else None,
                  "ms": round(v[1], 3), "algorithmic_ops": int(v[0])} for k, v in kern.items()}
-    return {
+    out = {
         "kernel": dom,
         "bound": "int32-issue",
         "achieved": round(ach, 3),
@@ -200,10 +264,15 @@ def roofline_numbers(prof, hash_evals, n, clock_mhz, sms):
         "frac": round(ach / peak, 4),
         "traffic": ncu_traffic() if dom.startswith("tree_kernel") else None,
         "traffic_unit": "bytes per launch (dram read + write, profiles/ncu_tree_latest.csv)",
-        "peak_source": "nominal 128 int32 ops/clk/SM x %d SMs x 1965 MHz (no integer peak in MEASURED_PEAKS.json)" % sms,
-        "frac_at_run_clock": round(ach / (peak * clock_mhz / 1965.0), 4) if clock_mhz else None,
+        "peak_source": "nominal 128 int32 ops/clk/SM x %d SMs x 1965 MHz (MEASURED_PEAKS.json has no integer "
+                       "peak; the measured microbenchmark peak is int_peak_measured)" % sms,
+        "frac_at_run_clock": round(ach / (peak * clock_mhz / MAX_MHZ), 4) if clock_mhz else None,
         "per_kernel": other,
     }
+    if int_peak:
+        out["int_peak_measured"] = int_peak["measured_best_Tops"] * sms / int_peak["sms"]
+        out["frac_of_measured"] = round(ach / out["int_peak_measured"], 4)
+    return out
 
 
 def cpu_baseline_sample(seconds_target=15.0):
@@ -214,34 +283,40 @@ def cpu_baseline_sample(seconds_target=15.0):
     return refbuild.time_build_sample(seconds_target=seconds_target)
 
 
+def init_dist(world, local):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local if DIST_BACKEND == "nccl" else 0)
+    if DIST_BACKEND == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        os.environ["SHK_DEVICE"] = "0"
+        dist.init_process_group(DIST_BACKEND)
+
+
 def run_ours(args):
     rank, world, local = dist_info()
     os.environ.setdefault("SHK_DEVICE", str(local))
     # SHK_FORCE_SHARDED=1 runs the sharded (NCCL) path even at world size 1
     sharded = world > 1 or os.environ.get("SHK_FORCE_SHARDED") == "1"
     if sharded:
-        import torch
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local if DIST_BACKEND == "nccl" else 0)
-        if DIST_BACKEND == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            os.environ["SHK_DEVICE"] = "0"
-            dist.init_process_group(DIST_BACKEND)
+        init_dist(world, local)
     from paper_2308_09561_b200 import dist as shdist
     from paper_2308_09561_b200 import device as dev
     from paper_2308_09561_b200 import recsplit
-    from paper_2308_09561_b200 import workloads as W
 
     N, n, b = CFG["N"], CFG["n"], CFG["b"]
     k, blob = input_keys()
     sms = dev.num_sms()
+    int_peak = measure_int_peak(dev, sms)
+    int_peak["sms"] = sms
     # resident inputs: the master codes, computed once on the GPU
     d_blob = dev.DeviceBuffer.from_host(blob)
     d_hi = dev.DeviceBuffer(8 * N)
     d_lo = dev.DeviceBuffer(8 * N)
     dev.blake2b_fixed_device(d_blob, 8, N, 0, d_hi, d_lo)
+    d_blob.free()
     dev.sync()
 
     def step():
@@ -263,14 +338,16 @@ def run_ours(args):
     for _ in range(args.warmup):
         desc, prof = step()
     parity = {}
-    if rank == 0 and desc is not None:
-        blob_desc = desc.serialize()
-        parity["desc_sha256"] = hashlib.sha256(blob_desc).hexdigest()
-        gpath = os.path.join(ROOT, "tests", "golden", "c4.json")
-        if os.path.exists(gpath):
-            g = json.load(open(gpath))
-            parity["desc_matches_reference"] = parity["desc_sha256"] == g["desc_sha"]
-        parity["bits_per_key"] = round(len(blob_desc) * 8 / N, 6)
+    gpath = os.path.join(ROOT, "tests", "golden", "c4.json")
+    g4 = json.load(open(gpath)) if os.path.exists(gpath) else None
+    blob_desc = desc.serialize()
+    parity["desc_sha256"] = hashlib.sha256(blob_desc).hexdigest()
+    if g4:
+        ok = parity["desc_sha256"] == g4["desc_sha"]
+        parity["desc_matches_reference"] = bool(reduce_over_ranks(1.0 if ok else 0.0, world, "sum") == world)
+        if world > 1:
+            parity["desc_matches_reference_on_ranks"] = world if parity["desc_matches_reference"] else "some ranks differ"
+    parity["bits_per_key"] = round(len(blob_desc) * 8 / N, 6)
     barrier(world)
     dev.sync()
     launches0 = dev.launch_count()
@@ -292,7 +369,7 @@ def run_ours(args):
     value = N / (ms_step * 1e-3)
 
     # e2e through the public API with host buffers: the caller's pinned key
-    # blob in, serialized descriptor bytes out (rank 0); max wall over ranks
+    # blob in, serialized descriptor bytes out; max wall over ranks
     desc_bytes = 0
     out = None
     pinned = dev.PinnedBuffer.from_array(blob)  # the caller's key buffer, page-locked
@@ -302,7 +379,7 @@ def run_ours(args):
             d2, _ = shdist.build_blob_sharded(pinned.array, 8, b, n, CFG["mode"], device=coll_device())
         else:
             d2 = recsplit.build_blob(pinned.array, 8, b, n, CFG["mode"])
-        return d2.serialize() if d2 is not None else None
+        return d2.serialize()
 
     e2e_step()  # warm-up of the host-buffer path (copy stream, events, pinned pages)
     dev.sync()
@@ -312,9 +389,8 @@ def run_ours(args):
     try:
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            o = e2e_step()
-            if o is not None:
-                out, desc_bytes = o, len(o)
+            out = e2e_step()
+            desc_bytes = len(out)
         e2e_s = (time.perf_counter() - t0) / args.steps
     finally:
         gc.enable()
@@ -335,15 +411,18 @@ def run_ours(args):
     hash_evals_all = reduce_over_ranks(hash_evals_local or 0, world, "sum")
     split_evals_all = reduce_over_ranks(split_evals_exact, world, "sum")
     tree_ms_max = max_over_ranks(prof["phase_ms"]["split_search"] + prof["phase_ms"]["leaf_search"], world)
+    bucket_ms = max_over_ranks(prof["phase_ms"]["bucketize"], world)
+
+    # queries (C4: 1e8 keys drawn from the set): replicated descriptor, batch
+    # sharded by range over the ranks, device-resident
+    query = None
+    if args.queries > 0:
+        query = bench_queries(desc, k, args, dev, sms, rank, world, int_peak)
     leaf_lines = {}
     if args.leaf_configs:
         for cfg in [int(x) for x in args.leaf_configs.split(",") if x]:
-            leaf_lines[f"C{cfg}"] = bench_leaf(cfg, args, dev, sms, None, rank, world)
-
-    # queries (C4: 1e8 keys drawn from the set), device-resident
-    query = None
-    if rank == 0 and args.queries > 0 and desc is not None:
-        query = bench_queries(desc, k, args, dev, sms)
+            leaf_lines[f"C{cfg}"] = bench_leaf(cfg, args, dev, sms, rank, world, int_peak)
+    c2 = bench_c2(args, dev, rank) if (args.c2 and rank == 0) else None
 
     if rank != 0:
         return
@@ -356,6 +435,7 @@ def run_ours(args):
         prof["phase_ms"]["split_search"], prof["phase_ms"]["leaf_search"] = tree_ms_max, 0.0
     hash_evals = hash_evals_all if hash_evals_all else None
     clocks = clk.summary()
+    hbm, hbm_src = hbm_peak()
     line = {
         "metric": "keys/s MPHF build (ShockHash-RS, N=1e7, n=40, b=2000, rotate)",
         "value": round(value, 1),
@@ -370,73 +450,132 @@ def run_ours(args):
         "dtype": "u64",
         "data": "synthetic: default_rng(4) uniform 64-bit keys as 8-byte LE strings (the reference's recipe, SURVEY.md §8(d))",
         "config": {"workload": "C4: ShockHash-RS build N=10,000,000, leaf n=40, bucket b=2000, mode rotate, eps=0.05",
-                   "N": N, "n": n, "b": b, "parallelism": f"bucket-range x{world}" if world > 1 else "single GPU",
+                   "N": N, "n": n, "b": b,
+                   "parallelism": (f"bucket-range x{world} ({DIST_BACKEND})" if world > 1 else "single GPU"),
                    "l2": "inputs 160 MB of resident master codes + 160 MB working keys > 126 MB L2 (no flush needed)"},
         "clocks": clocks,
         "gpu_launches": int(launches),
         "wall_s_timed": round(wall, 3),
         "phase_ms": {k2: round(v, 3) for k2, v in prof["phase_ms"].items()},
-        "split_level_ms": prof.get("split_level_ms"),
         "parity": parity,
+        "e2e": e2e,
     }
-    if e2e:
-        line["e2e"] = e2e
     if hash_evals is not None:
-        line["roofline"] = roofline_numbers(prof, hash_evals, n, clocks.get("sm_mhz"), sms * world)
+        line["roofline"] = roofline_numbers(prof, hash_evals, n, clocks.get("sm_mhz"), sms * world, int_peak)
         if world > 1:
             line["roofline"]["peak_source"] += f" (all {world} GPUs)"
+    line["int_peak"] = {k2: v for k2, v in int_peak.items() if k2 != "sms"}
+    # bucketing (a3): 32 algorithmic bytes per key (read hi/lo, write sorted hi/lo)
+    line["bucketize"] = {"ms": round(bucket_ms, 3), "algorithmic_bytes": 32 * N,
+                         "GBps": round(32 * N / (bucket_ms * 1e-3) / 1e9, 1),
+                         "hbm_frac": round(32 * N / (bucket_ms * 1e-3) / 1e9 / hbm, 4), "hbm_peak_GBps": hbm,
+                         "peak_source": hbm_src, "note": "every rank bucket-sorts all N keys (no all-to-all)"}
     if query:
         line["query"] = query
     if leaf_lines:
         line["leaf_search"] = leaf_lines
+    if c2:
+        line["c2"] = c2
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
         except Exception as e:  # report, never crash the GPU line
             line["cpu_baseline"] = {"error": f"{type(e).__name__}: {e}"}
+        if not args.no_cpu_leaf:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import refleaf
+
+            for cfg in [int(x) for x in args.leaf_configs.split(",") if x]:
+                try:
+                    leaf_lines[f"C{cfg}"]["cpu_baseline"] = refleaf.time_leaf_config(cfg)
+                except Exception as e:
+                    leaf_lines[f"C{cfg}"]["cpu_baseline"] = {"error": f"{type(e).__name__}: {e}"}
+            if c2:
+                try:
+                    import refbuild
+
+                    c2["cpu_baseline"] = refbuild.time_build_c2()
+                except Exception as e:
+                    c2["cpu_baseline"] = {"error": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
 
 
-def bench_queries(desc, k, args, dev, sms):
+def bench_queries(desc, k, args, dev, sms, rank, world, int_peak):
+    """1e8 C4 queries: every rank holds the whole descriptor and answers the
+    range [Q r/W, Q (r+1)/W) of the batch (no exchange); time = max over
+    ranks.  Outputs are hashed in rank order on rank 0 for parity."""
     from paper_2308_09561_b200 import workloads as W
 
     Q = args.queries
-    idx = W.query_indices(4, Q)
+    q0, q1 = (Q * rank) // world, (Q * (rank + 1)) // world
+    Qr = q1 - q0
+    idx = W.query_indices(4, Q)[q0:q1]
     # master codes of the query keys (blake2b on the GPU from the key bytes)
     qblob = np.frombuffer(np.ascontiguousarray(k[idx], dtype="<u8").tobytes(), dtype=np.uint8)
     d_qblob = dev.DeviceBuffer.from_host(qblob)
-    d_qhi = dev.DeviceBuffer(8 * Q)
-    d_qlo = dev.DeviceBuffer(8 * Q)
-    dev.blake2b_fixed_device(d_qblob, 8, Q, desc.salt, d_qhi, d_qlo)
+    d_qhi = dev.DeviceBuffer(8 * max(Qr, 1))
+    d_qlo = dev.DeviceBuffer(8 * max(Qr, 1))
+    dev.blake2b_fixed_device(d_qblob, 8, Qr, desc.salt, d_qhi, d_qlo)
     d_qblob.free()
-    d_out = dev.DeviceBuffer(8 * Q)
+    d_out = dev.DeviceBuffer(8 * max(Qr, 1))
     dd = desc.device()
-    dd.query_device(d_qhi.ptr, d_qlo.ptr, Q, d_out.ptr)
+    dd.query_device(d_qhi.ptr, d_qlo.ptr, Qr, d_out.ptr)  # warm-up; node index decoded once per descriptor
     dev.sync()
+    barrier(world)
     reps = max(1, args.query_reps)
     with dev.timer() as tm:
         for _ in range(reps):
-            dd.query_device(d_qhi.ptr, d_qlo.ptr, Q, d_out.ptr)
-    ms = tm.ms / reps
-    res = {"queries": Q, "value": round(Q / (ms * 1e-3), 1), "unit": "queries/s", "ms": round(ms, 3)}
-    hbm = 24.0 * Q / (ms * 1e-3) / 1e9
-    res["hbm_GBps_algorithmic"] = round(hbm, 1)
-    res["hbm_frac_of_measured"] = round(hbm / 6531.9, 4)
+            dd.query_device(d_qhi.ptr, d_qlo.ptr, Qr, d_out.ptr)
+    ms = max_over_ranks(tm.ms / reps, world)
+    res = {"queries": Q, "value": round(Q / (ms * 1e-3), 1), "unit": "queries/s", "ms": round(ms, 3),
+           "ranks": world, "sharding": "replicated descriptor, batch range per rank" if world > 1 else "single GPU"}
+    hbm, hbm_src = hbm_peak()
+    gbs = 24.0 * Q / (ms * 1e-3) / 1e9
+    res["hbm_GBps_algorithmic"] = round(gbs, 1)
+    res["hbm_frac"] = round(gbs / (hbm * world), 4)
+    res["hbm_peak_source"] = hbm_src
+    nominal = INT_OPS_PER_CLK_SM * sms * world * MAX_MHZ * 1e6 / 1e12
+    ach = W_QUERY * Q / (ms * 1e-3) / 1e12
+    res["int_roofline"] = {"achieved": round(ach, 3), "peak": round(nominal, 2), "unit": "Tops/s",
+                           "frac": round(ach / nominal, 4),
+                           "frac_of_measured": round(ach / (int_peak["measured_best_Tops"] * world), 4),
+                           "work": f"{W_QUERY} int32 ops per query (SURVEY.md §8(d), derived node index)"}
+    res["untimed"] = "node_index_kernel (Rice stream decoded once per descriptor, ~70 us at C4) runs in the warm-up"
     if args.check:
-        out = d_out.download(np.uint64, Q)
-        qsha = hashlib.sha256(out.astype("<u8").tobytes()).hexdigest()
+        out = d_out.download(np.uint64, Qr)
+        qsha = sha_rank_order(out.astype("<u8"), world)
         gpath = os.path.join(ROOT, "tests", "golden", "c4.json")
-        if os.path.exists(gpath):
+        if rank == 0 and os.path.exists(gpath) and Q == CFG["queries"]:
             res["matches_reference"] = qsha == json.load(open(gpath))["query_sha"]
     for b_ in (d_qhi, d_qlo, d_out):
         b_.free()
     return res
 
 
-def bench_leaf(cfg, args, dev, sms, clock_mhz, rank=0, world=1):
+def leaf_golden(cfg):
+    """Full-population reference goldens (tests/golden/c{cfg}_full.bin, every
+    leaf: seed, f bits), else the small json sample."""
+    full = os.path.join(ROOT, "tests", "golden", f"c{cfg}_full.bin")
+    if os.path.exists(full):
+        meta = json.load(open(os.path.join(ROOT, "tests", "golden", f"c{cfg}_full.json")))
+        raw = open(full, "rb").read()
+        if hashlib.sha256(raw).hexdigest() != meta["file_sha256"]:
+            raise RuntimeError(f"{full}: sha256 mismatch")
+        L = meta["leaves"]
+        a = np.frombuffer(raw, dtype="<u8")
+        return a[:L].view("<i8"), a[L : 2 * L]
+    gpath = os.path.join(ROOT, "tests", "golden", f"c{cfg}.json")
+    if os.path.exists(gpath):
+        g = json.load(open(gpath))
+        return np.asarray(g["seeds"], dtype=np.int64), np.asarray(g["fbits"], dtype=np.uint64)
+    return None, None
+
+
+def bench_leaf(cfg, args, dev, sms, rank, world, int_peak):
     """Leaf-search-only configs (BASELINE configs C1/C3/C5): leaf seeds tested/s.
     At N > 1 rank r searches the contiguous leaf range [L r/N, L (r+1)/N) (no
-    exchange); seeds tested are summed and the time is the max over ranks."""
+    exchange); seeds tested are summed and the time is the max over ranks.
+    Every leaf is checked against the reference's seeds and f bits."""
     from paper_2308_09561_b200 import workloads as W
     from paper_2308_09561_b200._kernels import kernels as K
 
@@ -469,25 +608,100 @@ def bench_leaf(cfg, args, dev, sms, clock_mhz, rank=0, world=1):
             run()
     ms = max_over_ranks(tm.ms / reps, world)
     seeds = d_seed.download(np.int64, L)
+    fbits = d_fb.download(np.uint64, L)
     seeds_tested = reduce_over_ranks(float((seeds + 1).sum()), world, "sum")
     w_key = 50 if n <= 32 else 53
     ops = seeds_tested * (n * w_key + W_SEED)
-    peak = INT_OPS_PER_CLK_SM * sms * world * 1965e6 / 1e12
+    peak = INT_OPS_PER_CLK_SM * sms * world * MAX_MHZ * 1e6 / 1e12
+    ach = ops / (ms * 1e-3) / 1e12
+    mean = seeds_tested / L_all
     res = {"config": f"C{cfg}: {L_all} leaves x n={n}, plain" + (f", {world} GPUs x contiguous leaf ranges"
                                                                   if world > 1 else ""),
+           "kernel": "leaf_steal_kernel (seed-block work stealing)" if n > 24 else "leaf_kernel (fixed teams)",
            "seeds_tested": int(seeds_tested),
-           "mean_seeds_per_leaf": round(seeds_tested / L_all, 1), "ms": round(ms, 3),
+           "mean_seeds_per_leaf": round(mean, 1), "ms": round(ms, 3),
            "value": round(seeds_tested / (ms * 1e-3), 1), "unit": "leaf seeds tested/s",
-           "roofline": {"bound": "int32-issue", "achieved": round(ops / (ms * 1e-3) / 1e12, 3),
-                        "peak": round(peak, 2), "unit": "Tops/s", "frac": round(ops / (ms * 1e-3) / 1e12 / peak, 4),
+           "roofline": {"bound": "int32-issue", "achieved": round(ach, 3),
+                        "peak": round(peak, 2), "unit": "Tops/s", "frac": round(ach / peak, 4),
+                        "frac_of_measured": round(ach / (int_peak["measured_best_Tops"] * world), 4),
                         "work": f"(seed+1) x (n x {w_key} + {W_SEED}) int32 ops"}}
-    gpath = os.path.join(ROOT, "tests", "golden", f"c{cfg}.json")
-    if os.path.exists(gpath) and rank == 0:
-        g = json.load(open(gpath))
-        kk = min(len(g["seeds"]), L)  # the golden prefix inside rank 0's leaf range
-        res["parity"] = {"leaves_checked": kk, "seeds_match_reference": seeds[:kk].tolist() == g["seeds"][:kk],
-                         "fbits_match_reference": d_fb.download(np.uint64, kk).tolist() == g["fbits"][:kk]}
+    if cfg == 3:
+        res["mean_vs_models"] = {"measured": round(mean, 1), "paper_fig2": C3_FIG2_MEAN, "rice_model": C3_RICE_MODEL,
+                                 "theorem_4_5_bound": 28200}
+    gs, gf = leaf_golden(cfg)
+    if gs is not None:
+        a, z = l0, min(l1, len(gs))  # the golden leaves inside this rank's range
+        kk = max(0, z - a)
+        bad_s = int((seeds[:kk] != gs[a:z]).sum()) if kk else 0
+        bad_f = int((fbits[:kk] != gf[a:z]).sum()) if kk else 0
+        checked = reduce_over_ranks(kk, world, "sum")
+        bad_s = reduce_over_ranks(bad_s, world, "sum")
+        bad_f = reduce_over_ranks(bad_f, world, "sum")
+        res["parity"] = {"leaves_checked": int(checked), "of_leaves": L_all,
+                         "golden": "full population" if len(gs) == L_all else "prefix sample",
+                         "seed_mismatches": int(bad_s), "fbits_mismatches": int(bad_f),
+                         "seeds_match_reference": bad_s == 0, "fbits_match_reference": bad_f == 0}
     for b_ in (d_hi, d_lo, d_off, d_seed, d_fb):
+        b_.free()
+    return res
+
+
+def bench_c2(args, dev, rank):
+    """C2 (configs[1]): N=1e5, n=24, b=500 rotate build from resident codes and
+    end to end from the host key blob, then its 1e6 queries; parity against
+    the reference's descriptor bytes and query outputs (single GPU, rank 0)."""
+    from paper_2308_09561_b200 import recsplit
+    from paper_2308_09561_b200 import workloads as W
+
+    N, n, b = CFG2["N"], CFG2["n"], CFG2["b"]
+    k = W.build_keys(2)
+    blob = np.frombuffer(np.ascontiguousarray(k, dtype="<u8").tobytes(), dtype=np.uint8)
+    d_blob = dev.DeviceBuffer.from_host(blob)
+    d_hi, d_lo = dev.DeviceBuffer(8 * N), dev.DeviceBuffer(8 * N)
+    dev.blake2b_fixed_device(d_blob, 8, N, 0, d_hi, d_lo)
+    d_blob.free()
+    for _ in range(3):
+        desc = recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, N, b, n, CFG2["mode"])
+    reps = 10
+    dev.sync()
+    with dev.timer() as tm:
+        for _ in range(reps):
+            desc = recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, N, b, n, CFG2["mode"])
+    ms = tm.ms / reps
+    pinned_blob = blob.copy()
+    recsplit.build_blob(pinned_blob, 8, b, n, CFG2["mode"]).serialize()
+    t = time.perf_counter()
+    for _ in range(reps):
+        out = recsplit.build_blob(pinned_blob, 8, b, n, CFG2["mode"]).serialize()
+    e2e_s = (time.perf_counter() - t) / reps
+    res = {"config": "C2: ShockHash-RS build N=100,000, n=24, b=500, rotate, eps=0.05",
+           "value": round(N / (ms * 1e-3), 1), "unit": "keys/s", "ms": round(ms, 3),
+           "e2e": {"value": round(N / e2e_s, 1), "unit": "keys/s", "ms": round(e2e_s * 1e3, 3),
+                   "path": "recsplit.build_blob(host blob) -> serialize()"}}
+    # 1e6 queries
+    idx = W.query_indices(2)
+    Q = len(idx)
+    qblob = np.frombuffer(np.ascontiguousarray(k[idx], dtype="<u8").tobytes(), dtype=np.uint8)
+    d_qb = dev.DeviceBuffer.from_host(qblob)
+    d_qhi, d_qlo, d_out = dev.DeviceBuffer(8 * Q), dev.DeviceBuffer(8 * Q), dev.DeviceBuffer(8 * Q)
+    dev.blake2b_fixed_device(d_qb, 8, Q, desc.salt, d_qhi, d_qlo)
+    dd = desc.device()
+    dd.query_device(d_qhi.ptr, d_qlo.ptr, Q, d_out.ptr)
+    dev.sync()
+    with dev.timer() as tq:
+        for _ in range(reps):
+            dd.query_device(d_qhi.ptr, d_qlo.ptr, Q, d_out.ptr)
+    qms = tq.ms / reps
+    res["query"] = {"queries": Q, "value": round(Q / (qms * 1e-3), 1), "unit": "queries/s", "ms": round(qms, 4)}
+    qout = d_out.download(np.uint64, Q)
+    gpath = os.path.join(ROOT, "tests", "golden", "c2.json")
+    if os.path.exists(gpath):
+        g = json.load(open(gpath))
+        res["parity"] = {"desc_matches_reference": hashlib.sha256(out).hexdigest() == g["desc_sha"],
+                         "queries_match_reference": hashlib.sha256(qout.astype("<u8").tobytes()).hexdigest()
+                         == g["query_sha"],
+                         "bits_per_key": round(len(out) * 8 / N, 6)}
+    for b_ in (d_hi, d_lo, d_qb, d_qhi, d_qlo, d_out):
         b_.free()
     return res
 
@@ -505,7 +719,7 @@ def run_reference(args):
         "metric": "keys/s MPHF build (ShockHash-RS, N=1e7, n=40, b=2000, rotate)",
         "value": r["value"],
         "unit": "keys/s",
-        "n_gpus": world,
+        "n_gpus": max(world, args.gpus),
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": r["ms_per_step"],
@@ -523,6 +737,21 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def relaunch(nproc):
+    """`--gpus N` without a launcher: re-run this script under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous)."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log("bench.py: launching", nproc, "ranks:", " ".join(cmd))
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -534,16 +763,24 @@ def main():
     ap.add_argument("--check", action="store_true", default=True)
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-leaf", action="store_true", help="skip the reference leaf-search CPU baselines")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--leaf-configs", default="1,3,5", help="leaf-search-only configs to add (C1,C3,C5; C5 is one ~13 s launch)")
+    ap.add_argument("--leaf-configs", default="1,3,5", help="leaf-search-only configs to add (C1,C3,C5; C5 is one ~12 s launch)")
     ap.add_argument("--leaf-reps", type=int, default=3)
+    ap.add_argument("--no-c2", dest="c2", action="store_false", help="skip the C2 build + queries line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
+    rank, world, _ = dist_info()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args.gpus)
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting the launcher's world size")
+    run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

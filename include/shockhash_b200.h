@@ -71,9 +71,16 @@ int shk_ctx_num_sms(shk_ctx* ctx);
 enum {
   SHK_OPT_EXACT_SPLIT_EVALS = 0, /* 1: builds also count the reference's split `evals` (slower) */
   SHK_OPT_LEAF_TEAM_WARPS = 1,   /* warps per leaf in the per-level schedule (0 = heuristic) */
-  SHK_OPT_SCHEDULE = 2           /* 0: one persistent task-queue launch per build; 1: one launch per level */
+  SHK_OPT_SCHEDULE = 2,          /* 0: one persistent task-queue launch per build; 1: one launch per level */
+  SHK_OPT_LEAF_FIXED_TEAMS = 3   /* 1: batched PLAIN leaf search with a fixed team per leaf (no seed-block
+                                    stealing; A/B only) */
 };
 int shk_ctx_set_option(shk_ctx* ctx, int opt, int64_t value);
+/* Integer-issue microbenchmark (measurement only; the reference has no
+ * counterpart): one timed launch of 8 independent 32-bit chains per thread,
+ * 64 warps per SM.  kind 0: LOP3, 1: IMAD, 2: LOP3+IMAD 1:1, 3: SHF+LOP3+IMAD
+ * 2:1:1.  Returns the device time and the int32 ops executed. */
+int shk_int_peak(shk_ctx* ctx, int kind, int iters, double* ms_out, double* ops_out);
 /* Device memory from the context's caching pool (bench / zero-copy users). */
 int shk_dev_alloc(shk_ctx* ctx, size_t bytes, void** out);
 /* Page-locked host memory (host<->device copies at full PCIe/C2C rate, and

@@ -288,3 +288,27 @@ def time_build_sample(seconds_target=15.0, steps=1, warmup=0):
 
 if __name__ == "__main__":
     print(time_build_sample(float(sys.argv[1]) if len(sys.argv) > 1 else 10.0))
+
+
+def time_build_c2(steps=2):
+    """keys/s of the reference build of all of C2 (N=1e5, b=500, n=24,
+    rotate) with the pool over buckets (same orchestration as above)."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from paper_2308_09561_b200 import workloads as W  # input recipe only
+
+    if not have_ref():
+        return {"error": "oracle/_ref (the reference's compiled kernels) is missing"}
+    cores = os.cpu_count() or 1
+    keys = W.keys_as_bytes(W.build_keys(2))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        build_sample_ref(keys, 500, 24, pool)
+        ts = []
+        for _ in range(steps):
+            t = time.perf_counter()
+            build_sample_ref(keys, 500, 24, pool)
+            ts.append(time.perf_counter() - t)
+    sec = float(np.mean(ts))
+    return {"value": round(len(keys) / sec, 1), "unit": "keys/s", "cores": cores, "kind": "reference",
+            "sample": f"all of C2: master hash + bucket sort + 200 buckets (reference _core kernels, restated "
+                      f"recsplit loop, {cores} processes) + sequential ribbon", "ms_per_step": round(sec * 1e3, 1)}

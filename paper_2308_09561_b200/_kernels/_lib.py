@@ -65,6 +65,7 @@ _SIGS = {
     "shk_ctx_set_stream": (_I, [_P, _P]),
     "shk_ctx_num_sms": (_I, [_P]),
     "shk_ctx_set_option": (_I, [_P, _I, _I64]),
+    "shk_int_peak": (_I, [_P, _I, _I, _P, _P]),
     "shk_dev_alloc": (_I, [_P, ctypes.c_size_t, _P]),
     "shk_dev_free": (_I, [_P, _P]),
     "shk_host_alloc": (_I, [_P, ctypes.c_size_t, _P]),

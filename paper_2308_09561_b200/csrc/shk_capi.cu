@@ -345,11 +345,50 @@ int shk_leaf_search(shk_ctx* c, int mode, int cache_k, int cache_min_leaf, const
   p.team_warps = team_warps;
   p.num_sms = c->num_sms;
   p.stride = 1;
-  RC(shk_launch_leaf_search(p, c->stream));
+  DBuf steal_state(c), steal_active(c);
+  if (mode == 0 && team_warps == 0 && max_n > 24 && !stats_out && !c->opt[SHK_OPT_LEAF_FIXED_TEAMS]) {
+    // plain search: every warp on its own, 32-seed blocks handed out per
+    // leaf, idle warps join the last leaves (shk_leaf_steal.cu).  Leaves of
+    // <= 24 keys need a few hundred seeds at most: one warp each, no
+    // stealing (the fixed-team kernel).  Per-leaf counters (stats_out)
+    // come from the fixed-team kernel too.
+    const int max_active = c->num_sms * 64 + 1;
+    RC(steal_state.alloc(shk_leaf_steal_state_bytes(L)));
+    RC(steal_active.alloc((size_t)max_active * 8));
+    RC(shk_launch_leaf_steal(p, steal_state.p, steal_active.as<long long>(), max_active, c->stream));
+  } else {
+    RC(shk_launch_leaf_search(p, c->stream));
+  }
   RC(finish_out(c, flags, seed_out, tseed, (size_t)L * 8));
   RC(finish_out(c, flags, fbits_out, tfb, (size_t)L * 8));
   RC(finish_out(c, flags, stats_out, tst, (size_t)L * 32));
   if (!(flags & SHK_DEVICE)) RC(csync(c));
+  return 0;
+}
+
+int shk_int_peak(shk_ctx* c, int kind, int iters, double* ms_out, double* ops_out) {
+  if (iters <= 0) {
+    shk_set_error("iters must be positive");
+    return SHK_INVALID;
+  }
+  DBuf sink(c);
+  RC(sink.alloc(64));
+  int64_t threads = 0;
+  int per = 0;
+  cudaEvent_t e0, e1;
+  SHK_CUDA(cudaEventCreate(&e0));
+  SHK_CUDA(cudaEventCreate(&e1));
+  RC(shk_launch_int_peak(kind, iters, c->num_sms, sink.as<uint32_t>(), &threads, &per, c->stream));  // warm-up
+  SHK_CUDA(cudaEventRecord(e0, c->stream));
+  RC(shk_launch_int_peak(kind, iters, c->num_sms, sink.as<uint32_t>(), &threads, &per, c->stream));
+  SHK_CUDA(cudaEventRecord(e1, c->stream));
+  SHK_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  SHK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_out = ms;
+  *ops_out = (double)threads * (double)iters * (double)per;
   return 0;
 }
 

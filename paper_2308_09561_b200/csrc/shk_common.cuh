@@ -102,10 +102,12 @@ struct WarpChk {
   int cv[64];
 };
 
-SHK_D bool warp_pf_check(const uint16_t* ew, int L, int rot, int n, int lane, WarpChk& s) {
+// col[i * stride] = edge i of the candidate (warp_pf_check: the column of
+// lane L in a stride-32 edge table).
+SHK_D bool warp_pf_check_col(const uint16_t* col, int stride, int rot, int n, int lane, WarpChk& s) {
   int u0 = -1, v0 = 0, u1 = -1, v1 = 0;
   if (lane < n) {
-    uint32_t w = ew[lane * 32 + L];
+    uint32_t w = col[lane * stride];
     u0 = w & 0x7F;
     v0 = (w >> 8) & 0x7F;
     if (w & 0x8000u) {
@@ -116,7 +118,7 @@ SHK_D bool warp_pf_check(const uint16_t* ew, int L, int rot, int n, int lane, Wa
     }
   }
   if (lane + 32 < n) {
-    uint32_t w = ew[(lane + 32) * 32 + L];
+    uint32_t w = col[(lane + 32) * stride];
     u1 = w & 0x7F;
     v1 = (w >> 8) & 0x7F;
     if (w & 0x8000u) {
@@ -182,6 +184,10 @@ SHK_D bool warp_pf_check(const uint16_t* ew, int L, int rot, int n, int lane, Wa
   const bool ok = !__any_sync(FULL_WARP, bad);
   __syncwarp();
   return ok;
+}
+
+SHK_D bool warp_pf_check(const uint16_t* ew, int L, int rot, int n, int lane, WarpChk& s) {
+  return warp_pf_check_col(ew + L, 32, rot, n, lane, s);
 }
 
 // First accepted candidate in (lane, r) order among the lanes' candidate

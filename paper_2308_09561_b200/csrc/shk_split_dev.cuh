@@ -9,7 +9,12 @@
 namespace shk {
 
 // Key loads of the split searches: warp-uniform addresses (broadcast).
-SHK_D ulonglong2 load_key(const ulonglong2* p) { return __ldg(p); }
+// Plain coherent loads (L1-cached): inside the persistent tree kernel the
+// same key array is partitioned in place by other warps during the launch,
+// so the read-only (.nc) path is not allowed; the acquire fence a warp runs
+// before it reads a published node orders these loads after the parent's
+// partition stores.
+SHK_D ulonglong2 load_key(const ulonglong2* p) { return *p; }
 
 // Part index of split hash value r against cumulative bounds (up to 4 parts).
 SHK_D uint32_t part_of(uint32_t r, uint32_t b0, uint32_t b1, uint32_t b2) {

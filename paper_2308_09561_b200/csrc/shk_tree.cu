@@ -97,8 +97,13 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
   asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
   // lower slots take split tickets until the split region is used up, then
   // leaf tickets; upper slots take leaf tickets only
-  if ((int)wid >= t.idle_wid) return;
-  bool splits_done = (int)wid >= t.slow_wid;
+  // Progress must not depend on the slot numbering (%warpid is volatile and
+  // other kernels / MPS clients may hold the low slots): warp 0 of CTA 0 is
+  // always split-capable and never idles, so every split node -- and with it
+  // every leaf slot -- is eventually published whatever slots the warps get.
+  const bool anchor = blockIdx.x == 0 && w == 0;
+  if ((int)wid >= t.idle_wid && !anchor) return;
+  bool splits_done = (int)wid >= t.slow_wid && !anchor;
   for (;;) {
     unsigned long long h = 0;
     if (!splits_done) {

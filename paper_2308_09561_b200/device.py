@@ -100,11 +100,27 @@ class timer:
 OPT_EXACT_SPLIT_EVALS = 0
 OPT_LEAF_TEAM_WARPS = 1
 OPT_SCHEDULE = 2  # 0 persistent task queue (default), 1 one launch per tree level
+OPT_LEAF_FIXED_TEAMS = 3  # 1: plain batched leaf search with fixed teams (no seed-block stealing)
 
 
 def set_option(opt: int, value: int):
     """Context tuning/instrumentation option (include/shockhash_b200.h)."""
     check(_lib.load_library().shk_ctx_set_option(ctx(), int(opt), int(value)), "option")
+
+
+INT_PEAK_KINDS = {0: "LOP3", 1: "IMAD", 2: "LOP3+IMAD 1:1", 3: "SHF+LOP3+IMAD 2:1:1"}
+
+
+def int_peak(kind: int, iters: int = 4096):
+    """(ms, int32 ops) of one timed launch of the integer-issue
+    microbenchmark (csrc/shk_peak.cu; kinds in INT_PEAK_KINDS)."""
+    import ctypes
+
+    ms = ctypes.c_double()
+    ops = ctypes.c_double()
+    check(_lib.load_library().shk_int_peak(ctx(), int(kind), int(iters), ctypes.byref(ms), ctypes.byref(ops)),
+          "int peak")
+    return ms.value, ops.value
 
 
 def launch_count() -> int:

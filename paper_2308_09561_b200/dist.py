@@ -8,7 +8,9 @@ an all-gather of (stream bit length, stream words, per-bucket bit offsets,
 choice bits).  Concatenating the rank streams at their global bit offsets
 gives exactly the single-GPU stream (same preorder, same seeds), so the
 descriptor is bit-identical for any world size.  The ribbon is global (one
-system over all N keys) and is solved by rank 0.
+system over all N keys) and is solved column-sharded by all ranks; every
+rank ends with the whole (replicated) descriptor, so queries shard by batch
+range with no further exchange.
 
 The host-side merge is plain numpy (``merge_streams``) so the N>1 logic is
 tested on CPU with the gloo backend; the collective goes through
@@ -219,11 +221,24 @@ def ribbon_sharded(gb, choice_sorted, m, max_tries, device=None):
     raise RuntimeError(f"retrieval system unsolvable after {max_tries} seeds")
 
 
-def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8, epsilon=0.05, device=None):
+def agree_flag(flag, device=None) -> bool:
+    """True on every rank iff any rank's flag is set (all-reduce MAX): the
+    ranks' salt decisions must agree (recsplit.py:433-446)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([1 if flag else 0], dtype=torch.int64, device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return bool(t.item())
+
+
+def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8, epsilon=0.05, device=None, salt=0):
     """Bucket-range-sharded build over the current torch.distributed group.
 
-    Returns the descriptor on rank 0 (None elsewhere) and this rank's
-    device-time profile."""
+    Every rank returns the whole descriptor (replicated: the stream, the
+    bucket table and the ribbon words are all-gathered) and its own
+    device-time profile.  Equal 128-bit codes on any rank raise
+    HashCollisionError on every rank (the caller's salt loop retries)."""
     import time
 
     import torch.distributed as dist
@@ -232,11 +247,15 @@ def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8,
     from . import shockhash as leaf_mod
     from ._kernels import kernels as K
 
+    recsplit._validate(n, b, mode)
+    if n_keys < 1:
+        raise recsplit.InvalidParameterError("key set must be non-empty")
     rank, world = dist.get_rank(), dist.get_world_size()
     t0 = time.perf_counter()
     nb = (n_keys + b - 1) // b
     gb = K.GpuBuild(None, None, nb, hi_ptr=hi_ptr, lo_ptr=lo_ptr, n=n_keys)
-    if gb.duplicate:
+    if agree_flag(gb.duplicate, device):
+        gb.close()
         raise recsplit.HashCollisionError("equal 128-bit codes in the input")
     key_prefix = gb.key_prefix()
     b0, b1 = shard_range(nb, rank, world)
@@ -259,35 +278,75 @@ def build_hashed_device_sharded(hi_ptr, lo_ptr, n_keys, b, n, mode=1, cache_k=8,
     else:
         choice = gb.choice_sorted(int(key_prefix[b0]), int(key_prefix[b1]))
         sw, bl, bit_offsets, choice_all = exchange_and_merge(words, bit_len, rel, choice, device)
-    desc = None
     m = retrieval._columns(n_keys, epsilon)
     if RIBBON_SHARDED:
         rseed, rwords = ribbon_sharded(gb, choice_all, m, retrieval.RETRY_CAP, device)
-    elif rank == 0:
-        rseed, rwords = gb.ribbon(m, retrieval.RETRY_CAP, choice=choice_all, sorted_keys=True)
-    if rank == 0:
-        ribbon = retrieval.RibbonSystem(epsilon, rseed, m, rwords)
-        desc = recsplit.MphfDescriptor(n_keys, b, n, mode, cache_k, 0, leaf_g, key_prefix, bit_offsets, sw, bl, ribbon)
-        desc.build_stats = {"build_seconds": time.perf_counter() - t0}
+    else:  # rank 0 solves alone, then the words are shared
+        if rank == 0:
+            rseed, rwords = gb.ribbon(m, retrieval.RETRY_CAP, choice=choice_all, sorted_keys=True)
+            mine = np.concatenate([np.asarray([rseed], dtype=np.uint64), np.asarray(rwords, dtype=np.uint64)])
+        else:
+            mine = np.zeros(0, dtype=np.uint64)
+        got = allgather_arrays(mine, device)[0]
+        rseed, rwords = int(got[0]), got[1:].copy()
+    ribbon = retrieval.RibbonSystem(epsilon, rseed, m, rwords)
+    desc = recsplit.MphfDescriptor(n_keys, b, n, mode, cache_k, salt, leaf_g, key_prefix, bit_offsets, sw, bl, ribbon)
+    desc.build_stats = {"build_seconds": time.perf_counter() - t0}
     phase, split_evals = gb.phase_ms()
     gb.close()
     return desc, {"phase_ms": phase, "split_evals": split_evals, "buckets": (b0, b1),
                   "hash_evals": int(st[0]), "filter_passes": int(st[1]), "leaf_count": int(st[6])}
 
 
-def build_blob_sharded(blob, key_len, b, n, mode=1, cache_k=8, epsilon=0.05, device=None):
+def build_blob_sharded(blob, key_len, b, n, mode=1, cache_k=8, epsilon=0.05, device=None, fingerprint=None):
     """recsplit.build_blob over the process group: every rank fingerprints the
     host key blob (H2D pipelined with blake2b) and builds its bucket range;
-    rank 0 returns the descriptor (salt 0; a duplicate code raises)."""
-    from . import device as dev
+    every rank returns (descriptor, profile).
 
-    blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    The salt loop is the single-GPU one (recsplit.py:433-446): equal codes on
+    any rank move every rank to the next salt together (all-reduce MAX of
+    the duplicate flag); if the input holds a repeated key every rank raises
+    DuplicateKeyError, and HashCollisionError after SALT_RETRY_CAP salts.
+    ``fingerprint(blob, key_len, N, salt, d_hi, d_lo)`` replaces the blake2b
+    stage (tests force a collision with it)."""
+    from . import device as dev
+    from . import recsplit
+
+    blob = np.ascontiguousarray(np.frombuffer(blob, dtype=np.uint8) if isinstance(blob, (bytes, bytearray)) else blob,
+                                dtype=np.uint8)
     n_keys = len(blob) // key_len
+    if n_keys == 0:
+        raise recsplit.InvalidParameterError("key set must be non-empty")
+    recsplit._validate(n, b, mode)
+    fp = fingerprint if fingerprint is not None else dev.blake2b_fixed_from_host
     d_hi = dev.DeviceBuffer(8 * n_keys)
     d_lo = dev.DeviceBuffer(8 * n_keys)
     try:
-        dev.blake2b_fixed_from_host(blob, key_len, n_keys, 0, d_hi, d_lo)
-        return build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, n_keys, b, n, mode, cache_k, epsilon, device)
+        for salt in range(recsplit.SALT_RETRY_CAP):
+            fp(blob, key_len, n_keys, salt, d_hi, d_lo)
+            try:
+                return build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, n_keys, b, n, mode, cache_k, epsilon, device,
+                                                   salt=salt)
+            except recsplit.HashCollisionError:
+                pass
+            keys = [bytes(blob[i * key_len : (i + 1) * key_len]) for i in range(n_keys)]
+            dups = recsplit._find_duplicates(keys)
+            if dups:
+                raise recsplit.DuplicateKeyError(f"{len(dups)} duplicate key(s), first at line {dups[0] + 1}", dups)
+        raise recsplit.HashCollisionError(f"master hash collisions persist after {recsplit.SALT_RETRY_CAP} salts")
     finally:
         d_hi.free()
         d_lo.free()
+
+
+def query_sharded(desc, hi_ptr, lo_ptr, Q, out_ptr):
+    """Replicated descriptor, sharded batch: this rank
+    answers queries [Q r/W, Q (r+1)/W) of a batch whose device arrays it
+    holds; returns that range."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    q0, q1 = (Q * rank) // world, (Q * (rank + 1)) // world
+    if q1 > q0:
+        desc.device().query_device(hi_ptr + 8 * q0, lo_ptr + 8 * q0, q1 - q0, out_ptr + 8 * q0)
+    return q0, q1

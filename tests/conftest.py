@@ -33,3 +33,19 @@ def hashed_leaf(n, gen_seed):
 
     hi, lo = synthetic_hashed(n, gen_seed)
     return [HashedKey(int(a), int(b)) for a, b in zip(hi, lo)]
+
+
+def full_leaf_golden(cfg):
+    """(seeds i64[L], fbits u64[L], passes u64[L], meta) of every leaf of a
+    leaf-only config, made by the reference's compiled search_plain + orient
+    (tests/golden/make_leaf_full.py); the file's sha256 is checked."""
+    import hashlib
+
+    meta = golden(f"c{cfg}_full.json")
+    with open(os.path.join(GOLDEN, f"c{cfg}_full.bin"), "rb") as f:
+        raw = f.read()
+    assert hashlib.sha256(raw).hexdigest() == meta["file_sha256"]
+    L = meta["leaves"]
+    a = np.frombuffer(raw, dtype="<u8")
+    assert a.size == 3 * L
+    return a[:L].view("<i8"), a[L : 2 * L], a[2 * L :], meta

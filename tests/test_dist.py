@@ -133,3 +133,38 @@ def test_boundary_maps_compose_like_the_serial_chain():
     for mp in reversed(maps):
         z = apply_map(mp, z)
     assert (np.unpackbits(z.view(np.uint8), bitorder="little")[:127] == v).all()
+
+
+def _worker_flag(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2308_09561_b200.dist import agree_flag
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # only rank 1 sees equal codes: both ranks must move to the next salt
+        q.put((rank, (agree_flag(rank == 1), agree_flag(False))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_salt_agreement():
+    import socket
+
+    import torch.multiprocessing as tmp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_flag, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    out = dict(q.get(timeout=5) for _ in range(2))
+    assert out == {0: (True, False), 1: (True, False)}

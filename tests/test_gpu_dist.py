@@ -142,8 +142,64 @@ def test_sharded_build_matches_reference(world):
         out[r] = (sha, buckets)
     for p in procs:
         p.join(timeout=60)
-    assert out[0][0] == golden("c2.json")["desc_sha"]
-    assert all(out[r][0] is None for r in range(1, world))
+    # every rank holds the whole (replicated) descriptor
+    assert all(out[r][0] == golden("c2.json")["desc_sha"] for r in range(world))
     # the ranks' bucket ranges tile [0, nb)
     ranges = sorted(out[r][1] for r in range(world))
     assert ranges[0][0] == 0 and all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+
+
+def _worker_salt(rank, world, port, q, case):
+    """The sharded salt loop (recsplit.py:433-446): a forced code collision at
+    salt 0 moves every rank to salt 1; a repeated key raises
+    DuplicateKeyError on every rank."""
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["SHK_DEVICE"] = "0"
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_2308_09561_b200 import device as dev
+        from paper_2308_09561_b200 import dist as shdist
+        from paper_2308_09561_b200 import recsplit
+        from paper_2308_09561_b200 import workloads as W
+
+        keys = W.build_keys(2)[:20000].copy()
+        if case == "dup":
+            keys[7] = keys[5]
+        blob = np.frombuffer(np.ascontiguousarray(keys, dtype="<u8").tobytes(), dtype=np.uint8)
+        N = len(keys)
+        salts = []
+
+        def collide_at_salt0(bl, kl, n_keys, salt, d_hi, d_lo):
+            dev.blake2b_fixed_from_host(bl, kl, n_keys, salt, d_hi, d_lo)
+            salts.append(salt)
+            if salt == 0 and case == "collide":
+                hi, lo = d_hi.download(np.uint64, n_keys), d_lo.download(np.uint64, n_keys)
+                hi[0], lo[0] = hi[1], lo[1]  # two distinct keys, one 128-bit code
+                d_hi.upload(hi)
+                d_lo.upload(lo)
+
+        try:
+            desc, _ = shdist.build_blob_sharded(blob, 8, 500, 24, 1, fingerprint=collide_at_salt0)
+        except Exception as e:  # noqa: BLE001 - the test compares the class
+            q.put((rank, (type(e).__name__, salts)))
+            return
+        # the single-GPU build of the same keys at the salt the ranks agreed on
+        d_hi, d_lo = dev.DeviceBuffer(8 * N), dev.DeviceBuffer(8 * N)
+        dev.blake2b_fixed_from_host(blob, 8, N, desc.salt, d_hi, d_lo)
+        one = recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, N, 500, 24, 1, salt=desc.salt).serialize()
+        q.put((rank, (desc.salt, salts, desc.serialize() == one)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_salt_retry_on_collision():
+    out = _spawn(_worker_salt, 2, "collide")
+    assert out == {0: (1, [0, 1], True), 1: (1, [0, 1], True)}
+
+
+def test_sharded_duplicate_key_raises_on_every_rank():
+    out = _spawn(_worker_salt, 2, "dup")
+    assert out == {0: ("DuplicateKeyError", [0]), 1: ("DuplicateKeyError", [0])}

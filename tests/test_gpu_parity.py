@@ -108,6 +108,57 @@ def test_leaf_config_golden(K, cfg, sample):
         assert sha(seeds.astype("<i8").tobytes() + fb.astype("<u8").tobytes())[:16] == g["sha16"]
 
 
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_leaf_config_full_population(K, cfg):
+    """Every leaf of C3 (100,000 x n=32) and C5 (20,000 x n=56) against the
+    reference's own minimum seed, f bits and filter-pass counter."""
+    import os
+
+    from conftest import GOLDEN, full_leaf_golden
+    from paper_2308_09561_b200 import workloads as W
+
+    if not os.path.exists(os.path.join(GOLDEN, f"c{cfg}_full.json")):
+        pytest.skip(f"c{cfg}_full golden not generated")
+    gs, gf, gp, meta = full_leaf_golden(cfg)
+    hi, lo = W.leaf_inputs(cfg)
+    n = meta["n"]
+    off = np.arange(0, n * (meta["leaves"] + 1), n)
+    seeds, fb, st = K.leaf_search_batch(hi, lo, off, 0)
+    bad = np.flatnonzero(seeds != gs)
+    assert bad.size == 0, (bad[:10], seeds[bad[:10]], gs[bad[:10]])
+    assert (fb == gf).all(), np.flatnonzero(fb != gf)[:10]
+    assert (st[:, 0] == (gs + 1) * n).all()
+    assert (st[:, 1].astype(np.uint64) == gp).all() and (st[:, 2] == st[:, 1]).all()
+    assert sha(seeds.astype("<i8").tobytes() + fb.astype("<u8").tobytes())[:16] == meta["sha16"]
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_leaf_config_full_population_device(K, cfg):
+    """The bench path (device pointers, no stats) on every leaf of C3 / C5."""
+    import os
+
+    from conftest import GOLDEN, full_leaf_golden
+    from paper_2308_09561_b200 import device as dev
+    from paper_2308_09561_b200 import workloads as W
+
+    if not os.path.exists(os.path.join(GOLDEN, f"c{cfg}_full.json")):
+        pytest.skip(f"c{cfg}_full golden not generated")
+    gs, gf, _, meta = full_leaf_golden(cfg)
+    hi, lo = W.leaf_inputs(cfg)
+    L, n = meta["leaves"], meta["n"]
+    bufs = [dev.DeviceBuffer.from_host(np.ascontiguousarray(x).ravel()) for x in (hi, lo)]
+    d_off = dev.DeviceBuffer.from_host(np.arange(0, (L + 1) * n, n, dtype=np.int64))
+    d_seed, d_fb = dev.DeviceBuffer(8 * L), dev.DeviceBuffer(8 * L)
+    try:
+        K.leaf_search_device(bufs[0].ptr, bufs[1].ptr, d_off.ptr, L, 0, d_seed.ptr, d_fb.ptr)
+        dev.sync()
+        assert (d_seed.download(np.int64, L) == gs).all()
+        assert (d_fb.download(np.uint64, L) == gf).all()
+    finally:
+        for b_ in bufs + [d_off, d_seed, d_fb]:
+            b_.free()
+
+
 def test_split_search_golden(K):
     from paper_2308_09561_b200.keys import synthetic_hashed
 

@@ -14,6 +14,8 @@ from paper_2308_09561_b200 import device as dev
 from paper_2308_09561_b200 import workloads as W
 from paper_2308_09561_b200._kernels import kernels as K
 
+if os.environ.get("SHK_LEAF_FIXED") == "1":  # A/B: fixed team per leaf, no seed-block stealing
+    dev.set_option(dev.OPT_LEAF_FIXED_TEAMS, 1)
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 spec = W.LEAF_CONFIGS[cfg]
 L = int(sys.argv[2]) if len(sys.argv) > 2 else spec["leaves"]
