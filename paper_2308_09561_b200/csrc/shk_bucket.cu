@@ -182,6 +182,170 @@ __global__ void __launch_bounds__(256) bucket_sort_bins_kernel(const ulonglong2*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory path (nb <= BK_MAX_NB buckets, buckets <= BK_MAX_SORT keys,
+// N < 2^32): three streaming passes and no global atomics.
+//   1. bk_hist: CTA c of G histograms its contiguous key chunk in shared
+//      memory and writes the counts column-wise, M[b * G + c];
+//   2. an exclusive scan of M (bucket-major) gives every (bucket, CTA) its
+//      write offset in the bucket-sorted array; key_prefix[b] = M[b * G];
+//   3. bk_scatter: CTA c re-reads its chunk, recomputes the bucket hash (no
+//      bucket-id array) and places each key at its (bucket, CTA) cursor,
+//      advanced with shared-memory atomics;
+//   4. bk_sort: one CTA per bucket stages the bucket in shared memory,
+//      distributes it over 4096 bins by the top 12 bits of hi, and every
+//      key's final position is its bin start + the number of keys of its
+//      bin that sort before it by (hi, lo) (~0.5 other keys per bin at
+//      b = 2000); equal codes share a bin and raise the duplicate flag.
+// Traffic: 16 B read (1) + 32 B (3) + 32 B (4) per key, plus M.
+constexpr int BK_G = 296;            // CTAs of the histogram / scatter passes
+constexpr int BK_MAX_NB = 40960;     // shared-memory histogram limit (160 KB)
+constexpr int BK_MAX_SORT = 11264;   // keys per bucket staged in shared memory
+
+SHK_D uint32_t bucket_of_d(uint64_t hi, uint64_t lo, u2 x, uint32_t nb) {
+  return __umulhi(remix_d(split64(hi), split64(lo), x).hi, nb);
+}
+
+__global__ void __launch_bounds__(512) bk_hist_kernel(const uint64_t* hi, const uint64_t* lo, int64_t N, uint32_t nb,
+                                                      int64_t* M) {
+  extern __shared__ uint32_t h[];
+  const int G = gridDim.x, c = blockIdx.x;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const u2 x = split64(seed_mixer(0, TAG_BUCKET));
+  const int64_t c0 = N * c / G, c1 = N * (c + 1) / G;
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&h[bucket_of_d(hi[i], lo[i], x, nb)], 1u);
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) M[(int64_t)b * G + c] = h[b];
+}
+
+// key_prefix[b] = offset of (b, CTA 0); key_prefix[nb] = N; and the largest bucket.
+__global__ void bk_prefix_kernel(const int64_t* Moff, int G, int64_t nb, int64_t* prefix, int64_t* maxv) {
+  int64_t m = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = Moff[b * G];
+    prefix[b] = v;
+    if (b < nb) m = max(m, Moff[(b + 1) * G] - v);
+  }
+  atomicMax((unsigned long long*)maxv, (unsigned long long)m);
+}
+
+// L2 policies of the scatter: its 16-byte stores land in random bucket
+// slots, so a 32-byte sector is completed by a later store of another CTA;
+// the destination lines are kept in L2 (evict_last) until they fill, and the
+// streamed inputs are dropped first (evict_first), instead of partial
+// sectors going to DRAM as read-modify-writes.
+SHK_D uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+SHK_D uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+SHK_D uint64_t ld_hint_u64(const uint64_t* a, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+SHK_D void st_hint_u64x2(ulonglong2* a, ulonglong2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(a), "l"(v.x), "l"(v.y), "l"(pol)
+               : "memory");
+}
+SHK_D ulonglong2 ld_hint_u64x2(const ulonglong2* a, uint64_t pol) {
+  ulonglong2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+
+#ifndef SHK_BUCKET_L2HINT
+#define SHK_BUCKET_L2HINT 1
+#endif
+__global__ void __launch_bounds__(512) bk_scatter_kernel(const uint64_t* hi, const uint64_t* lo, int64_t N,
+                                                         uint32_t nb, const int64_t* Moff, ulonglong2* out) {
+  extern __shared__ uint32_t cur[];
+  const int G = gridDim.x, c = blockIdx.x;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cur[b] = (uint32_t)Moff[(int64_t)b * G + c];
+  __syncthreads();
+  const u2 x = split64(seed_mixer(0, TAG_BUCKET));
+  const int64_t c0 = N * c / G, c1 = N * (c + 1) / G;
+  const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    const uint64_t a = SHK_BUCKET_L2HINT ? ld_hint_u64(hi + i, stream) : hi[i];
+    const uint64_t z = SHK_BUCKET_L2HINT ? ld_hint_u64(lo + i, stream) : lo[i];
+    const uint32_t p = atomicAdd(&cur[bucket_of_d(a, z, x, nb)], 1u);
+    if (SHK_BUCKET_L2HINT)
+      st_hint_u64x2(out + p, make_ulonglong2(a, z), keep);
+    else
+      out[p] = make_ulonglong2(a, z);
+  }
+}
+
+__global__ void __launch_bounds__(256) bk_sort_kernel(const ulonglong2* in, const int64_t* prefix, int64_t nb,
+                                                      ulonglong2* out, int* dup_flag) {
+  extern __shared__ __align__(16) unsigned char bk_smem[];
+  int* cur = reinterpret_cast<int*>(bk_smem);                                   // [4096]
+  ulonglong2* A = reinterpret_cast<ulonglong2*>(bk_smem + SORT_BINS * 4);       // [cnt]
+  __shared__ int wsum[8];
+  for (int64_t bu = blockIdx.x; bu < nb; bu += gridDim.x) {
+    const int64_t s0 = prefix[bu];
+    const int cnt = (int)(prefix[bu + 1] - s0);
+    if (cnt == 0) continue;
+    uint16_t* B = reinterpret_cast<uint16_t*>(A + cnt);  // [cnt] bin-ordered key indices
+    for (int i = threadIdx.x; i < SORT_BINS; i += blockDim.x) cur[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const ulonglong2 k = SHK_BUCKET_L2HINT ? ld_hint_u64x2(in + s0 + i, policy_evict_first()) : in[s0 + i];
+      A[i] = k;
+      atomicAdd(&cur[(int)(k.x >> 52)], 1);
+    }
+    __syncthreads();
+    {  // exclusive scan of the 4096 bin counts (16 per thread)
+      const int t = threadIdx.x, base = t * (SORT_BINS / 256);
+      int loc[SORT_BINS / 256], run = 0;
+#pragma unroll
+      for (int k = 0; k < SORT_BINS / 256; ++k) {
+        loc[k] = run;
+        run += cur[base + k];
+      }
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL_WARP, incl, o);
+        if ((t & 31) >= o) incl += v;
+      }
+      if ((t & 31) == 31) wsum[t >> 5] = incl;
+      __syncthreads();
+      int woff = 0;
+      for (int w = 0; w < (t >> 5); ++w) woff += wsum[w];
+      const int excl = woff + incl - run;
+#pragma unroll
+      for (int k = 0; k < SORT_BINS / 256; ++k) cur[base + k] = excl + loc[k];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) B[atomicAdd(&cur[(int)(A[i].x >> 52)], 1)] = (uint16_t)i;
+    __syncthreads();
+    // cur[bin] is the end of the bin, its start the previous bin's end
+    for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
+      const ulonglong2 k = A[B[p]];
+      const int bin = (int)(k.x >> 52);
+      const int a = bin ? cur[bin - 1] : 0, e = cur[bin];
+      int r = a;
+      for (int q = a; q < e; ++q) {
+        if (q == p) continue;
+        const ulonglong2 o = A[B[q]];
+        const bool eq = o.x == k.x && o.y == k.y;
+        if (eq) atomicOr(dup_flag, 1);
+        r += key_less(o, k) || (eq && q < p);
+      }
+      out[s0 + r] = k;
+    }
+    __syncthreads();
+  }
+}
+
 // Fallback for buckets larger than the shared-memory sort: rank by counting
 // (O(cnt^2) per bucket, correct for any size; only reached with huge b).
 __global__ void bucket_rank_kernel(const ulonglong2* in, int64_t s0, int cnt, ulonglong2* out, int* dup_flag) {
@@ -243,13 +407,77 @@ int shk_launch_choice_sorted(const uint64_t* keys, const uint64_t* sorted, const
 
 size_t shk_bucketize_scratch(int64_t N, int64_t nb) {
   size_t s = 0;
+  // shared-memory path: M and its scan (nb * BK_G + 1 each) + scan scratch
+  const int64_t nm = nb * BK_G + 1;
+  size_t sm_path = ((size_t)nm * 8 + 255) & ~(size_t)255;
+  sm_path *= 2;
+  sm_path += ((size_t)N * 16 + 255) & ~(size_t)255;
+  sm_path += 256 + shk_scan_scratch(nm);
   s += ((size_t)N * 4 + 255) & ~(size_t)255;        // bucket ids
   s += ((size_t)N * 16 + 255) & ~(size_t)255;       // unsorted scatter
   s += ((size_t)(nb + 1) * 8 + 255) & ~(size_t)255;  // counts
   s += ((size_t)(nb + 1) * 8 + 255) & ~(size_t)255;  // cursor
   s += 256;                                          // max
   s += shk_scan_scratch(nb);
-  return s;
+  return s > sm_path ? s : sm_path;
+}
+
+// The shared-memory path; returns 1 when it does not apply (caller falls back).
+static int bucketize_smem(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nb, ulonglong2* out,
+                          int64_t* prefix, int* dup_flag, void* scratch, int64_t* max_bucket_out, cudaStream_t st,
+                          uint64_t* h_prefix, int* handled) {
+  *handled = 0;
+  if (nb > BK_MAX_NB || N >= (int64_t(1) << 32) || N < BK_G) return 0;
+  const int64_t nm = nb * BK_G + 1;
+  char* p = (char*)scratch;
+  int64_t* M = (int64_t*)p;
+  p += ((size_t)nm * 8 + 255) & ~(size_t)255;
+  int64_t* Moff = (int64_t*)p;
+  p += ((size_t)nm * 8 + 255) & ~(size_t)255;
+  ulonglong2* unsorted = (ulonglong2*)p;
+  p += ((size_t)N * 16 + 255) & ~(size_t)255;
+  int64_t* maxv = (int64_t*)p;
+  p += 256;
+  void* scan_scratch = p;
+  const size_t hsm = (size_t)nb * 4;
+  // (per call: the attribute is per device)
+  SHK_CUDA(cudaFuncSetAttribute(bk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BK_MAX_NB * 4));
+  SHK_CUDA(cudaFuncSetAttribute(bk_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BK_MAX_NB * 4));
+  SHK_CUDA(cudaFuncSetAttribute(bk_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                SORT_BINS * 4 + BK_MAX_SORT * 18 + 16));
+  SHK_CUDA(cudaMemsetAsync(maxv, 0, 8, st));
+  SHK_CUDA(cudaMemsetAsync(dup_flag, 0, sizeof(int), st));
+  SHK_CUDA(cudaMemsetAsync(M + nb * BK_G, 0, 8, st));
+  bk_hist_kernel<<<BK_G, 512, hsm, st>>>(hi, lo, N, (uint32_t)nb, M);
+  SHK_LAUNCHED();
+  int rc = shk_exclusive_scan_i64(M, Moff, nb * BK_G, scan_scratch, shk_scan_scratch(nm), st);
+  if (rc) return rc;
+  bk_prefix_kernel<<<(unsigned)((nb + 256) / 256 < 148 ? (nb + 256) / 256 : 148), 256, 0, st>>>(Moff, BK_G, nb,
+                                                                                                 prefix, maxv);
+  SHK_LAUNCHED();
+  int64_t maxb = 0;
+  if (h_prefix) {
+    SHK_CUDA(cudaMemcpyAsync(h_prefix, prefix, (size_t)(nb + 1) * 8, cudaMemcpyDeviceToHost, st));
+  }
+  SHK_CUDA(cudaMemcpyAsync(&maxb, maxv, 8, cudaMemcpyDeviceToHost, st));
+  // the largest bucket picks the sort kernel; the caller's host work overlaps
+  // the scatter and the sort (only the histogram and the scan are waited for)
+  SHK_CUDA(cudaStreamSynchronize(st));
+  if (max_bucket_out) *max_bucket_out = maxb;
+  bk_scatter_kernel<<<BK_G, 512, hsm, st>>>(hi, lo, N, (uint32_t)nb, Moff, unsorted);
+  SHK_LAUNCHED();
+  if (maxb > BK_MAX_SORT) {
+    int64_t grid = nb < 148 * 8 ? nb : 148 * 8;
+    bucket_sort_bins_kernel<<<(unsigned)grid, 256, 0, st>>>(unsorted, prefix, nb, out, dup_flag);
+    SHK_LAUNCHED();
+  } else {
+    const size_t ssm = SORT_BINS * 4 + (size_t)maxb * 18 + 16;
+    int64_t grid = nb < 148 * 16 ? nb : 148 * 16;
+    bk_sort_kernel<<<(unsigned)grid, 256, ssm, st>>>(unsorted, prefix, nb, out, dup_flag);
+    SHK_LAUNCHED();
+  }
+  *handled = 1;
+  return 0;
 }
 
 int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nb, uint64_t* skeys_u64,
@@ -262,6 +490,15 @@ int shk_bucketize(const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nb,
   if (nb <= 0 || nb > 0xFFFFFFFFll) {
     shk_set_error("bad bucket count");
     return 3;
+  }
+#ifndef SHK_BUCKET_SMEM
+#define SHK_BUCKET_SMEM 1
+#endif
+  if (SHK_BUCKET_SMEM) {
+    int handled = 0;
+    int rc = bucketize_smem(hi, lo, N, nb, (ulonglong2*)skeys_u64, (int64_t*)key_prefix, dup_flag, scratch,
+                            max_bucket_out, st, h_prefix, &handled);
+    if (rc || handled) return rc;
   }
   char* p = (char*)scratch;
   uint32_t* bid = (uint32_t*)p;

@@ -26,6 +26,9 @@
 //      chunk's boundary), a fully parallel map (step 3 stored the forms).
 #include <cuda_pipeline.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "shk_common.cuh"
 #include "shk_kernels.h"
 
@@ -713,9 +716,27 @@ int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c
   for (int pass = 0;;) {
     for (int k = 0; k < BATCH; ++k, ++pass) {
       SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 8, st));
+      static const bool trace = getenv("SHK_RIBBON_TRACE") != nullptr;  // analysis: per-pass counts + times
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (trace) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+      }
       ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(pass == 0 ? cur : b.rows2, b.rowoff, nch, M, b.sp0, b.sp1,
                                                         b.occ, b.sb, b.ovf, b.cnt, bad, (first && pass == 0) ? 1 : 0);
       SHK_LAUNCHED();
+      if (trace) {
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        int64_t h2[2];
+        cudaMemcpy(h2, b.cnt, 16, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "ribbon pass %d: elim %.1f us, rows overflowing %lld\n", pass, ms * 1e3, (long long)h2[0]);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      }
       int rc = rib_regroup(b, b.ovf, b.cnt, M, c0, st);
       if (rc) return rc;
     }
