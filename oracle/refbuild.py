@@ -192,7 +192,7 @@ def build_bucket(args):
                 bounds.append(bounds[-1] + sz)
             for i in range(len(sizes) - 1, -1, -1):
                 stack.append((bounds[i], bounds[i + 1]))
-    return w.bit_len, shi, slo, choice
+    return w.bit_len, shi, slo, choice, w.words
 
 
 def master_hash_many(keys, salt=0):  # keys.py:46-58
@@ -238,6 +238,62 @@ def build_sample_ref(keys, b, n, pool):
         if K.ribbon_solve(st, p0, p1, choice, m) is not None:
             return bits, seed
     raise RuntimeError("ribbon unsolvable")
+
+
+def build_descriptor_ref(keys, b, n, pool, eps=0.05, cache_k=8):
+    """The whole reference build (rotate mode, salt 0) -> serialized
+    descriptor bytes (format of recsplit.py:295-308).  Same orchestration as
+    build_sample_ref; pinned to the stock reference's build() by
+    tests/test_oracle.py::test_refbuild_matches_stock_reference."""
+    K = ref_kernels()
+    N = len(keys)
+    hi, lo = master_hash_many(keys)
+    nb = (N + b - 1) // b
+    bucket = K.hash_range_batch(K.remix_batch(hi, lo, 0, 4), nb).astype(np.int64)
+    order = np.lexsort((lo, hi, bucket))
+    shi, slo = hi[order], lo[order]
+    kp = np.zeros(nb + 1, dtype=np.int64)
+    kp[1:] = np.cumsum(np.bincount(bucket, minlength=nb))
+    tasks = [(shi[kp[i] : kp[i + 1]], slo[kp[i] : kp[i + 1]], n, 0) for i in range(nb) if kp[i + 1] > kp[i]]
+    res = iter(pool.map(build_bucket, tasks, chunksize=1))
+    bit_offsets = np.zeros(nb + 1, dtype=np.int64)
+    stream = 0  # the concatenated stream as one big integer, LSB first
+    total = 0
+    parts = []
+    for i in range(nb):
+        bit_offsets[i] = total
+        if kp[i + 1] > kp[i]:
+            bl, bhi, blo, ch, words = next(res)
+            for k, wd in enumerate(words):
+                stream |= int(wd) << (total + 64 * k)
+            stream &= (1 << (total + bl)) - 1
+            total += bl
+            parts.append((bhi, blo, ch))
+    bit_offsets[nb] = total
+    nw = (total + 63) // 64
+    words = np.array([(stream >> (64 * k)) & ((1 << 64) - 1) for k in range(nw)], dtype=np.uint64)
+    shi = np.concatenate([p[0] for p in parts])
+    slo = np.concatenate([p[1] for p in parts])
+    choice = np.concatenate([p[2] for p in parts])
+    m = max(128, int(np.ceil((1.0 + eps) * N)))
+    for seed in range(64):
+        st, p0, p1 = K.ribbon_rows(shi, slo, seed, m)
+        rw = K.ribbon_solve(st, p0, p1, choice, m)
+        if rw is not None:
+            break
+    else:
+        raise RuntimeError("ribbon unsolvable")
+    leaf_g = [leaf_rice_param(x) for x in range(n + 1)]
+    width = 32 if N < 2**32 and total < 2**32 else 64
+    out = bytearray(b"SHKH")
+    out += struct.pack("<HBQIBBBBQ", 1, 1, N, b, n, 1, cache_k, width, 0)
+    out += struct.pack("<B", n) + bytes(leaf_g[1:])
+    fmt = "<II" if width == 32 else "<QQ"
+    for i in range(nb + 1):
+        out += struct.pack(fmt, int(kp[i]), int(bit_offsets[i]))
+    out += struct.pack("<Q", total) + words.astype("<u8").tobytes()
+    out += struct.pack("<IQQ", int(round(eps * 65536)), seed, m) + np.asarray(rw, dtype="<u8").tobytes()
+    return bytes(out)
 
 
 def time_build_sample(seconds_target=15.0, steps=1, warmup=0):

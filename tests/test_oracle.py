@@ -3,13 +3,14 @@ vectors.  CPU only; these make the oracle a trustworthy checker for the
 GPU parity tests."""
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
 
 import oracle
 import oracle.host as OH
-from conftest import golden
+from conftest import ROOT, golden
 
 
 def sha(b):
@@ -176,3 +177,33 @@ def test_enumeration_census_pinned():
     for r in golden("experiments.json")["enumerate"]:
         assert (census(r["n"], 1), census(r["n"], 2)) == (r["pf_count"], r["sum_2c"])
     assert census(0, 1) == 1 and census(0, 2) == 1
+
+
+def test_refbuild_matches_stock_reference():
+    """The reference CPU arm (oracle/refbuild.py: the reference's compiled
+    kernels under a restated build loop with a process pool) produces the
+    STOCK reference's descriptor bytes: pinned on the first 100,000 C4 keys
+    (b=2000, n=40, rotate) against shockhash.build from the unmodified
+    package installed in baseline/_ref."""
+    import multiprocessing as mp
+    import sys
+
+    ref_site = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_site, "shockhash")):
+        pytest.skip("reference package not installed in baseline/_ref")
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refbuild
+
+    if not refbuild.have_ref():
+        pytest.skip("oracle/_ref not built")
+    if ref_site not in sys.path:
+        sys.path.insert(0, ref_site)
+    import shockhash
+
+    from paper_2308_09561_b200 import workloads as W
+
+    keys = W.keys_as_bytes(W.raw_keys(4, 100_000))
+    stock = shockhash.build(keys, 2000, 40).serialize()
+    with mp.get_context("fork").Pool(min(8, os.cpu_count() or 1)) as pool:
+        mine = refbuild.build_descriptor_ref(keys, 2000, 40, pool)
+    assert mine == stock
