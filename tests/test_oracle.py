@@ -89,6 +89,28 @@ def test_c5_sample_golden():
     assert seeds.tolist() == g["seeds"][:4]
 
 
+@pytest.mark.parametrize("cfg,count", [(3, 400), (5, 6)])
+def test_full_population_golden_sample(cfg, count):
+    """The C oracle on a sample of the full-population reference goldens
+    (tests/golden/c{3,5}_full.bin): random C3 leaves, and the C5 leaves with
+    the smallest seeds (so the CPU search stays short)."""
+    from conftest import full_leaf_golden
+    from paper_2308_09561_b200 import workloads as W
+
+    gs, gf, gp, meta = full_leaf_golden(cfg)
+    n = meta["n"]
+    if cfg == 3:
+        idx = np.sort(np.random.default_rng(33).choice(meta["leaves"], count, replace=False))
+    else:
+        idx = np.sort(np.argsort(gs, kind="stable")[:count])
+    hi, lo = W.leaf_inputs(cfg)
+    for i in idx:
+        t = oracle.search_plain(hi[i], lo[i], n, 1 << 40)
+        assert t[0] == int(gs[i]) and t[2] == int(gp[i]), (cfg, int(i))
+        assert oracle.orient(oracle.edges_plain(hi[i], lo[i], t[0], n), n) == int(gf[i])
+    assert int((gs + 1).sum()) == meta["seeds_tested"]
+
+
 def test_split_golden():
     for r in golden("split.json")["cases"]:
         hi, lo = synthetic_hashed(r["m"], r["gen"])
