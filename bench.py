@@ -21,7 +21,8 @@ Buckets are sharded by range over ranks (strong scaling, total N fixed); one
 all-gather joins streams and choice bits; the ranks solve the global ribbon
 column-sharded (dist.ribbon_sharded) and every rank ends with the whole
 descriptor.  Queries: replicated descriptor, batch sharded by range.  Leaf
-configs: contiguous leaf ranges per rank.  Time = max over ranks.
+configs C3/C5: one leaf queue shared by all ranks (a CUDA IPC counter, see
+dist.SharedLeafQueue); C1: contiguous leaf ranges.  Time = max over ranks.
 ``SHK_DIST_BACKEND=gloo`` runs the N ranks on one GPU (functional check).
 
 ``--impl reference`` times the reference's CPU implementation of the same
@@ -179,6 +180,19 @@ def sha_rank_order(arr, world):
     t = torch.from_numpy(raw.copy() if raw.size else np.zeros(1, np.uint8)).to(dev)
     dist.send(t, dst=0)
     return None
+
+
+def gather_ints(x, world):
+    """[x of rank 0, x of rank 1, ...] on every rank."""
+    if world == 1:
+        return [x]
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([int(x)], dtype=torch.int64, device=coll_device())
+    out = [torch.zeros(1, dtype=torch.int64, device=coll_device()) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [int(o.item()) for o in out]
 
 
 def input_keys():
@@ -581,7 +595,10 @@ def bench_leaf(cfg, args, dev, sms, rank, world, int_peak):
 
     spec = W.LEAF_CONFIGS[cfg]
     L_all, n = spec["leaves"], spec["n"]
-    l0, l1 = (L_all * rank) // world, (L_all * (rank + 1)) // world
+    # N > 1 and the stealing kernel (n > 24): one cross-GPU leaf queue, every
+    # rank holds all leaves (dist.SharedLeafQueue); else contiguous ranges
+    shared = world > 1 and n > 24 and os.environ.get("SHK_LEAF_SHARED", "1") != "0"
+    l0, l1 = (0, L_all) if shared else ((L_all * rank) // world, (L_all * (rank + 1)) // world)
     L = l1 - l0
     if cfg == 5:
         fp = np.random.default_rng(5).integers(0, 2**64, (L_all, n, 2), dtype=np.uint64)[l0:l1]
@@ -597,26 +614,41 @@ def bench_leaf(cfg, args, dev, sms, rank, world, int_peak):
     d_off = dev.DeviceBuffer.from_host(np.arange(0, (L + 1) * n, n, dtype=np.int64))
     d_seed = dev.DeviceBuffer(8 * L)
     d_fb = dev.DeviceBuffer(8 * L)
-    run = lambda: K.leaf_search_device(d_hi.ptr, d_lo.ptr, d_off.ptr, L, 0, d_seed.ptr, d_fb.ptr)
-    if cfg != 5:
-        run()  # warm-up
-    dev.sync()
-    barrier(world)
     reps = 1 if cfg == 5 else max(1, args.leaf_reps)
-    with dev.timer() as tm:
-        for _ in range(reps):
-            run()
-    ms = max_over_ranks(tm.ms / reps, world)
-    seeds = d_seed.download(np.int64, L)
-    fbits = d_fb.download(np.uint64, L)
-    seeds_tested = reduce_over_ranks(float((seeds + 1).sum()), world, "sum")
+    if shared:
+        from paper_2308_09561_b200 import dist as shdist
+
+        with shdist.SharedLeafQueue(coll_device()) as q:
+            if cfg != 5:
+                q.search(d_hi.ptr, d_lo.ptr, d_off.ptr, L, d_seed.ptr, d_fb.ptr)  # warm-up
+            ms = sum(q.search(d_hi.ptr, d_lo.ptr, d_off.ptr, L, d_seed.ptr, d_fb.ptr) for _ in range(reps)) / reps
+            ms = max_over_ranks(ms, world)
+            mine = int((d_seed.download(np.int64, L) >= -1).sum())
+            seeds, fbits = q.combine(d_seed.download(np.int64, L), d_fb.download(np.uint64, L))
+        per_rank = [int(x) for x in gather_ints(mine, world)]
+        seeds_tested = float((seeds + 1).sum())
+    else:
+        run = lambda: K.leaf_search_device(d_hi.ptr, d_lo.ptr, d_off.ptr, L, 0, d_seed.ptr, d_fb.ptr)
+        if cfg != 5:
+            run()  # warm-up
+        dev.sync()
+        barrier(world)
+        with dev.timer() as tm:
+            for _ in range(reps):
+                run()
+        ms = max_over_ranks(tm.ms / reps, world)
+        seeds = d_seed.download(np.int64, L)
+        fbits = d_fb.download(np.uint64, L)
+        seeds_tested = reduce_over_ranks(float((seeds + 1).sum()), world, "sum")
+        per_rank = None
     w_key = 50 if n <= 32 else 53
     ops = seeds_tested * (n * w_key + W_SEED)
     peak = INT_OPS_PER_CLK_SM * sms * world * MAX_MHZ * 1e6 / 1e12
     ach = ops / (ms * 1e-3) / 1e12
     mean = seeds_tested / L_all
-    res = {"config": f"C{cfg}: {L_all} leaves x n={n}, plain" + (f", {world} GPUs x contiguous leaf ranges"
-                                                                  if world > 1 else ""),
+    how = (f", {world} GPUs x one shared leaf queue (CUDA IPC counter)" if shared else
+           f", {world} GPUs x contiguous leaf ranges" if world > 1 else "")
+    res = {"config": f"C{cfg}: {L_all} leaves x n={n}, plain" + how,
            "kernel": "leaf_steal_kernel (seed-block work stealing)" if n > 24 else "leaf_kernel (fixed teams)",
            "seeds_tested": int(seeds_tested),
            "mean_seeds_per_leaf": round(mean, 1), "ms": round(ms, 3),
@@ -625,12 +657,16 @@ def bench_leaf(cfg, args, dev, sms, rank, world, int_peak):
                         "peak": round(peak, 2), "unit": "Tops/s", "frac": round(ach / peak, 4),
                         "frac_of_measured": round(ach / (int_peak["measured_best_Tops"] * world), 4),
                         "work": f"(seed+1) x (n x {w_key} + {W_SEED}) int32 ops"}}
+    if per_rank is not None:
+        res["leaves_solved_per_rank"] = per_rank
     if cfg == 3:
         res["mean_vs_models"] = {"measured": round(mean, 1), "paper_fig2": C3_FIG2_MEAN, "rice_model": C3_RICE_MODEL,
                                  "theorem_4_5_bound": 28200}
     gs, gf = leaf_golden(cfg)
     if gs is not None:
         a, z = l0, min(l1, len(gs))  # the golden leaves inside this rank's range
+        if shared and rank != 0:  # every rank holds the combined result: rank 0 checks it
+            z = a
         kk = max(0, z - a)
         bad_s = int((seeds[:kk] != gs[a:z]).sum()) if kk else 0
         bad_f = int((fbits[:kk] != gf[a:z]).sum()) if kk else 0

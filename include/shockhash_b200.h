@@ -76,6 +76,21 @@ enum {
                                     stealing; A/B only) */
 };
 int shk_ctx_set_option(shk_ctx* ctx, int opt, int64_t value);
+/* Cross-GPU leaf queue for the batched PLAIN leaf search (no reference
+ * counterpart: the reference is single-threaded).  One rank allocates a
+ * device counter and exports its CUDA IPC handle (64 bytes); every rank
+ * opens it and sets it on its context; then every rank launches
+ * shk_leaf_search over ALL leaves (device buffers pre-set: seeds to a value
+ * < -1, fbits to 0) and the launches take leaves from the one counter (NVLink
+ * system-scope atomics), so the ranks finish together however the per-leaf
+ * seed counts fall.  Each leaf is written by exactly one rank; a MAX / SUM
+ * all-reduce of the seed / f-bit arrays completes every rank's copy.  The
+ * owner resets the counter (shk_ipc_counter_reset) before each batch. */
+int shk_ipc_counter_alloc(shk_ctx* ctx, void* handle_out, void** dev_ptr);
+int shk_ipc_counter_open(shk_ctx* ctx, const void* handle, void** dev_ptr);
+int shk_ipc_counter_close(shk_ctx* ctx, void* dev_ptr, int owner);
+int shk_ipc_counter_reset(shk_ctx* ctx, void* dev_ptr);
+int shk_ctx_set_leaf_counter(shk_ctx* ctx, void* dev_ptr); /* NULL: the context's own counter */
 /* Integer-issue microbenchmark (measurement only; the reference has no
  * counterpart): one timed launch of 8 independent 32-bit chains per thread,
  * 64 warps per SM.  kind 0: LOP3, 1: IMAD, 2: LOP3+IMAD 1:1, 3: SHF+LOP3+IMAD
@@ -89,6 +104,8 @@ int shk_host_alloc(shk_ctx* ctx, size_t bytes, void** out);
 int shk_host_free(shk_ctx* ctx, void* p);
 int shk_dev_free(shk_ctx* ctx, void* p);
 int shk_memcpy(shk_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /*0 H2D 1 D2H 2 D2D*/);
+/* Stream-ordered byte fill of device memory (value & 0xFF). */
+int shk_memset(shk_ctx* ctx, void* dst, int value, size_t bytes);
 /* Events on the context stream: elapsed milliseconds between two records. */
 int shk_timer_start(shk_ctx* ctx);
 int shk_timer_stop(shk_ctx* ctx, float* ms);

@@ -66,11 +66,17 @@ _SIGS = {
     "shk_ctx_num_sms": (_I, [_P]),
     "shk_ctx_set_option": (_I, [_P, _I, _I64]),
     "shk_int_peak": (_I, [_P, _I, _I, _P, _P]),
+    "shk_ipc_counter_alloc": (_I, [_P, _P, _P]),
+    "shk_ipc_counter_open": (_I, [_P, _P, _P]),
+    "shk_ipc_counter_close": (_I, [_P, _P, _I]),
+    "shk_ipc_counter_reset": (_I, [_P, _P]),
+    "shk_ctx_set_leaf_counter": (_I, [_P, _P]),
     "shk_dev_alloc": (_I, [_P, ctypes.c_size_t, _P]),
     "shk_dev_free": (_I, [_P, _P]),
     "shk_host_alloc": (_I, [_P, ctypes.c_size_t, _P]),
     "shk_host_free": (_I, [_P, _P]),
     "shk_memcpy": (_I, [_P, _P, _P, ctypes.c_size_t, _I]),
+    "shk_memset": (_I, [_P, _P, _I, ctypes.c_size_t]),
     "shk_timer_start": (_I, [_P]),
     "shk_timer_stop": (_I, [_P, _P]),
     "shk_launch_count": (_I64, [_P]),

@@ -58,6 +58,7 @@ struct shk_ctx {
   ShkRibbon* rib = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int64_t opt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // shk_ctx_set_option
+  int* shared_leaf_counter = nullptr;  // shk_ctx_set_leaf_counter (cross-GPU leaf queue)
 };
 
 static size_t round_up(size_t b) {
@@ -265,6 +266,10 @@ int shk_memcpy(shk_ctx* c, void* dst, const void* src, size_t bytes, int kind) {
   SHK_CUDA(cudaMemcpyAsync(dst, src, bytes, k, c->stream));
   return csync(c);
 }
+int shk_memset(shk_ctx* c, void* dst, int value, size_t bytes) {
+  SHK_CUDA(cudaMemsetAsync(dst, value, bytes, c->stream));
+  return 0;
+}
 int shk_timer_start(shk_ctx* c) {
   SHK_CUDA(cudaEventRecord(c->t0, c->stream));
   return 0;
@@ -355,7 +360,12 @@ int shk_leaf_search(shk_ctx* c, int mode, int cache_k, int cache_min_leaf, const
     const int max_active = c->num_sms * 64 + 1;
     RC(steal_state.alloc(shk_leaf_steal_state_bytes(L)));
     RC(steal_active.alloc((size_t)max_active * 8));
-    RC(shk_launch_leaf_steal(p, steal_state.p, steal_active.as<long long>(), max_active, c->stream));
+    int shared = 0;
+    if (c->shared_leaf_counter) {  // leaves handed out by a counter shared with other GPUs / processes
+      p.counter = c->shared_leaf_counter;
+      shared = 1;
+    }
+    RC(shk_launch_leaf_steal(p, steal_state.p, steal_active.as<long long>(), max_active, shared, c->stream));
   } else {
     RC(shk_launch_leaf_search(p, c->stream));
   }
@@ -363,6 +373,42 @@ int shk_leaf_search(shk_ctx* c, int mode, int cache_k, int cache_min_leaf, const
   RC(finish_out(c, flags, fbits_out, tfb, (size_t)L * 8));
   RC(finish_out(c, flags, stats_out, tst, (size_t)L * 32));
   if (!(flags & SHK_DEVICE)) RC(csync(c));
+  return 0;
+}
+
+// ---- cross-GPU leaf queue (CUDA IPC) ------------------------------------------
+int shk_ipc_counter_alloc(shk_ctx* c, void* handle_out, void** dev_ptr) {
+  int* p = nullptr;
+  SHK_CUDA(cudaSetDevice(c->device));
+  SHK_CUDA(cudaMalloc(&p, 256));
+  SHK_CUDA(cudaMemset(p, 0, 256));
+  cudaIpcMemHandle_t h;
+  SHK_CUDA(cudaIpcGetMemHandle(&h, p));
+  memcpy(handle_out, &h, sizeof(h));
+  *dev_ptr = p;
+  return 0;
+}
+int shk_ipc_counter_open(shk_ctx* c, const void* handle, void** dev_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  SHK_CUDA(cudaSetDevice(c->device));
+  SHK_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+int shk_ipc_counter_close(shk_ctx* c, void* dev_ptr, int owner) {
+  SHK_CUDA(cudaSetDevice(c->device));
+  if (owner)
+    SHK_CUDA(cudaFree(dev_ptr));
+  else
+    SHK_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return 0;
+}
+int shk_ipc_counter_reset(shk_ctx* c, void* dev_ptr) {
+  SHK_CUDA(cudaMemsetAsync(dev_ptr, 0, sizeof(int), c->stream));
+  return csync(c);
+}
+int shk_ctx_set_leaf_counter(shk_ctx* c, void* dev_ptr) {
+  c->shared_leaf_counter = (int*)dev_ptr;
   return 0;
 }
 

@@ -38,7 +38,8 @@ int shk_launch_leaf_search(const ShkLeafLaunch& p, cudaStream_t st);
 size_t shk_leaf_steal_state_bytes(int64_t L);
 int shk_launch_int_peak(int kind, int iters, int num_sms, uint32_t* sink, int64_t* threads_out, int* ops_per_step,
                         cudaStream_t st);
-int shk_launch_leaf_steal(const ShkLeafLaunch& p, void* state, long long* active, int max_active, cudaStream_t st);
+int shk_launch_leaf_steal(const ShkLeafLaunch& p, void* state, long long* active, int max_active, int shared_counter,
+                          cudaStream_t st);
 int shk_launch_orient(const uint8_t* eu, const uint8_t* ev, const int64_t* off, int64_t L, uint64_t* fbits, int* ok,
                       cudaStream_t st);
 

@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(128, 8) leaf_steal_kernel(LeafArgs a, StealLea
     bool owner = false;
     if (!tail) {
       long long l = 0;
-      if (lane == 0) l = atomicAdd(leaf_counter, 1);
+      // system scope: the counter may live on another GPU (CUDA IPC, NVLink
+      // atomics) and be shared by every rank's launch (cross-GPU leaf queue)
+      if (lane == 0) l = atomicAdd_system(leaf_counter, 1);
       l = __shfl_sync(FULL_WARP, l, 0);
       if (l < a.L) {
         leaf = l;
@@ -249,7 +251,7 @@ using namespace shk;
 
 size_t shk_leaf_steal_state_bytes(int64_t L) { return (size_t)L * sizeof(StealLeaf); }
 
-int shk_launch_leaf_steal(const ShkLeafLaunch& p, void* state, long long* active, int max_active,
+int shk_launch_leaf_steal(const ShkLeafLaunch& p, void* state, long long* active, int max_active, int shared_counter,
                           cudaStream_t st) {
   if (p.L <= 0) return 0;
   LeafArgs a{};
@@ -282,7 +284,7 @@ int shk_launch_leaf_steal(const ShkLeafLaunch& p, void* state, long long* active
   if (blocks * 4 + 1 > max_active) blocks = (max_active - 1) / 4;
   SHK_CUDA(cudaMemsetAsync(active, 0xFF, (size_t)blocks * 4 * sizeof(long long), st));
   SHK_CUDA(cudaMemsetAsync(active + blocks * 4, 0, sizeof(long long), st));  // owners searching
-  SHK_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(int), st));
+  if (!shared_counter) SHK_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(int), st));  // a shared one is reset by its owner
   kfn<<<(unsigned)blocks, 128, 0, st>>>(a, reinterpret_cast<StealLeaf*>(state), active, p.counter);
   SHK_LAUNCHED();
   return 0;

@@ -79,6 +79,11 @@ class PinnedBuffer:
             pass
 
 
+def memset_device(ptr: int, value: int, nbytes: int):
+    """Stream-ordered byte fill of device memory."""
+    check(_lib.load_library().shk_memset(ctx(), ptr, int(value), int(nbytes)), "memset")
+
+
 def sync():
     check(_lib.load_library().shk_ctx_sync(ctx()), "sync")
 

@@ -350,3 +350,96 @@ def query_sharded(desc, hi_ptr, lo_ptr, Q, out_ptr):
     if q1 > q0:
         desc.device().query_device(hi_ptr + 8 * q0, lo_ptr + 8 * q0, q1 - q0, out_ptr + 8 * q0)
     return q0, q1
+
+
+class SharedLeafQueue:
+    """Cross-GPU leaf queue (one device counter shared over CUDA IPC).
+
+    Rank 0 allocates the counter on its GPU and broadcasts its IPC handle;
+    every rank maps it and sets it on its library context, so each rank's
+    batched plain leaf search (the seed-block stealing kernel) takes leaves
+    from the same counter with system-scope atomics over NVLink.  Every rank
+    searches the whole leaf array; each leaf is solved by exactly one rank,
+    and the ranks finish together whatever the per-leaf seed counts are
+    (contiguous leaf ranges finish when their heaviest leaves do).  Use as a
+    context manager around ``search``."""
+
+    def __init__(self, device=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import device as dev
+        from ._kernels import _lib
+
+        self._L = _lib.load_library()
+        self._ctx = dev.ctx()
+        self.rank = dist.get_rank()
+        self.device = device
+        handle = ctypes.create_string_buffer(64)
+        ptr = ctypes.c_void_p()
+        if self.rank == 0:
+            dev.check(self._L.shk_ipc_counter_alloc(self._ctx, handle, ctypes.byref(ptr)), "ipc alloc")
+        obj = [bytes(handle.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, device=device if getattr(device, "type", "cpu") == "cuda" else None)
+        if self.rank != 0:
+            h = ctypes.create_string_buffer(obj[0], 64)
+            dev.check(self._L.shk_ipc_counter_open(self._ctx, h, ctypes.byref(ptr)), "ipc open")
+        self.ptr = ptr.value
+
+    def search(self, hi_ptr, lo_ptr, off_ptr, L, seeds_ptr, fbits_ptr, max_seed=1 << 40):
+        """All L leaves (device buffers; every rank holds all of them) with the
+        shared queue; returns the rank's kernel time in ms.  The output
+        buffers hold, after the call, only the leaves this rank solved: seeds
+        of the others are < -1, their f bits 0 (see ``combine``)."""
+        import torch.distributed as dist
+
+        from . import device as dev
+        from ._kernels import kernels as K
+
+        dist.barrier()  # every rank's previous search has finished before the owner resets the counter
+        dev.check(self._L.shk_ctx_set_leaf_counter(self._ctx, self.ptr), "set counter")
+        try:
+            if self.rank == 0:
+                dev.check(self._L.shk_ipc_counter_reset(self._ctx, self.ptr), "ipc reset")
+            dev.memset_device(seeds_ptr, 0xFE, 8 * L)
+            dev.memset_device(fbits_ptr, 0, 8 * L)
+            dev.sync()
+            dist.barrier()
+            with dev.timer() as tm:
+                K.leaf_search_device(hi_ptr, lo_ptr, off_ptr, L, 0, seeds_ptr, fbits_ptr, max_seed=max_seed)
+            dev.sync()
+        finally:
+            dev.check(self._L.shk_ctx_set_leaf_counter(self._ctx, None), "set counter")
+        return tm.ms
+
+    def combine(self, seeds, fbits):
+        """Every rank's full result from the per-rank partial arrays (host
+        numpy): MAX over the seeds (unsolved entries are < -1), SUM over the
+        f bits (unsolved entries are 0)."""
+        import torch
+        import torch.distributed as dist
+
+        dev_ = self.device if self.device is not None else torch.device("cpu")
+        s = torch.from_numpy(np.ascontiguousarray(seeds, dtype=np.int64)).to(dev_)
+        f = torch.from_numpy(np.ascontiguousarray(fbits).view(np.int64)).to(dev_)
+        dist.all_reduce(s, op=dist.ReduceOp.MAX)
+        dist.all_reduce(f, op=dist.ReduceOp.SUM)
+        return s.cpu().numpy(), f.cpu().numpy().view(np.uint64)
+
+    def close(self):
+        from . import device as dev
+
+        if self.ptr:
+            dev.check(self._L.shk_ipc_counter_close(self._ctx, self.ptr, 1 if self.rank == 0 else 0), "ipc close")
+            self.ptr = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        import torch.distributed as dist
+
+        dist.barrier()  # nobody still uses the owner's counter
+        self.close()
+        return False

@@ -203,3 +203,50 @@ def test_sharded_salt_retry_on_collision():
 def test_sharded_duplicate_key_raises_on_every_rank():
     out = _spawn(_worker_salt, 2, "dup")
     assert out == {0: ("DuplicateKeyError", [0]), 1: ("DuplicateKeyError", [0])}
+
+
+def _worker_shared_queue(rank, world, port, q, cfg, L):
+    """Two ranks take leaves from ONE counter mapped over CUDA IPC (on this
+    box both processes share the GPU; their kernels never wait on each
+    other, they only compete for leaves)."""
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["SHK_DEVICE"] = "0"
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_2308_09561_b200 import device as dev
+        from paper_2308_09561_b200 import dist as shdist
+        from paper_2308_09561_b200 import workloads as W
+
+        hi, lo = W.leaf_inputs(cfg, L)
+        n = W.LEAF_CONFIGS[cfg]["n"]
+        d_hi, d_lo = dev.DeviceBuffer.from_host(hi.ravel()), dev.DeviceBuffer.from_host(lo.ravel())
+        d_off = dev.DeviceBuffer.from_host(np.arange(0, (L + 1) * n, n, dtype=np.int64))
+        d_s, d_f = dev.DeviceBuffer(8 * L), dev.DeviceBuffer(8 * L)
+        out = []
+        with shdist.SharedLeafQueue() as sq:
+            for _ in range(2):  # the owner resets the counter between batches
+                sq.search(d_hi.ptr, d_lo.ptr, d_off.ptr, L, d_s.ptr, d_f.ptr)
+                s_part, f_part = d_s.download(np.int64, L), d_f.download(np.uint64, L)
+                mine = int((s_part >= -1).sum())
+                s, f = sq.combine(s_part, f_part)
+                out.append((mine, s.tolist(), f.tolist()))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,L", [(3, 6000), (5, 40)])
+def test_shared_leaf_queue_two_ranks(cfg, L):
+    from conftest import full_leaf_golden
+
+    gs, gf, _, _ = full_leaf_golden(cfg)
+    out = _spawn(_worker_shared_queue, 2, cfg, L)
+    for batch in range(2):
+        mine = out[0][batch][0] + out[1][batch][0]
+        assert mine == L  # every leaf solved by exactly one rank
+        for r in range(2):
+            assert out[r][batch][1] == gs[:L].tolist()
+            assert out[r][batch][2] == gf[:L].tolist()
