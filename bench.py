@@ -555,12 +555,30 @@ def bench_queries(desc, k, args, dev, sms, rank, world, int_peak):
                            "frac_of_measured": round(ach / (int_peak["measured_best_Tops"] * world), 4),
                            "work": f"{W_QUERY} int32 ops per query (SURVEY.md §8(d), derived node index)"}
     res["untimed"] = "node_index_kernel (Rice stream decoded once per descriptor, ~70 us at C4) runs in the warm-up"
+    # e2e through the public API with host buffers: the query keys' 8-byte
+    # strings (pinned) in, indices out (MphfDescriptor.query_blob: H2D,
+    # blake2b, query, D2H pipelined in chunks); max wall over ranks
+    pinned = dev.PinnedBuffer.from_array(qblob)
+    hout = dev.PinnedBuffer(8 * max(Qr, 1), dtype=np.uint64)
+    desc.query_blob(pinned.array, 8, out=hout.array[:Qr])  # warm-up
+    barrier(world)
+    t0 = time.perf_counter()
+    desc.query_blob(pinned.array, 8, out=hout.array[:Qr])
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    res["e2e"] = {"value": round(Q / e2e_s, 1), "unit": "queries/s", "ms": round(e2e_s * 1e3, 3),
+                  "h2d_bytes": 8 * Q, "d2h_bytes": 8 * Q,
+                  "path": "MphfDescriptor.query_blob(pinned 8-byte keys) -> indices in pinned host memory"}
+    e2e_ok = None
     if args.check:
         out = d_out.download(np.uint64, Qr)
+        e2e_ok = bool((hout.array[:Qr] == out).all())
         qsha = sha_rank_order(out.astype("<u8"), world)
         gpath = os.path.join(ROOT, "tests", "golden", "c4.json")
         if rank == 0 and os.path.exists(gpath) and Q == CFG["queries"]:
             res["matches_reference"] = qsha == json.load(open(gpath))["query_sha"]
+        res["e2e"]["outputs_equal_device_path"] = bool(reduce_over_ranks(1.0 if e2e_ok else 0.0, world, "sum") == world)
+    pinned.free()
+    hout.free()
     for b_ in (d_qhi, d_qlo, d_out):
         b_.free()
     return res

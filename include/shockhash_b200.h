@@ -291,6 +291,12 @@ int shk_qdesc_create(shk_ctx* ctx, int64_t n_keys, int64_t nbuckets, int mode, i
                      int64_t stream_nwords, int64_t stream_bit_len, const shk_plans* plans, uint64_t rib_seed,
                      int64_t rib_m, const uint64_t* rib_words, int64_t rib_nwords, shk_qdesc** out);
 int shk_query(shk_qdesc* d, const uint64_t* hi, const uint64_t* lo, int64_t Q, uint64_t* out, int clamp, int flags);
+/* MphfDescriptor.query_many(keys) end to end (recsplit.py:270-275): N
+ * fixed-length keys packed in a HOST buffer (page-locked for full PCIe
+ * rate) -> indices in a host array.  Chunks are copied in, fingerprinted
+ * (blake2b-128, salt) and queried on the device while the neighbouring
+ * chunks' copies run (two copy streams).  clamp as shk_query. */
+int shk_query_blob(shk_qdesc* q, const uint8_t* blob, int key_len, int64_t Q, uint64_t salt, uint64_t* out, int clamp);
 /* MphfDescriptor.verify (recsplit.py:383-394) on the device: query the Q
  * hashed keys (clamped) and check the outputs form a bijection onto [0, N).
  * *ok = 1 iff so; otherwise *offender = the first input index whose output is

@@ -438,6 +438,18 @@ class DeviceDescriptor:
         check(_L().shk_verify(self.handle, ptr(hi), ptr(lo), len(hi), 0, ctypes.byref(ok), ctypes.byref(off)), "verify")
         return bool(ok.value), int(off.value)
 
+    def query_blob(self, blob, key_len, salt, out=None, clamp=True):
+        """Indices of N fixed-length keys packed in a host buffer (ideally
+        page-locked): H2D, blake2b, query and D2H pipelined in chunks."""
+        blob = np.ascontiguousarray(blob, dtype=np.uint8)
+        Q = len(blob) // int(key_len)
+        if out is None:
+            out = np.empty(Q, dtype=np.uint64)
+        if Q:
+            check(_L().shk_query_blob(self.handle, ptr(blob), int(key_len), Q, int(salt), ptr(out), 1 if clamp else 0),
+                  "query")
+        return out
+
     def query_device(self, hi_ptr, lo_ptr, Q, out_ptr, clamp=True):
         """Stream-ordered query on device pointers (bench / zero-copy)."""
         check(_L().shk_query(self.handle, hi_ptr, lo_ptr, int(Q), out_ptr, 1 if clamp else 0, SHK_DEVICE), "query")

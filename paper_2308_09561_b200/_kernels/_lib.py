@@ -125,6 +125,7 @@ _SIGS = {
     "shk_build_destroy": (_I, [_P]),
     "shk_qdesc_create": (_I, [_P, _I64, _I64, _I, _I64, _P, _P, _P, _I64, _I64, _P, _U64, _I64, _P, _I64, _P]),
     "shk_query": (_I, [_P, _P, _P, _I64, _P, _I, _I]),
+    "shk_query_blob": (_I, [_P, _P, _I, _I64, _U64, _P, _I]),
     "shk_verify": (_I, [_P, _P, _P, _I64, _I, _P, _P]),
     "shk_qdesc_destroy": (_I, [_P]),
 }

@@ -13,6 +13,8 @@
 // the interleaved sorted keys and flags adjacent duplicates.
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "shk_common.cuh"
 #include "shk_kernels.h"
 
@@ -208,8 +210,12 @@ SHK_D uint32_t bucket_of_d(uint64_t hi, uint64_t lo, u2 x, uint32_t nb) {
   return __umulhi(remix_d(split64(hi), split64(lo), x).hi, nb);
 }
 
+constexpr int BK_SB = 16;  // buckets per super-bucket (the cluster path below)
+
+// Msb (optional): the CTA's key count per super-bucket of BK_SB buckets,
+// Msb[sb * G + c] (the first-level scatter of the cluster path).
 __global__ void __launch_bounds__(512) bk_hist_kernel(const uint64_t* hi, const uint64_t* lo, int64_t N, uint32_t nb,
-                                                      int64_t* M) {
+                                                      int64_t* M, int64_t* Msb) {
   extern __shared__ uint32_t h[];
   const int G = gridDim.x, c = blockIdx.x;
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
@@ -219,6 +225,14 @@ __global__ void __launch_bounds__(512) bk_hist_kernel(const uint64_t* hi, const 
   for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&h[bucket_of_d(hi[i], lo[i], x, nb)], 1u);
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) M[(int64_t)b * G + c] = h[b];
+  if (Msb) {
+    const uint32_t nsb = (nb + BK_SB - 1) / BK_SB;
+    for (uint32_t sb = threadIdx.x; sb < nsb; sb += blockDim.x) {
+      uint32_t t = 0;
+      for (uint32_t b = sb * BK_SB; b < sb * BK_SB + BK_SB && b < nb; ++b) t += h[b];
+      Msb[(int64_t)sb * G + c] = t;
+    }
+  }
 }
 
 // key_prefix[b] = offset of (b, CTA 0); key_prefix[nb] = N; and the largest bucket.
@@ -354,6 +368,208 @@ __global__ void __launch_bounds__(256) bk_sort_kernel(const ulonglong2* in, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster path (B200: thread-block clusters + distributed shared memory).
+// The scatter above writes 16-byte keys to random slots of 5,000 bucket
+// ranges, which reach DRAM as partial sectors (374 MB read + 254 MB written
+// for 160 MB of keys at C4).  Here the keys move in two coalesced steps:
+//   L1 (bk_l1_scatter): to their SUPER-bucket (BK_SB = 32 consecutive
+//      buckets, ~64k keys at C4) -- each CTA sorts a 2,048-key tile by
+//      super-bucket in shared memory and writes runs (~13 keys = 208 B);
+//   L2 (bk_cluster_sort): one cluster of BK_CL = 8 CTAs per super-bucket,
+//      each CTA owning BK_SB / BK_CL = 4 buckets: the CTAs read the
+//      super-bucket's range in eighths, count keys per bucket, exchange the
+//      counts through distributed shared memory, and store every key straight
+//      into the shared memory of the CTA that owns its bucket; after a
+//      cluster barrier each CTA sorts its buckets in its own shared memory
+//      (rank within 4096 top-bit bins, as bk_sort) and writes them out.
+// DRAM traffic: 16 B (hist) + 32 B (L1) + 32 B (L2) per key.
+constexpr int BK_CL = 16;              // cluster size (non-portable: set at launch)
+constexpr int BK_TILE = 2048;          // keys per L1 tile (512 threads x 4)
+
+// Exclusive scan of n <= 2048 ints in shared memory by 512 threads (4 each);
+// out[n] = total.  Both arrays in shared memory; ends synchronized.
+SHK_D void block_scan_2048(const uint32_t* in, uint32_t* out, int n, uint32_t* wsum) {
+  const int t = threadIdx.x, base = t * 4;
+  uint32_t v[4], run = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[k] = (base + k < n) ? in[base + k] : 0u;
+    run += v[k];
+  }
+  uint32_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL_WARP, incl, o);
+    if ((t & 31) >= o) incl += y;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = incl;
+  __syncthreads();
+  if (t < 32) {
+    uint32_t w = (t < 16) ? wsum[t] : 0u, wi = w;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL_WARP, wi, o);
+      if (t >= o) wi += y;
+    }
+    if (t < 16) wsum[t] = wi - w;  // exclusive warp offsets
+    if (t == 15) wsum[16] = wi;    // total
+  }
+  __syncthreads();
+  uint32_t e = wsum[t >> 5] + incl - run;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (base + k < n) out[base + k] = e;
+    e += v[k];
+  }
+  if (t == 0) out[n] = wsum[16];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(512) bk_l1_scatter_kernel(const uint64_t* hi, const uint64_t* lo, int64_t N,
+                                                            uint32_t nb, const int64_t* Msboff, ulonglong2* out) {
+  extern __shared__ __align__(16) unsigned char l1sm[];
+  const uint32_t nsb = (nb + BK_SB - 1) / BK_SB;
+  ulonglong2* stage = reinterpret_cast<ulonglong2*>(l1sm);                 // [BK_TILE]
+  uint16_t* ssb = reinterpret_cast<uint16_t*>(stage + BK_TILE);            // [BK_TILE]
+  uint32_t* cur = reinterpret_cast<uint32_t*>(ssb + BK_TILE);              // [nsb]
+  uint32_t* th = cur + nsb;                                                // [nsb]
+  uint32_t* toff = th + nsb;                                               // [nsb + 1]
+  __shared__ uint32_t wsum[17];
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
+  for (uint32_t sb = tid; sb < nsb; sb += blockDim.x) cur[sb] = (uint32_t)Msboff[(int64_t)sb * G + c];
+  const u2 x = split64(seed_mixer(0, TAG_BUCKET));
+  const uint64_t stream = policy_evict_first();
+  const int64_t c0 = N * c / G, c1 = N * (c + 1) / G;
+  for (int64_t base = c0; base < c1; base += BK_TILE) {
+    const int nt = (int)((c1 - base < BK_TILE) ? (c1 - base) : BK_TILE);
+    for (uint32_t sb = tid; sb < nsb; sb += blockDim.x) th[sb] = 0;
+    __syncthreads();
+    ulonglong2 k[4];
+    uint32_t sbk[4], r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = tid + u * 512;
+      sbk[u] = 0xFFFFu;
+      if (j < nt) {
+        const int64_t i = base + j;
+        k[u] = make_ulonglong2(ld_hint_u64(hi + i, stream), ld_hint_u64(lo + i, stream));
+        sbk[u] = bucket_of_d(k[u].x, k[u].y, x, nb) / BK_SB;
+        r[u] = atomicAdd(&th[sbk[u]], 1u);
+      }
+    }
+    __syncthreads();
+    block_scan_2048(th, toff, (int)nsb, wsum);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (sbk[u] != 0xFFFFu) {
+        const uint32_t p = toff[sbk[u]] + r[u];
+        stage[p] = k[u];
+        ssb[p] = (uint16_t)sbk[u];
+      }
+    }
+    __syncthreads();
+    // write the tile in super-bucket order: consecutive threads, consecutive slots
+    for (int t = tid; t < nt; t += blockDim.x) {
+      const uint32_t sb = ssb[t];
+      out[cur[sb] + (uint32_t)t - toff[sb]] = stage[t];
+    }
+    __syncthreads();
+    for (uint32_t sb = tid; sb < nsb; sb += blockDim.x) cur[sb] += toff[sb + 1] - toff[sb];
+    __syncthreads();
+  }
+}
+
+// One cluster of BK_CL CTAs per super-bucket; CTA k owns bucket BK_SB*sb + k.
+constexpr int BK_CBINS = 1024;  // top-10-bit bins of the in-cluster sort (~2 keys per bin at b = 2000)
+__global__ void __launch_bounds__(256)
+    bk_cluster_sort_kernel(const ulonglong2* in, const int64_t* prefix, int64_t nb, int cap, ulonglong2* out,
+                           int* dup_flag) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char csm[];
+  ulonglong2* keys = reinterpret_cast<ulonglong2*>(csm);            // [cap] this CTA's bucket
+  uint16_t* idx = reinterpret_cast<uint16_t*>(keys + cap);          // [cap]
+  int* bins = reinterpret_cast<int*>(idx + ((cap + 7) & ~7));      // [BK_CBINS]
+  __shared__ uint32_t cnt[BK_SB];  // keys of my input slice per bucket of the super-bucket (read remotely)
+  __shared__ uint32_t dst[BK_SB];  // my write cursor in each owner's key array
+  __shared__ int wsum[8];
+  const int kr = (int)cluster.block_rank(), tid = threadIdx.x;
+  const int64_t sb = blockIdx.x / BK_CL;
+  const int64_t b0 = sb * BK_SB, bend = (b0 + BK_SB < nb) ? b0 + BK_SB : nb;
+  const int64_t s0 = prefix[b0], s1 = prefix[bend];
+  if (tid < BK_SB) cnt[tid] = 0;
+  __syncthreads();
+  const u2 x = split64(seed_mixer(0, TAG_BUCKET));
+  const int64_t na = s1 - s0, a = s0 + na * kr / BK_CL, z = s0 + na * (kr + 1) / BK_CL;
+  for (int64_t i = a + tid; i < z; i += blockDim.x) {
+    const ulonglong2 k = in[i];
+    atomicAdd(&cnt[bucket_of_d(k.x, k.y, x, (uint32_t)nb) - (uint32_t)b0], 1u);
+  }
+  cluster.sync();  // every CTA's slice counts are final
+  if (tid < BK_SB) {
+    uint32_t base = 0;
+    for (int k2 = 0; k2 < kr; ++k2) base += cluster.map_shared_rank(cnt, k2)[tid];
+    dst[tid] = base;
+  }
+  __syncthreads();
+  for (int64_t i = a + tid; i < z; i += blockDim.x) {
+    const ulonglong2 k = in[i];
+    const uint32_t lb = bucket_of_d(k.x, k.y, x, (uint32_t)nb) - (uint32_t)b0;
+    const uint32_t slot = atomicAdd(&dst[lb], 1u);
+    cluster.map_shared_rank(keys, (int)lb)[slot] = k;  // DSMEM store into the bucket's CTA
+  }
+  cluster.sync();  // all keys have arrived; no remote access after this point
+  const int64_t b = b0 + kr;
+  if (b >= bend) return;
+  const int cntb = (int)(prefix[b + 1] - prefix[b]);
+  if (cntb == 0) return;
+  for (int i = tid; i < BK_CBINS; i += blockDim.x) bins[i] = 0;
+  __syncthreads();
+  for (int i = tid; i < cntb; i += blockDim.x) atomicAdd(&bins[(int)(keys[i].x >> 54)], 1);
+  __syncthreads();
+  {  // exclusive scan of the bin counts (4 per thread)
+    const int base = tid * (BK_CBINS / 256);
+    int loc[BK_CBINS / 256], run = 0;
+#pragma unroll
+    for (int q = 0; q < BK_CBINS / 256; ++q) {
+      loc[q] = run;
+      run += bins[base + q];
+    }
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL_WARP, incl, o);
+      if ((tid & 31) >= o) incl += v;
+    }
+    if ((tid & 31) == 31) wsum[tid >> 5] = incl;
+    __syncthreads();
+    int woff = 0;
+    for (int w = 0; w < (tid >> 5); ++w) woff += wsum[w];
+    const int excl = woff + incl - run;
+#pragma unroll
+    for (int q = 0; q < BK_CBINS / 256; ++q) bins[base + q] = excl + loc[q];
+  }
+  __syncthreads();
+  for (int i = tid; i < cntb; i += blockDim.x) idx[atomicAdd(&bins[(int)(keys[i].x >> 54)], 1)] = (uint16_t)i;
+  __syncthreads();
+  const int64_t o0 = prefix[b];
+  for (int p = tid; p < cntb; p += blockDim.x) {
+    const ulonglong2 k = keys[idx[p]];
+    const int bin = (int)(k.x >> 54);
+    const int lo_ = bin ? bins[bin - 1] : 0, hi_ = bins[bin];
+    int r = lo_;
+    for (int q = lo_; q < hi_; ++q) {
+      if (q == p) continue;
+      const ulonglong2 o = keys[idx[q]];
+      const bool eq = o.x == k.x && o.y == k.y;
+      if (eq) atomicOr(dup_flag, 1);
+      r += key_less(o, k) || (eq && q < p);
+    }
+    out[o0 + r] = k;
+  }
+}
+
 // Fallback for buckets larger than the shared-memory sort: rank by counting
 // (O(cnt^2) per bucket, correct for any size; only reached with huge b).
 __global__ void bucket_rank_kernel(const ulonglong2* in, int64_t s0, int cnt, ulonglong2* out, int* dup_flag) {
@@ -417,8 +633,10 @@ size_t shk_bucketize_scratch(int64_t N, int64_t nb) {
   size_t s = 0;
   // shared-memory path: M and its scan (nb * BK_G + 1 each) + scan scratch
   const int64_t nm = nb * BK_G + 1;
+  const int64_t nms = ((nb + BK_SB - 1) / BK_SB) * BK_G + 1;
   size_t sm_path = ((size_t)nm * 8 + 255) & ~(size_t)255;
   sm_path *= 2;
+  sm_path += 2 * (((size_t)nms * 8 + 255) & ~(size_t)255) + shk_scan_scratch(nms) + 256;
   sm_path += ((size_t)N * 16 + 255) & ~(size_t)255;
   sm_path += 256 + shk_scan_scratch(nm);
   s += ((size_t)N * 4 + 255) & ~(size_t)255;        // bucket ids
@@ -446,6 +664,13 @@ static int bucketize_smem(const uint64_t* hi, const uint64_t* lo, int64_t N, int
   p += ((size_t)N * 16 + 255) & ~(size_t)255;
   int64_t* maxv = (int64_t*)p;
   p += 256;
+  const int64_t nsb = (nb + BK_SB - 1) / BK_SB, nms = nsb * BK_G + 1;
+  int64_t* Msb = (int64_t*)p;
+  p += ((size_t)nms * 8 + 255) & ~(size_t)255;
+  int64_t* Msboff = (int64_t*)p;
+  p += ((size_t)nms * 8 + 255) & ~(size_t)255;
+  void* scan_scratch2 = p;
+  p += shk_scan_scratch(nms) + 256;
   void* scan_scratch = p;
   const size_t hsm = (size_t)nb * 4;
   // (per call: the attribute is per device)
@@ -456,9 +681,12 @@ static int bucketize_smem(const uint64_t* hi, const uint64_t* lo, int64_t N, int
   SHK_CUDA(cudaMemsetAsync(maxv, 0, 8, st));
   SHK_CUDA(cudaMemsetAsync(dup_flag, 0, sizeof(int), st));
   SHK_CUDA(cudaMemsetAsync(M + nb * BK_G, 0, 8, st));
-  bk_hist_kernel<<<BK_G, 512, hsm, st>>>(hi, lo, N, (uint32_t)nb, M);
+  SHK_CUDA(cudaMemsetAsync(Msb + nsb * BK_G, 0, 8, st));
+  bk_hist_kernel<<<BK_G, 512, hsm, st>>>(hi, lo, N, (uint32_t)nb, M, Msb);
   SHK_LAUNCHED();
   int rc = shk_exclusive_scan_i64(M, Moff, nb * BK_G, scan_scratch, shk_scan_scratch(nm), st);
+  if (rc) return rc;
+  rc = shk_exclusive_scan_i64(Msb, Msboff, nsb * BK_G, scan_scratch2, shk_scan_scratch(nms), st);
   if (rc) return rc;
   bk_prefix_kernel<<<(unsigned)((nb + 256) / 256 < 148 ? (nb + 256) / 256 : 148), 256, 0, st>>>(Moff, BK_G, nb,
                                                                                                  prefix, maxv);
@@ -472,6 +700,38 @@ static int bucketize_smem(const uint64_t* hi, const uint64_t* lo, int64_t N, int
   // the scatter and the sort (only the histogram and the scan are waited for)
   SHK_CUDA(cudaStreamSynchronize(st));
   if (max_bucket_out) *max_bucket_out = maxb;
+  static const bool use_cluster = [] {
+    const char* e = getenv("SHK_BUCKET_CLUSTER");
+    return !(e && e[0] == '0');
+  }();
+  const int64_t cap = maxb;
+  const size_t csm = (size_t)cap * 16 + (size_t)((cap + 7) & ~7) * 2 + BK_CBINS * 4;
+  if (use_cluster && csm <= 200 * 1024) {
+    // super-bucket scatter (coalesced runs), then one 16-CTA cluster per super-bucket
+    const size_t l1sm = (size_t)BK_TILE * 18 + (size_t)(3 * nsb + 1) * 4;
+    SHK_CUDA(cudaFuncSetAttribute(bk_l1_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l1sm));
+    bk_l1_scatter_kernel<<<BK_G, 512, l1sm, st>>>(hi, lo, N, (uint32_t)nb, Msboff, unsorted);
+    SHK_LAUNCHED();
+    SHK_CUDA(cudaFuncSetAttribute(bk_cluster_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    SHK_CUDA(cudaFuncSetAttribute(bk_cluster_sort_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nsb * BK_CL), 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = csm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = BK_CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SHK_CUDA(cudaLaunchKernelEx(&cfg, bk_cluster_sort_kernel, (const ulonglong2*)unsorted, (const int64_t*)prefix, nb,
+                                (int)cap, out, dup_flag));
+    SHK_LAUNCHED();
+    *handled = 1;
+    return 0;
+  }
   // (A/B: SHK_BUCKET_SLICE_MB=S scatters S-MB destination slices, one pass
   // each; at C4 48 MB slices measured 0.61 ms vs 0.58 ms for one pass)
   static const int64_t slice_bytes = [] {

@@ -49,6 +49,7 @@ struct shk_ctx {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // side stream for pipelined host->device copies
+  cudaStream_t copy_out = nullptr;  // side stream for pipelined device->host copies
   int num_sms = 148;
   std::multimap<size_t, void*> free_blocks;
   std::unordered_map<void*, size_t> live;
@@ -203,6 +204,7 @@ int shk_ctx_create(int device, shk_ctx** out) {
   c->num_sms = prop.multiProcessorCount;
   SHK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   SHK_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  SHK_CUDA(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
   c->stream = c->own;
   SHK_CUDA(cudaMalloc(&c->d_counter, 256));
   SHK_CUDA(cudaMallocHost(&c->h_flags, 64 * sizeof(int)));
@@ -226,6 +228,7 @@ int shk_ctx_destroy(shk_ctx* c) {
   cudaEventDestroy(c->t1);
   cudaStreamDestroy(c->own);
   cudaStreamDestroy(c->copy);
+  cudaStreamDestroy(c->copy_out);
   delete c;
   return 0;
 }
@@ -1844,6 +1847,86 @@ int shk_query(shk_qdesc* q, const uint64_t* hi, const uint64_t* lo, int64_t Q, u
   SHK_CUDA(cudaMemsetAsync(err, 0, 4, c->stream));
   RC(shk_launch_query(q->d, (const uint64_t*)dh, (const uint64_t*)dl, Q, (uint64_t*)dout, err, clamp, c->stream));
   RC(finish_out(c, flags, out, to, (size_t)Q * 8));
+  int herr = 0;
+  RC(d2h(c, &herr, err, 4));
+  RC(csync(c));
+  if (herr) {
+    shk_set_error("bit stream overrun");
+    return SHK_FORMAT;
+  }
+  return 0;
+}
+
+// query_many(keys) end to end from a host buffer of fixed-length keys:
+// chunks of the key blob go H2D on the copy stream, are fingerprinted and
+// queried on the context stream, and the outputs come back D2H on a second
+// copy stream, so the PCIe transfers of chunk k+1 (in) and k-1 (out)
+// overlap the kernels of chunk k.  Host-blocking.  (recsplit.py:270-275:
+// master_hash_many + query_hashed_many.)
+int shk_query_blob(shk_qdesc* q, const uint8_t* blob, int key_len, int64_t Q, uint64_t salt, uint64_t* out, int clamp) {
+  shk_ctx* c = q->c;
+  if (Q <= 0) return 0;
+  if (key_len < 1 || key_len > 128) {
+    shk_set_error("fixed-length keys must be 1..128 bytes");
+    return SHK_INVALID;
+  }
+  const int64_t CH = (int64_t)1 << 22;  // keys per chunk
+  const int64_t per = Q < CH ? Q : CH;
+  DBuf kb[2] = {DBuf(c), DBuf(c)}, ob[2] = {DBuf(c), DBuf(c)}, hh(c), ll(c);
+  for (int k = 0; k < 2; ++k) {
+    RC(kb[k].alloc((size_t)per * key_len));
+    RC(ob[k].alloc((size_t)per * 8));
+  }
+  RC(hh.alloc((size_t)per * 8));
+  RC(ll.alloc((size_t)per * 8));
+  int* err = c->d_counter + 5;
+  SHK_CUDA(cudaMemsetAsync(err, 0, 4, c->stream));
+  const int64_t nch = (Q + per - 1) / per;
+  cudaEvent_t in_done[2], comp_done[2], out_done[2];
+  for (int k = 0; k < 2; ++k) {
+    SHK_CUDA(cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming));
+    SHK_CUDA(cudaEventCreateWithFlags(&comp_done[k], cudaEventDisableTiming));
+    SHK_CUDA(cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming));
+  }
+  int rc = 0;
+  for (int64_t k = 0; k < nch && !rc; ++k) {
+    const int s = (int)(k & 1);
+    const int64_t a = k * per, n = (a + per < Q) ? per : Q - a;
+    cudaError_t e = cudaSuccess;
+    if (k >= 2) e = cudaStreamWaitEvent(c->copy, comp_done[s], 0);  // the key buffer was consumed
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(kb[s].p, blob + (size_t)a * key_len, (size_t)n * key_len, cudaMemcpyHostToDevice, c->copy);
+    if (e == cudaSuccess) e = cudaEventRecord(in_done[s], c->copy);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, in_done[s], 0);
+    if (e == cudaSuccess && k >= 2) e = cudaStreamWaitEvent(c->stream, out_done[s], 0);  // outputs copied out
+    if (e != cudaSuccess) {
+      shk_set_error("query pipeline: %s", cudaGetErrorString(e));
+      rc = -1000 - (int)e;
+      break;
+    }
+    rc = shk_launch_blake2b_fixed(kb[s].as<uint8_t>(), key_len, n, salt, hh.as<uint64_t>(), ll.as<uint64_t>(),
+                                  c->stream);
+    if (!rc) rc = shk_launch_query(q->d, hh.as<uint64_t>(), ll.as<uint64_t>(), n, ob[s].as<uint64_t>(), err, clamp,
+                                   c->stream);
+    if (rc) break;
+    e = cudaEventRecord(comp_done[s], c->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy_out, comp_done[s], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out + a, ob[s].p, (size_t)n * 8, cudaMemcpyDeviceToHost, c->copy_out);
+    if (e == cudaSuccess) e = cudaEventRecord(out_done[s], c->copy_out);
+    if (e != cudaSuccess) {
+      shk_set_error("query pipeline: %s", cudaGetErrorString(e));
+      rc = -1000 - (int)e;
+    }
+  }
+  cudaStreamSynchronize(c->copy);
+  cudaStreamSynchronize(c->stream);
+  cudaStreamSynchronize(c->copy_out);
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(in_done[k]);
+    cudaEventDestroy(comp_done[k]);
+    cudaEventDestroy(out_done[k]);
+  }
+  if (rc) return rc;
   int herr = 0;
   RC(d2h(c, &herr, err, 4));
   RC(csync(c));

@@ -155,11 +155,14 @@ SHK_D void plain_fill_edges(const uint4* keys, int n, uint64_t s, unsigned lanes
 // to the ALU pipe (tools/ab_leaf.sh: C3 26.0 -> 25.5 ms; C5 13.03-13.08 ->
 // 12.82-12.92 s).  The rotate search in the build keeps the FMA placement:
 // the tree kernel is ALU-heavier (split hashes), ncu ALU 72% / fmaheavy 65%.
+// Re-swept for the stealing kernel (ncu C3: ALU 76%, fmaheavy 64%): C3 best
+// with shift 4 on the FMA pipe (0x0F: 23.62 vs 23.93 ms), C5 with shifts 1
+// and 3 there (0x15: 11.20 vs 11.41 s); all-FMA (0x00) is the slowest.
 #ifndef SHK_PLAIN_SHIFT_MASK
-#define SHK_PLAIN_SHIFT_MASK 0x1F
+#define SHK_PLAIN_SHIFT_MASK 0x0F
 #endif
 #ifndef SHK_PLAIN_SHIFT_MASK_WIDE
-#define SHK_PLAIN_SHIFT_MASK_WIDE 0x1F
+#define SHK_PLAIN_SHIFT_MASK_WIDE 0x15
 #endif
 template <bool WIDE, bool STORE = true>
 SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {

@@ -242,6 +242,13 @@ def test_c2_build_golden():
     assert sha(np.asarray(out, "<u8").tobytes()) == g["query_sha"]
     own = desc.query_hashed_many(hi, lo)
     assert (np.bincount(own.astype(np.int64), minlength=len(keys)) == 1).all()
+    # query_many(keys) end to end (the pipelined host-blob path, chunks of 4M
+    # keys: 1e6 queries are one chunk, so also a 9M-query batch of the same keys)
+    qkeys = [keys[i] for i in idx]
+    assert sha(np.asarray(desc.query_many(qkeys), "<u8").tobytes()) == g["query_sha"]
+    blob9 = np.frombuffer(b"".join(qkeys) * 9, dtype=np.uint8)
+    out9 = desc.query_blob(blob9, 8)
+    assert (out9.reshape(9, -1) == np.asarray(out, dtype=np.uint64)[None, :]).all()
 
 
 @pytest.mark.parametrize("env", [
