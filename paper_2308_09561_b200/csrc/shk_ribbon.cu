@@ -28,6 +28,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "shk_common.cuh"
 #include "shk_kernels.h"
@@ -44,7 +46,8 @@ constexpr int CE = SHK_RIBBON_CE;
 #ifndef SHK_RIBBON_CB
 #define SHK_RIBBON_CB 8192
 #endif
-constexpr int CB = SHK_RIBBON_CB;  // back-substitution chunk (columns), multiple of CE and 64
+constexpr int CB = SHK_RIBBON_CB;
+#define RIB_SPAN_DEFAULT "1,2"  // back-substitution chunk (columns), multiple of CE and 64
 
 struct RRow {
   uint64_t p0, p1;
@@ -142,30 +145,34 @@ __global__ void ribbon_rows_scatter_kernel(const int64_t* starts, const uint64_t
 // iteration (then it sees the winner's row).  A set occupancy bit therefore
 // always refers to data written before the previous __syncwarp.  Any
 // insertion order yields the same final solution.
+// S: elimination chunks merged per warp (1 for the first pass; later passes
+// take S consecutive chunks so a row can walk S chunks in one pass).
+template <int S>
 __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const int64_t* row_off, int64_t nchunks,
                                                          int64_t m, uint64_t* sp0, uint64_t* sp1, uint32_t* occ,
                                                          uint32_t* sbit, RRow* ovf, int64_t* ovf_count,
                                                          int* inconsistent, int first_pass) {
-  __shared__ uint64_t q0s[CE], q1s[CE];
-  __shared__ uint32_t occs[CE / 32], sbs[CE / 32];
+  constexpr int CEs = CE * S;
+  __shared__ uint64_t q0s[CEs], q1s[CEs];
+  __shared__ uint32_t occs[CEs / 32], sbs[CEs / 32];
   const int64_t c = blockIdx.x;
-  if (c >= nchunks) return;
-  const int64_t r0 = row_off[c], r1 = row_off[c + 1];
+  if (c * S >= nchunks) return;
+  const int64_t r0 = row_off[c * S], r1 = row_off[(c + 1) * S < nchunks ? (c + 1) * S : nchunks];
   if (r0 == r1) return;
   const int lane = threadIdx.x;
-  const int64_t base = c * CE;
-  const int64_t cols = (m - base < CE) ? (m - base) : CE;
+  const int64_t base = c * CEs;
+  const int64_t cols = (m - base < CEs) ? (m - base) : CEs;
   const int64_t nrows = r1 - r0;
   const int64_t wbase = base / 32;
   if (first_pass) {  // slots start empty: no global state to load
-    for (int j = lane; j < CE / 32; j += 32) occs[j] = sbs[j] = 0;
+    for (int j = lane; j < CEs / 32; j += 32) occs[j] = sbs[j] = 0;
   } else {
-    for (int j = lane; j < CE; j += 32) {
+    for (int j = lane; j < CEs; j += 32) {
       const bool in = j < cols;
       q0s[j] = in ? sp0[base + j] : 0;
       q1s[j] = in ? sp1[base + j] : 0;
     }
-    for (int j = lane; j < CE / 32; j += 32) {
+    for (int j = lane; j < CEs / 32; j += 32) {
       const bool in = (j * 32) < cols;
       occs[j] = in ? occ[wbase + j] : 0;
       sbs[j] = in ? sbit[wbase + j] : 0;
@@ -203,7 +210,7 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
   fetch();
   while (__any_sync(FULL_WARP, active)) {
     // phase A: read the slot at the current pivot
-    const bool esc = active && j >= CE;
+    const bool esc = active && j >= CEs;
     uint32_t w = 0, sw = 0;
     uint64_t q0 = 0, q1 = 0;
     if (active && !esc) {
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
     sp0[base + jj] = q0s[jj];
     sp1[base + jj] = q1s[jj];
   }
-  for (int jj = lane; jj < CE / 32; jj += 32) {
+  for (int jj = lane; jj < CEs / 32; jj += 32) {
     if ((jj * 32) < cols) {
       occ[wbase + jj] = occs[jj];
       sbit[wbase + jj] = sbs[jj];
@@ -938,6 +945,29 @@ int rib_regroup(const RibBufs& b, const RRow* src, const int64_t* np, int64_t M,
   return 0;
 }
 
+// Chunks per warp of elimination pass `pass` (SHK_RIBBON_SPAN="1,1,4": a
+// list per pass, the last entry repeats).  The first passes hold rows in
+// every chunk and need one warp per chunk for parallelism; the late passes
+// hold a few rows that walk several chunks, so merging chunks saves passes.
+int rib_span(int pass) {
+  static const std::vector<int> spans = [] {
+    std::vector<int> v;
+    const char* e = getenv("SHK_RIBBON_SPAN");
+    std::string str = e ? e : RIB_SPAN_DEFAULT;
+    size_t i = 0;
+    while (i < str.size()) {
+      const int x = atoi(str.c_str() + i);
+      v.push_back((x == 2 || x == 4) ? x : 1);
+      const size_t j = str.find(',', i);
+      if (j == std::string::npos) break;
+      i = j + 1;
+    }
+    if (v.empty()) v.push_back(1);
+    return v;
+  }();
+  return spans[(size_t)pass < spans.size() ? (size_t)pass : spans.size() - 1];
+}
+
 // Elimination passes over the chunk-grouped rows at `cur` (offsets in
 // rowoff) into the slot table of M local columns, until no row is left
 // inside the range.  first: the slot table is known empty.  Rows leaving the
@@ -1001,7 +1031,7 @@ int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c
   const int64_t nch = (M + CE - 1) / CE;
   int* bad = (int*)(b.cnt + 1);
   *bad_out = 0;
-  constexpr int BATCH = 6;
+  constexpr int BATCH = 4;
   for (int pass = 0;;) {
     for (int k = 0; k < BATCH; ++k, ++pass) {
       SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 8, st));
@@ -1012,8 +1042,20 @@ int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
       }
-      ribbon_elim_kernel<<<(unsigned)nch, 32, 0, st>>>(pass == 0 ? cur : b.rows2, b.rowoff, nch, M, b.sp0, b.sp1,
-                                                        b.occ, b.sb, b.ovf, b.cnt, bad, (first && pass == 0) ? 1 : 0);
+      // first pass: one warp per 512-column chunk (all chunks hold rows);
+      // later passes: 4 chunks per warp (few chunks hold rows, and a row may
+      // walk 4 chunks before it overflows: ~3 passes after the first instead
+      // of ~11)
+      const int S = rib_span(pass);
+      RRow* src = pass == 0 ? cur : b.rows2;
+      const int fp = (first && pass == 0) ? 1 : 0;
+      const unsigned g = (unsigned)((nch + S - 1) / S);
+      if (S == 1)
+        ribbon_elim_kernel<1><<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+      else if (S == 2)
+        ribbon_elim_kernel<2><<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+      else
+        ribbon_elim_kernel<4><<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
       SHK_LAUNCHED();
       if (trace) {
         cudaEventRecord(e1, st);

@@ -108,3 +108,56 @@ def test_large_build_is_a_bijection():
     blob = desc.serialize()
     assert recsplit.MphfDescriptor.deserialize(blob).serialize() == blob
     assert len(blob) * 8 / N < 1.7  # ~1.61 bits/key at n=40, b=2000
+
+
+def _steal_search(hi, lo, off, max_seed=1 << 40):
+    """The stealing kernel's path: device pointers, no counters requested."""
+    from paper_2308_09561_b200 import device as dev
+    from paper_2308_09561_b200._kernels import kernels as K
+
+    L = len(off) - 1
+    bufs = [dev.DeviceBuffer.from_host(np.ascontiguousarray(x, dtype=np.uint64)) for x in (hi, lo)]
+    d_off = dev.DeviceBuffer.from_host(np.asarray(off, dtype=np.int64))
+    d_s, d_f = dev.DeviceBuffer(8 * L), dev.DeviceBuffer(8 * L)
+    try:
+        K.leaf_search_device(bufs[0].ptr, bufs[1].ptr, d_off.ptr, L, 0, d_s.ptr, d_f.ptr, max_seed=max_seed)
+        dev.sync()
+        return d_s.download(np.int64, L), d_f.download(np.uint64, L)
+    finally:
+        for b_ in bufs + [d_off, d_s, d_f]:
+            b_.free()
+
+
+def test_steal_kernel_ragged_batch_matches_counting_kernel():
+    """Ragged CSR leaves of 1..64 keys in one batch (n = 1 leaves, 32-bit and
+    64-bit masks mixed): the stealing kernel's seeds and f bits equal the
+    fixed-team kernel's (which also returns the reference's counters)."""
+    from paper_2308_09561_b200._kernels import kernels as K
+
+    rng = np.random.default_rng(77)
+    sizes = np.concatenate([[1, 25, 64, 33, 2], rng.integers(1, 49, 600)])
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    hi, lo = synthetic_hashed(int(off[-1]), 4242)
+    s_ref, f_ref, _ = K.leaf_search_batch(hi, lo, off, 0)
+    s, f = _steal_search(hi, lo, off)
+    assert (s == s_ref).all() and (f == f_ref).all()
+
+
+def test_steal_kernel_exhaustion_and_single_leaf():
+    """max_seed cuts: a leaf whose minimum seed is >= max_seed reports -1
+    (the reference's exhaustion value, _core.pyx:223-229) and the others are
+    unaffected; a lone leaf (all warps join it) gives the oracle's seed."""
+    import oracle
+
+    n = 40
+    hi, lo = synthetic_hashed(8 * n, 99)
+    off = np.arange(0, 9 * n, n)
+    ref = [oracle.search_plain(hi[i * n : (i + 1) * n], lo[i * n : (i + 1) * n], n, 1 << 40)[0] for i in range(8)]
+    cut = sorted(ref)[4]  # half of the leaves need more seeds than this
+    s, f = _steal_search(hi, lo, off, max_seed=cut)
+    assert s.tolist() == [x if x < cut else -1 for x in ref]
+    assert all(int(f[i]) == 0 for i in range(8) if ref[i] >= cut)
+    s1, f1 = _steal_search(hi[:n], lo[:n], np.array([0, n]))
+    assert int(s1[0]) == ref[0]
+    e = oracle.edges_plain(hi[:n], lo[:n], ref[0], n)
+    assert int(f1[0]) == oracle.orient(e, n)
