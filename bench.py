@@ -325,11 +325,18 @@ def run_ours(args):
     sms = dev.num_sms()
     int_peak = measure_int_peak(dev, sms)
     int_peak["sms"] = sms
-    # resident inputs: the master codes, computed once on the GPU
-    d_blob = dev.DeviceBuffer.from_host(blob)
-    d_hi = dev.DeviceBuffer(8 * N)
-    d_lo = dev.DeviceBuffer(8 * N)
-    dev.blake2b_fixed_device(d_blob, 8, N, 0, d_hi, d_lo)
+    # N > 1: each rank holds only its slice of the keys (input-sharded build,
+    # two all-to-alls); SHK_SHARD_INPUT=0: every rank holds all keys
+    # (replicated fingerprinting and bucket sort)
+    input_sharded = sharded and os.environ.get("SHK_SHARD_INPUT", "1") != "0"
+    k0, k1 = ((N * rank) // world, (N * (rank + 1)) // world) if input_sharded else (0, N)
+    n_loc = k1 - k0
+    my_blob = blob[8 * k0 : 8 * k1]
+    # resident inputs: the master codes (of this rank's keys), computed once on the GPU
+    d_blob = dev.DeviceBuffer.from_host(my_blob)
+    d_hi = dev.DeviceBuffer(8 * n_loc)
+    d_lo = dev.DeviceBuffer(8 * n_loc)
+    dev.blake2b_fixed_device(d_blob, 8, n_loc, 0, d_hi, d_lo)
     d_blob.free()
     dev.sync()
 
@@ -337,7 +344,12 @@ def run_ours(args):
         if not sharded:
             d = recsplit.build_hashed_device(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"])
             return d, d.device_profile
-        d, prof = shdist.build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"], device=coll_device())
+        if input_sharded:
+            d, prof = shdist.build_hashed_device_sharded_input(d_hi.ptr, d_lo.ptr, n_loc, N, b, n, CFG["mode"],
+                                                               device=coll_device())
+        else:
+            d, prof = shdist.build_hashed_device_sharded(d_hi.ptr, d_lo.ptr, N, b, n, CFG["mode"],
+                                                         device=coll_device())
         prof = dict(prof)
         prof["phase_ms"] = dict(zip(("bucketize", "split_search", "leaf_search", "rice", "ribbon"), prof["phase_ms"]))
         return d, prof
@@ -386,10 +398,12 @@ def run_ours(args):
     # blob in, serialized descriptor bytes out; max wall over ranks
     desc_bytes = 0
     out = None
-    pinned = dev.PinnedBuffer.from_array(blob)  # the caller's key buffer, page-locked
+    pinned = dev.PinnedBuffer.from_array(my_blob)  # the caller's key buffer (this rank's slice), page-locked
 
     def e2e_step():
-        if sharded:
+        if input_sharded:
+            d2, _ = shdist.build_blob_sharded_input(pinned.array, 8, N, b, n, CFG["mode"], device=coll_device())
+        elif sharded:
             d2, _ = shdist.build_blob_sharded(pinned.array, 8, b, n, CFG["mode"], device=coll_device())
         else:
             d2 = recsplit.build_blob(pinned.array, 8, b, n, CFG["mode"])
@@ -409,9 +423,10 @@ def run_ours(args):
     finally:
         gc.enable()
     e2e_s = max_over_ranks(e2e_s, world)
-    e2e = {"value": round(N / e2e_s, 1), "unit": "keys/s", "h2d_bytes_per_step": int(blob.nbytes) * world,
+    e2e = {"value": round(N / e2e_s, 1), "unit": "keys/s", "h2d_bytes_per_step": int(my_blob.nbytes) * world,
            "d2h_bytes_per_step": int(desc_bytes), "ms_per_step": round(e2e_s * 1e3, 3),
-           "path": ("dist.build_blob_sharded" if sharded else "recsplit.build_blob")
+           "path": ("dist.build_blob_sharded_input" if input_sharded else
+                    "dist.build_blob_sharded" if sharded else "recsplit.build_blob")
            + "(pinned host 8-byte key blob) -> serialize(); H2D+blake2b+build+D2H timed"
            + (", max wall over ranks" if world > 1 else "")}
     pinned.free()
@@ -465,7 +480,10 @@ def run_ours(args):
         "data": "synthetic: default_rng(4) uniform 64-bit keys as 8-byte LE strings (the reference's recipe, SURVEY.md §8(d))",
         "config": {"workload": "C4: ShockHash-RS build N=10,000,000, leaf n=40, bucket b=2000, mode rotate, eps=0.05",
                    "N": N, "n": n, "b": b,
-                   "parallelism": (f"bucket-range x{world} ({DIST_BACKEND})" if world > 1 else "single GPU"),
+                   "parallelism": ((f"bucket-range x{world} ({DIST_BACKEND}), "
+                                    + ("input-sharded: keys -> bucket owners, rows -> column owners (all-to-all)"
+                                       if input_sharded else "replicated input"))
+                                   if world > 1 else "single GPU"),
                    "l2": "inputs 160 MB of resident master codes + 160 MB working keys > 126 MB L2 (no flush needed)"},
         "clocks": clocks,
         "gpu_launches": int(launches),
@@ -480,10 +498,13 @@ def run_ours(args):
             line["roofline"]["peak_source"] += f" (all {world} GPUs)"
     line["int_peak"] = {k2: v for k2, v in int_peak.items() if k2 != "sms"}
     # bucketing (a3): 32 algorithmic bytes per key (read hi/lo, write sorted hi/lo)
-    line["bucketize"] = {"ms": round(bucket_ms, 3), "algorithmic_bytes": 32 * N,
-                         "GBps": round(32 * N / (bucket_ms * 1e-3) / 1e9, 1),
-                         "hbm_frac": round(32 * N / (bucket_ms * 1e-3) / 1e9 / hbm, 4), "hbm_peak_GBps": hbm,
-                         "peak_source": hbm_src, "note": "every rank bucket-sorts all N keys (no all-to-all)"}
+    nb_keys = N if (world == 1 or not input_sharded) else (N + world - 1) // world  # keys one rank sorts
+    line["bucketize"] = {"ms": round(bucket_ms, 3), "algorithmic_bytes": 32 * nb_keys,
+                         "GBps": round(32 * nb_keys / (bucket_ms * 1e-3) / 1e9, 1),
+                         "hbm_frac": round(32 * nb_keys / (bucket_ms * 1e-3) / 1e9 / hbm, 4), "hbm_peak_GBps": hbm,
+                         "peak_source": hbm_src,
+                         "note": ("each rank sorts the keys of its bucket range (max over ranks)" if input_sharded
+                                  else "every rank bucket-sorts all N keys" if world > 1 else "single GPU")}
     if query:
         line["query"] = query
     if leaf_lines:

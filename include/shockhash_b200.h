@@ -258,6 +258,21 @@ int shk_build_choice_sorted(shk_build* b, int64_t k0, int64_t k1, uint8_t* out /
  * its (c1 - c0 + 63) / 64 solution words (host). */
 int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int flags, int64_t m, uint64_t seed,
                             int64_t c0, int64_t c1, int64_t* n_export, int* bad);
+/* Input-sharded multi-GPU build (dist.py; no reference counterpart): the
+ * column-sharded ribbon fed with explicit keys (device, interleaved (hi, lo)
+ * pairs) and rhs bytes that were routed to this rank, and the device
+ * pointers of a finished build's keys in leaf order and their choice bytes. */
+int shk_build_dribbon_begin_keys(shk_build* b, const uint64_t* keys_dev, const uint8_t* rhs_dev, int64_t n, int64_t m,
+                                 uint64_t seed, int64_t c0, int64_t c1, int64_t* n_export, int* bad);
+int shk_build_leaf_arrays(shk_build* b, void** keys_dev, void** choice_dev);
+/* Partition n keys (device, interleaved pairs) by owner rank -- kind 0: the
+ * rank owning the key's bucket (nbm = number of buckets), kind 1: the rank
+ * owning its ribbon row's start column (nbm = m, seed = ribbon seed); rank r
+ * owns values [bounds[r], bounds[r+1]) (host array of W+1).  keys_out /
+ * aux_out (device) receive the keys (and the optional per-key byte aux)
+ * grouped by rank; counts_out (host, W) the group sizes.  Synchronous. */
+int shk_route(shk_ctx* ctx, const uint64_t* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+              const int64_t* bounds, int W, uint64_t* keys_out, uint8_t* aux_out, int64_t* counts_out);
 int shk_build_dribbon_exports(shk_build* b, void* rows_out, int64_t n);
 int shk_build_dribbon_import(shk_build* b, const void* rows_in, int64_t n, int64_t* n_export, int* bad);
 int shk_build_dribbon_backsub(shk_build* b, const uint32_t* y_in, uint32_t* y_out, uint64_t* words_out);

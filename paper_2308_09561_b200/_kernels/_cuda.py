@@ -476,6 +476,19 @@ def query_stream(hi, lo, nbuckets, key_prefix, bit_offsets, stream_words, stream
 # MPHF construction runtime (native orchestration in the C-ABI)
 
 
+def route(keys_ptr, aux_ptr, n, kind, nbm, seed, bounds, keys_out_ptr, aux_out_ptr):
+    """Partition n device keys (interleaved pairs) by owner rank (kind 0:
+    bucket, kind 1: ribbon start column; rank r owns [bounds[r],
+    bounds[r+1])) into keys_out (and the per-key bytes aux into aux_out);
+    returns the group sizes."""
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    W = len(b) - 1
+    counts = np.zeros(W, dtype=np.int64)
+    check(_L().shk_route(ctx(), keys_ptr, aux_ptr, int(n), int(kind), int(nbm), int(seed), ptr(b), W, keys_out_ptr,
+                         aux_out_ptr, ptr(counts)), "route")
+    return counts
+
+
 class GpuBuild:
     """Handle on a device-side build: bucketed keys, tree, stream, ribbon.
 
@@ -587,6 +600,23 @@ class GpuBuild:
         check(_L().shk_build_dribbon_begin(self.handle, cp, fl, int(m), int(seed), int(c0), int(c1),
                                            ctypes.byref(nexp), ctypes.byref(bad)), "ribbon (sharded)")
         return int(nexp.value), bool(bad.value)
+
+    def dribbon_begin_keys(self, keys_ptr, rhs_ptr, n, m, seed, c0, c1):
+        """Column-sharded ribbon from explicit device keys (interleaved pairs)
+        and rhs bytes routed to this rank (input-sharded build)."""
+        nexp = ctypes.c_int64(0)
+        bad = ctypes.c_int(0)
+        check(_L().shk_build_dribbon_begin_keys(self.handle, keys_ptr, rhs_ptr, int(n), int(m), int(seed), int(c0),
+                                                int(c1), ctypes.byref(nexp), ctypes.byref(bad)), "ribbon (sharded)")
+        return int(nexp.value), bool(bad.value)
+
+    def leaf_arrays(self):
+        """(keys, choice) device pointers: the keys in leaf order
+        (interleaved pairs) and their choice bytes, after run()."""
+        k = ctypes.c_void_p()
+        c = ctypes.c_void_p()
+        check(_L().shk_build_leaf_arrays(self.handle, ctypes.byref(k), ctypes.byref(c)), "leaf arrays")
+        return k.value, c.value
 
     def dribbon_exports(self, n):
         rows = np.zeros(3 * max(int(n), 0), dtype=np.uint64)

@@ -115,6 +115,9 @@ _SIGS = {
     "shk_build_dribbon_map": (_I, [_P, _P]),
     "shk_build_dribbon_finish": (_I, [_P, _P, _P]),
     "shk_build_dribbon_exports": (_I, [_P, _P, _I64]),
+    "shk_build_dribbon_begin_keys": (_I, [_P, _P, _P, _I64, _I64, _U64, _I64, _I64, _P, _P]),
+    "shk_build_leaf_arrays": (_I, [_P, _P, _P]),
+    "shk_route": (_I, [_P, _P, _P, _I64, _I, _U64, _U64, _P, _I, _P, _P, _P]),
     "shk_build_dribbon_import": (_I, [_P, _P, _I64, _P, _P]),
     "shk_build_dribbon_backsub": (_I, [_P, _P, _P, _P]),
     "shk_build_run": (_I, [_P, _P, _I, _I, _I, _I64, _I64, _U64, _P]),

@@ -379,6 +379,20 @@ int shk_leaf_search(shk_ctx* c, int mode, int cache_k, int cache_min_leaf, const
   return 0;
 }
 
+// ---- routing to owner ranks (input-sharded build) ------------------------------
+int shk_route(shk_ctx* c, const uint64_t* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+              const int64_t* bounds, int W, uint64_t* keys_out, uint8_t* aux_out, int64_t* counts_out) {
+  if ((kind != 0 && kind != 1) || n < 0) {
+    shk_set_error("route: kind 0 (bucket) or 1 (ribbon column)");
+    return SHK_INVALID;
+  }
+  DBuf cnt(c), cur(c);
+  RC(cnt.alloc(64 * 8));
+  RC(cur.alloc(64 * 8));
+  return shk_launch_route(keys, aux, n, kind, nbm, seed, bounds, W, cnt.as<unsigned long long>(),
+                          cur.as<unsigned long long>(), keys_out, aux_out, counts_out, c->stream);
+}
+
 // ---- cross-GPU leaf queue (CUDA IPC) ------------------------------------------
 int shk_ipc_counter_alloc(shk_ctx* c, void* handle_out, void** dev_ptr) {
   int* p = nullptr;
@@ -1520,6 +1534,29 @@ int shk_build_dribbon_begin(shk_build* b, const uint8_t* choice_sorted, int flag
   b->mark(6);  // ribbon phase: from here to the end of backsub (exchanges included)
   return shk_ribbon_dist_begin(c->rib, b->sorted.as<uint64_t>(), b->drhs.as<uint8_t>(), b->N, m, seed, c0, c1,
                                n_export, bad, c->stream);
+}
+
+// Column-sharded ribbon from explicit rows' keys (device, interleaved
+// (hi, lo) pairs) and their rhs bytes: the input-sharded build routes every
+// key with its choice bit to the owner of its row's start column first.
+int shk_build_dribbon_begin_keys(shk_build* b, const uint64_t* keys_dev, const uint8_t* rhs_dev, int64_t n, int64_t m,
+                                 uint64_t seed, int64_t c0, int64_t c1, int64_t* n_export, int* bad) {
+  shk_ctx* c = b->c;
+  b->dcols = c1 - c0;
+  b->mark(6);
+  return shk_ribbon_dist_begin(c->rib, keys_dev, rhs_dev, n, m, seed, c0, c1, n_export, bad, c->stream);
+}
+
+// Device pointers of the build's keys in leaf order (interleaved pairs) and
+// their choice bytes, valid until the build is destroyed (after run()).
+int shk_build_leaf_arrays(shk_build* b, void** keys_dev, void** choice_dev) {
+  if (!b->ran) {
+    shk_set_error("leaf arrays need a finished run()");
+    return SHK_INVALID;
+  }
+  *keys_dev = b->keys.p;
+  *choice_dev = b->choice.p;
+  return 0;
 }
 
 int shk_build_dribbon_exports(shk_build* b, void* rows_out, int64_t n) {

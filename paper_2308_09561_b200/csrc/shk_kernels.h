@@ -237,3 +237,6 @@ int shk_launch_brute(const uint64_t* khi, const uint64_t* klo, int n, uint64_t b
 int shk_launch_mc_filter(const uint64_t* khi, const uint64_t* klo, int n, uint64_t count,
                          unsigned long long* passes, int num_sms, cudaStream_t st);
 int shk_launch_enumerate(int n, unsigned long long* out, int num_sms, cudaStream_t st);
+int shk_launch_route(const uint64_t* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+                     const int64_t* bounds, int W, unsigned long long* counts_dev, unsigned long long* cursors_dev,
+                     uint64_t* out, uint8_t* aux_out, int64_t* counts_host, cudaStream_t st);

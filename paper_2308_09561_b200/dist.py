@@ -165,7 +165,7 @@ def apply_map(mp: np.ndarray, y: np.ndarray) -> np.ndarray:
     return out
 
 
-def ribbon_sharded(gb, choice_sorted, m, max_tries, device=None):
+def ribbon_sharded(gb, choice_sorted, m, max_tries, device=None, begin=None):
     """Column-sharded ribbon solve (SURVEY.md §8(e) option B) over the process
     group; every rank returns (seed, words of the whole system).
 
@@ -189,7 +189,10 @@ def ribbon_sharded(gb, choice_sorted, m, max_tries, device=None):
         return int(t.item())
 
     for seed in range(max_tries):
-        nexp, bad = gb.dribbon_begin(choice_sorted, m, seed, c0, c1) if own else (0, False)
+        if begin is not None:  # input-sharded build: routes the rows (a collective), then begins
+            nexp, bad = begin(seed, c0, c1, own)
+        else:
+            nexp, bad = gb.dribbon_begin(choice_sorted, m, seed, c0, c1) if own else (0, False)
         passthrough = np.zeros(0, dtype=np.uint64)
         while True:
             if reduce(bad, dist.ReduceOp.MAX):
@@ -443,3 +446,192 @@ class SharedLeafQueue:
         dist.barrier()  # nobody still uses the owner's counter
         self.close()
         return False
+
+
+# ---------------------------------------------------------------------------
+# Input-sharded build: each rank holds 1/W of the keys and never touches the
+# others.  Two all-to-alls replace the replicated fingerprinting and bucket
+# sort of all N keys on every rank:
+#   1. keys -> the rank owning their bucket (shk_route kind 0), which builds
+#      its bucket range from exactly its keys; an all-reduce of the per-bucket
+#      counts gives the global key_prefix; the Rice streams are all-gathered
+#      as in the replicated path;
+#   2. (key, choice bit) in leaf order -> the rank owning the row's start
+#      column (shk_route kind 1, per ribbon seed), which starts its column
+#      range of the sharded ribbon from exactly those rows
+#      (shk_build_dribbon_begin_keys); exports, maps and words as before.
+# Same descriptor bytes as the single-GPU build (order independence of the
+# bucket sort input and of the ribbon rows).
+
+class _CudaArray:
+    def __init__(self, p, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(p), False),
+                                         "version": 3, "strides": None}
+
+
+def _torch_view(p, n, typestr="<i8"):
+    """A torch CUDA tensor aliasing n elements at device pointer p."""
+    import torch
+
+    if n == 0:
+        return torch.empty(0, dtype=torch.int64 if typestr == "<i8" else torch.uint8, device="cuda")
+    return torch.as_tensor(_CudaArray(p, n, typestr), device="cuda")
+
+
+def _all_to_all(send, counts, device):
+    """All-to-all of a CUDA tensor grouped by destination (counts[r] rows for
+    rank r; rows of any trailing shape); returns the received CUDA tensor,
+    grouped by source.  NCCL: all_to_all_single; other backends (gloo on one
+    GPU): through the host with all-gathers."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    row = int(np.prod(send.shape[1:])) if send.dim() > 1 else 1
+    cnt = [int(c) for c in counts]
+    all_c = [np.asarray(x, dtype=np.int64) for x in allgather_arrays(np.asarray(cnt, dtype=np.int64), device)]
+    recv_cnt = [int(all_c[r][rank]) for r in range(world)]
+    if device is not None and getattr(device, "type", "cpu") == "cuda":
+        out = torch.empty((sum(recv_cnt),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
+        dist.all_to_all_single(out.view(-1), send.contiguous().view(-1), [c * row for c in recv_cnt],
+                               [c * row for c in cnt])
+        return out
+    host = send.contiguous().view(-1).cpu().numpy()
+    parts = allgather_arrays(host, device)
+    pieces = []
+    for r in range(world):
+        off = int(all_c[r][:rank].sum()) * row
+        pieces.append(parts[r][off : off + recv_cnt[r] * row])
+    flat = np.concatenate(pieces) if pieces else host[:0]
+    return torch.from_numpy(flat.copy()).to(send.device).view((-1,) + tuple(send.shape[1:]))
+
+
+def build_hashed_device_sharded_input(hi_ptr, lo_ptr, n_local, n_keys, b, n, mode=1, cache_k=8, epsilon=0.05,
+                                      device=None, salt=0):
+    """Bucket-range build where rank r holds only its slice of the master
+    codes (device arrays hi/lo of n_local keys; n_keys in all).  Returns the
+    whole descriptor on every rank and this rank's profile (see the block
+    comment above)."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from . import device as dev
+    from . import recsplit, retrieval
+    from . import shockhash as leaf_mod
+    from ._kernels import kernels as K
+
+    recsplit._validate(n, b, mode)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    t0 = time.perf_counter()
+    nb = (n_keys + b - 1) // b
+    dev.sync()
+    pairs = torch.stack([_torch_view(hi_ptr, n_local), _torch_view(lo_ptr, n_local)], dim=1).contiguous()
+    routed = torch.empty_like(pairs)
+    torch.cuda.current_stream().synchronize()
+    bounds = [shard_range(nb, r, world)[0] for r in range(world)] + [nb]
+    counts = K.route(pairs.data_ptr(), None, n_local, 0, nb, 0, bounds, routed.data_ptr(), None)
+    mine = _all_to_all(routed, counts, device)  # the keys of this rank's buckets
+    del pairs, routed
+    hi_m, lo_m = mine[:, 0].contiguous(), mine[:, 1].contiguous()
+    torch.cuda.current_stream().synchronize()
+    n_mine = int(mine.shape[0])
+    gb = K.GpuBuild(None, None, nb, hi_ptr=hi_m.data_ptr(), lo_ptr=lo_m.data_ptr(), n=max(n_mine, 1)) if n_mine else None
+    dup = bool(gb.duplicate) if gb is not None else False
+    if agree_flag(dup, device):
+        if gb is not None:
+            gb.close()
+        raise recsplit.HashCollisionError("equal 128-bit codes in the input")
+    b0, b1 = shard_range(nb, rank, world)
+    local = np.zeros(nb, dtype=np.int64)
+    if gb is not None:
+        local = np.diff(gb.key_prefix().astype(np.int64))
+    cnt_t = torch.from_numpy(local).to(device if device is not None else "cpu")
+    dist.all_reduce(cnt_t, op=dist.ReduceOp.SUM)
+    key_prefix = np.zeros(nb + 1, dtype=np.uint64)
+    key_prefix[1:] = np.cumsum(cnt_t.cpu().numpy()).astype(np.uint64)
+    leaf_g = recsplit.leaf_g_table(n)
+    ck = cache_k if mode == leaf_mod.MODE_ROTATE_CACHED else 0
+    if gb is not None:
+        sizes = np.unique(np.diff(key_prefix[b0 : b1 + 1].astype(np.int64)))
+        plans = recsplit.packed_plans_for_sizes(sizes, n, leaf_g)
+        st = gb.run(plans, 0 if mode == leaf_mod.MODE_PLAIN else 1, ck, leaf_mod.CACHE_MIN_LEAF, b0, b1,
+                    leaf_mod.MAX_SEED)
+        words, bit_len, bo = gb.stream()
+        rel = bo[: b1 - b0 + 1]
+    else:
+        st = np.zeros(8, dtype=np.int64)
+        words, bit_len, rel = np.zeros(0, dtype=np.uint64), 0, np.zeros(b1 - b0 + 1, dtype=np.uint64)
+    sw, bl, bit_offsets = exchange_streams(words, bit_len, rel, device)
+    m = retrieval._columns(n_keys, epsilon)
+    col_bounds = [column_range(m, r, world)[0] for r in range(world)] + [m]
+    if gb is not None:
+        kp, cp = gb.leaf_arrays()
+    held = {}
+
+    def begin(seed, c0, c1, own):
+        k_out = torch.empty((n_mine, 2), dtype=torch.int64, device="cuda")
+        c_out = torch.empty(n_mine, dtype=torch.uint8, device="cuda")
+        counts_r = (K.route(kp, cp, n_mine, 1, m, seed, col_bounds, k_out.data_ptr(), c_out.data_ptr())
+                    if n_mine else np.zeros(world, dtype=np.int64))
+        rk = _all_to_all(k_out, counts_r, device)
+        rc = _all_to_all(c_out, counts_r, device)
+        torch.cuda.current_stream().synchronize()
+        held["rows"] = (rk, rc)  # alive until the next seed's begin
+        if not own:
+            return 0, False
+        return gb.dribbon_begin_keys(rk.data_ptr(), rc.data_ptr(), int(rk.shape[0]), m, seed, c0, c1)
+
+    if gb is None and column_range(m, rank, world)[1] > column_range(m, rank, world)[0]:
+        raise RuntimeError("a rank without keys cannot own ribbon columns in this build")
+    rseed, rwords = ribbon_sharded(gb, None, m, retrieval.RETRY_CAP, device, begin=begin)
+    ribbon = retrieval.RibbonSystem(epsilon, rseed, m, rwords)
+    desc = recsplit.MphfDescriptor(n_keys, b, n, mode, cache_k, salt, leaf_g, key_prefix, bit_offsets, sw, bl, ribbon)
+    desc.build_stats = {"build_seconds": time.perf_counter() - t0}
+    phase, split_evals = gb.phase_ms() if gb is not None else ([0.0] * 5, 0)
+    if gb is not None:
+        gb.close()
+    return desc, {"phase_ms": phase, "split_evals": split_evals, "buckets": (b0, b1), "keys_owned": n_mine,
+                  "hash_evals": int(st[0]), "filter_passes": int(st[1]), "leaf_count": int(st[6])}
+
+
+def build_blob_sharded_input(blob, key_len, n_keys, b, n, mode=1, cache_k=8, epsilon=0.05, device=None,
+                             fingerprint=None):
+    """build_blob where rank r holds only ITS slice of the host key blob (keys
+    [N r/W, N (r+1)/W) of n_keys, key_len bytes each): the rank copies and
+    fingerprints just that slice, then build_hashed_device_sharded_input.
+    The salt loop agrees across ranks (all-reduce of the duplicate flag); a
+    repeated key raises DuplicateKeyError on every rank."""
+    import torch.distributed as dist
+
+    from . import device as dev
+    from . import recsplit
+
+    blob = np.ascontiguousarray(np.frombuffer(blob, dtype=np.uint8) if isinstance(blob, (bytes, bytearray)) else blob,
+                                dtype=np.uint8)
+    n_local = len(blob) // key_len
+    recsplit._validate(n, b, mode)
+    fp = fingerprint if fingerprint is not None else dev.blake2b_fixed_from_host
+    d_hi = dev.DeviceBuffer(8 * max(n_local, 1))
+    d_lo = dev.DeviceBuffer(8 * max(n_local, 1))
+    try:
+        for salt in range(recsplit.SALT_RETRY_CAP):
+            if n_local:
+                fp(blob, key_len, n_local, salt, d_hi, d_lo)
+            try:
+                return build_hashed_device_sharded_input(d_hi.ptr, d_lo.ptr, n_local, n_keys, b, n, mode, cache_k,
+                                                         epsilon, device, salt=salt)
+            except recsplit.HashCollisionError:
+                pass
+            # a repeated key may span two ranks' slices: look at all keys
+            slices = allgather_arrays(blob, device)
+            allb = np.concatenate(slices)
+            keys = [bytes(allb[i * key_len : (i + 1) * key_len]) for i in range(len(allb) // key_len)]
+            dups = recsplit._find_duplicates(keys)
+            if dups:
+                raise recsplit.DuplicateKeyError(f"{len(dups)} duplicate key(s), first at line {dups[0] + 1}", dups)
+        raise recsplit.HashCollisionError(f"master hash collisions persist after {recsplit.SALT_RETRY_CAP} salts")
+    finally:
+        d_hi.free()
+        d_lo.free()

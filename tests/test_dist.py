@@ -168,3 +168,47 @@ def test_gloo_world2_salt_agreement():
         p.join(timeout=240)
     out = dict(q.get(timeout=5) for _ in range(2))
     assert out == {0: (True, False), 1: (True, False)}
+
+
+def _worker_a2a(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_09561_b200.dist import _all_to_all
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank r sends (r + d) rows to rank d, each row (r, d, j) as int64
+        counts = [rank + d for d in range(world)]
+        rows = [[rank, d, j] for d in range(world) for j in range(rank + d)]
+        send = torch.tensor(rows, dtype=torch.int64).view(-1, 3)
+        got = _all_to_all(send, counts, None)
+        q.put((rank, got.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_all_to_all():
+    """The host all-to-all of the input-sharded build (dist._all_to_all):
+    rows arrive grouped by source rank, in order."""
+    import socket
+
+    import torch.multiprocessing as tmp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    W = 3
+    procs = [ctx.Process(target=_worker_a2a, args=(r, W, port, q)) for r in range(W)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    out = dict(q.get(timeout=5) for _ in range(W))
+    for d in range(W):
+        assert out[d] == [[r, d, j] for r in range(W) for j in range(r + d)]
