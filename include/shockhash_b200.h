@@ -76,6 +76,20 @@ enum {
                                     stealing; A/B only) */
 };
 int shk_ctx_set_option(shk_ctx* ctx, int opt, int64_t value);
+/* Fused route + all-to-all over peer memory (input-sharded build): count
+ * the keys per owner rank (as shk_route), then store every key (and its aux
+ * byte) straight into the owner's receive buffer -- peer_bufs[d] is this
+ * process's mapping of rank d's buffer (CUDA IPC: shk_ipc_buffer_alloc +
+ * shk_ipc_counter_open, which maps any IPC handle), laid out as cap keys of
+ * 16 B then cap aux bytes; this rank's keys for d land at slots
+ * [peer_base[d], peer_base[d] + count_d).  Synchronous; the caller orders
+ * the receivers' reads after every sender's return (a barrier). */
+int shk_route_count(shk_ctx* ctx, const uint64_t* keys, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+                    const int64_t* bounds, int W, int64_t* counts_out);
+int shk_route_p2p(shk_ctx* ctx, const uint64_t* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm,
+                  uint64_t seed, const int64_t* bounds, int W, void* const* peer_bufs, const int64_t* peer_base,
+                  int64_t cap);
+int shk_ipc_buffer_alloc(shk_ctx* ctx, size_t bytes, void* handle_out, void** dev_ptr);
 /* Cross-GPU leaf queue for the batched PLAIN leaf search (no reference
  * counterpart: the reference is single-threaded).  One rank allocates a
  * device counter and exports its CUDA IPC handle (64 bytes); every rank

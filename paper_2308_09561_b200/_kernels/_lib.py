@@ -118,6 +118,9 @@ _SIGS = {
     "shk_build_dribbon_begin_keys": (_I, [_P, _P, _P, _I64, _I64, _U64, _I64, _I64, _P, _P]),
     "shk_build_leaf_arrays": (_I, [_P, _P, _P]),
     "shk_route": (_I, [_P, _P, _P, _I64, _I, _U64, _U64, _P, _I, _P, _P, _P]),
+    "shk_route_count": (_I, [_P, _P, _I64, _I, _U64, _U64, _P, _I, _P]),
+    "shk_route_p2p": (_I, [_P, _P, _P, _I64, _I, _U64, _U64, _P, _I, _P, _P, _I64]),
+    "shk_ipc_buffer_alloc": (_I, [_P, ctypes.c_size_t, _P, _P]),
     "shk_build_dribbon_import": (_I, [_P, _P, _I64, _P, _P]),
     "shk_build_dribbon_backsub": (_I, [_P, _P, _P, _P]),
     "shk_build_run": (_I, [_P, _P, _I, _I, _I, _I64, _I64, _U64, _P]),

@@ -393,6 +393,33 @@ int shk_route(shk_ctx* c, const uint64_t* keys, const uint8_t* aux, int64_t n, i
                           cur.as<unsigned long long>(), keys_out, aux_out, counts_out, c->stream);
 }
 
+int shk_route_count(shk_ctx* c, const uint64_t* keys, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+                    const int64_t* bounds, int W, int64_t* counts_out) {
+  DBuf cnt(c);
+  RC(cnt.alloc(64 * 8));
+  return shk_launch_route_count(keys, n, kind, nbm, seed, bounds, W, cnt.as<unsigned long long>(), counts_out,
+                                c->stream);
+}
+int shk_route_p2p(shk_ctx* c, const uint64_t* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm,
+                  uint64_t seed, const int64_t* bounds, int W, void* const* peer_bufs, const int64_t* peer_base,
+                  int64_t cap) {
+  DBuf cur(c);
+  RC(cur.alloc(64 * 8));
+  return shk_launch_route_p2p(keys, aux, n, kind, nbm, seed, bounds, W, peer_bufs, peer_base, cap,
+                              cur.as<unsigned long long>(), c->stream);
+}
+// IPC-shareable device buffers (the peer receive buffers of shk_route_p2p)
+int shk_ipc_buffer_alloc(shk_ctx* c, size_t bytes, void* handle_out, void** dev_ptr) {
+  void* p = nullptr;
+  SHK_CUDA(cudaSetDevice(c->device));
+  SHK_CUDA(cudaMalloc(&p, bytes ? bytes : 1));
+  cudaIpcMemHandle_t h;
+  SHK_CUDA(cudaIpcGetMemHandle(&h, p));
+  memcpy(handle_out, &h, sizeof(h));
+  *dev_ptr = p;
+  return 0;
+}
+
 // ---- cross-GPU leaf queue (CUDA IPC) ------------------------------------------
 int shk_ipc_counter_alloc(shk_ctx* c, void* handle_out, void** dev_ptr) {
   int* p = nullptr;

@@ -240,3 +240,9 @@ int shk_launch_enumerate(int n, unsigned long long* out, int num_sms, cudaStream
 int shk_launch_route(const uint64_t* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm, uint64_t seed,
                      const int64_t* bounds, int W, unsigned long long* counts_dev, unsigned long long* cursors_dev,
                      uint64_t* out, uint8_t* aux_out, int64_t* counts_host, cudaStream_t st);
+int shk_launch_route_count(const uint64_t* keys, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+                           const int64_t* bounds, int W, unsigned long long* counts_dev, int64_t* counts_host,
+                           cudaStream_t st);
+int shk_launch_route_p2p(const uint64_t* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+                         const int64_t* bounds, int W, void* const* peer_bufs, const int64_t* peer_base, int64_t cap,
+                         unsigned long long* cursors_dev, cudaStream_t st);

@@ -69,6 +69,44 @@ __global__ void route_scatter_kernel(const ulonglong2* keys, const uint8_t* aux,
   }
 }
 
+// Fused route + all-to-all over peer memory: every key is stored straight
+// into the receive buffer of the rank that owns it (CUDA IPC mappings of the
+// peers' buffers: NVLink stores on a multi-GPU node), at that rank's slot
+// for this source (peer_base[d]) plus a warp-aggregated local cursor.  The
+// receive buffer holds cap keys (16 B) followed by cap aux bytes.
+struct PeerPtrs {
+  unsigned char* p[RT_MAXW];
+  int64_t base[RT_MAXW];
+};
+
+__global__ void route_p2p_kernel(const ulonglong2* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm,
+                                 uint64_t seed, RouteBounds B, int W, PeerPtrs P, int64_t cap,
+                                 unsigned long long* cursors) {
+  const u2 x = split64(seed_mixer(seed, kind == 0 ? TAG_BUCKET : TAG_RSTART));
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool in = i < n;
+    ulonglong2 k = make_ulonglong2(0, 0);
+    int d = -1;
+    if (in) {
+      k = keys[i];
+      d = route_dest(k, kind, nbm, x, B, W);
+    }
+    const unsigned peers = __match_any_sync(FULL_WARP, d);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long pos = 0;
+    if (in && lane == leader) pos = atomicAdd(&cursors[d], (unsigned long long)__popc(peers));
+    pos = __shfl_sync(FULL_WARP, pos, leader);
+    if (in) {
+      const int64_t slot = P.base[d] + (int64_t)(pos + __popc(peers & ((1u << lane) - 1u)));
+      reinterpret_cast<ulonglong2*>(P.p[d])[slot] = k;  // NVLink store into the owner's buffer
+      if (aux) P.p[d][cap * 16 + slot] = aux[i];
+    }
+  }
+  __threadfence_system();
+}
+
 }  // namespace shk
 
 using namespace shk;
@@ -104,6 +142,57 @@ int shk_launch_route(const uint64_t* keys, const uint8_t* aux, int64_t n, int ki
   if (n > 0) {
     route_scatter_kernel<<<(unsigned)g, 256, 0, st>>>((const ulonglong2*)keys, aux, n, kind, nbm, seed, B, W,
                                                       cursors_dev, (ulonglong2*)out, aux_out);
+    SHK_LAUNCHED();
+  }
+  SHK_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int shk_launch_route_count(const uint64_t* keys, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+                           const int64_t* bounds, int W, unsigned long long* counts_dev, int64_t* counts_host,
+                           cudaStream_t st) {
+  if (W < 1 || W > RT_MAXW) {
+    shk_set_error("route: 1..%d ranks", RT_MAXW);
+    return 3;
+  }
+  RouteBounds B;
+  for (int r = 0; r <= W; ++r) B.b[r] = bounds[r];
+  SHK_CUDA(cudaMemsetAsync(counts_dev, 0, (size_t)W * 8, st));
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  if (g < 1) g = 1;
+  if (n > 0) {
+    route_count_kernel<<<(unsigned)g, 256, 0, st>>>((const ulonglong2*)keys, n, kind, nbm, seed, B, W, counts_dev);
+    SHK_LAUNCHED();
+  }
+  unsigned long long hc[RT_MAXW] = {0};
+  SHK_CUDA(cudaMemcpyAsync(hc, counts_dev, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaStreamSynchronize(st));
+  for (int r = 0; r < W; ++r) counts_host[r] = (int64_t)hc[r];
+  return 0;
+}
+
+int shk_launch_route_p2p(const uint64_t* keys, const uint8_t* aux, int64_t n, int kind, uint64_t nbm, uint64_t seed,
+                         const int64_t* bounds, int W, void* const* peer_bufs, const int64_t* peer_base, int64_t cap,
+                         unsigned long long* cursors_dev, cudaStream_t st) {
+  if (W < 1 || W > RT_MAXW) {
+    shk_set_error("route: 1..%d ranks", RT_MAXW);
+    return 3;
+  }
+  RouteBounds B;
+  PeerPtrs P;
+  for (int r = 0; r <= W; ++r) B.b[r] = bounds[r];
+  for (int r = 0; r < W; ++r) {
+    P.p[r] = (unsigned char*)peer_bufs[r];
+    P.base[r] = peer_base[r];
+  }
+  SHK_CUDA(cudaMemsetAsync(cursors_dev, 0, (size_t)W * 8, st));
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  if (g < 1) g = 1;
+  if (n > 0) {
+    route_p2p_kernel<<<(unsigned)g, 256, 0, st>>>((const ulonglong2*)keys, aux, n, kind, nbm, seed, B, W, P, cap,
+                                                  cursors_dev);
     SHK_LAUNCHED();
   }
   SHK_CUDA(cudaStreamSynchronize(st));

@@ -463,6 +463,10 @@ class SharedLeafQueue:
 # Same descriptor bytes as the single-GPU build (order independence of the
 # bucket sort input and of the ribbon rows).
 
+# route through peer memory (PeerRouter, default) or NCCL all-to-all (SHK_P2P=0)
+P2P_ROUTE = os.environ.get("SHK_P2P", "1") != "0"
+
+
 class _CudaArray:
     def __init__(self, p, n, typestr):
         self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(p), False),
@@ -531,8 +535,11 @@ def build_hashed_device_sharded_input(hi_ptr, lo_ptr, n_local, n_keys, b, n, mod
     routed = torch.empty_like(pairs)
     torch.cuda.current_stream().synchronize()
     bounds = [shard_range(nb, r, world)[0] for r in range(world)] + [nb]
-    counts = K.route(pairs.data_ptr(), None, n_local, 0, nb, 0, bounds, routed.data_ptr(), None)
-    mine = _all_to_all(routed, counts, device)  # the keys of this rank's buckets
+    if P2P_ROUTE:  # one kernel stores every key into its owner's buffer (peer memory)
+        mine, _ = _peer_router(device).route(pairs.data_ptr(), None, n_local, 0, nb, 0, bounds)
+    else:
+        counts = K.route(pairs.data_ptr(), None, n_local, 0, nb, 0, bounds, routed.data_ptr(), None)
+        mine = _all_to_all(routed, counts, device)  # the keys of this rank's buckets
     del pairs, routed
     hi_m, lo_m = mine[:, 0].contiguous(), mine[:, 1].contiguous()
     torch.cuda.current_stream().synchronize()
@@ -571,12 +578,16 @@ def build_hashed_device_sharded_input(hi_ptr, lo_ptr, n_local, n_keys, b, n, mod
     held = {}
 
     def begin(seed, c0, c1, own):
-        k_out = torch.empty((n_mine, 2), dtype=torch.int64, device="cuda")
-        c_out = torch.empty(n_mine, dtype=torch.uint8, device="cuda")
-        counts_r = (K.route(kp, cp, n_mine, 1, m, seed, col_bounds, k_out.data_ptr(), c_out.data_ptr())
-                    if n_mine else np.zeros(world, dtype=np.int64))
-        rk = _all_to_all(k_out, counts_r, device)
-        rc = _all_to_all(c_out, counts_r, device)
+        if P2P_ROUTE:
+            rk, rc = _peer_router(device).route(kp if n_mine else None, cp if n_mine else None, n_mine, 1, m, seed,
+                                                col_bounds)
+        else:
+            k_out = torch.empty((n_mine, 2), dtype=torch.int64, device="cuda")
+            c_out = torch.empty(n_mine, dtype=torch.uint8, device="cuda")
+            counts_r = (K.route(kp, cp, n_mine, 1, m, seed, col_bounds, k_out.data_ptr(), c_out.data_ptr())
+                        if n_mine else np.zeros(world, dtype=np.int64))
+            rk = _all_to_all(k_out, counts_r, device)
+            rc = _all_to_all(c_out, counts_r, device)
         torch.cuda.current_stream().synchronize()
         held["rows"] = (rk, rc)  # alive until the next seed's begin
         if not own:
@@ -635,3 +646,108 @@ def build_blob_sharded_input(blob, key_len, n_keys, b, n, mode=1, cache_k=8, eps
     finally:
         d_hi.free()
         d_lo.free()
+
+
+class PeerRouter:
+    """Route + all-to-all fused into one kernel over peer memory
+    (shk_route_p2p): every rank maps every other rank's receive buffer once
+    (CUDA IPC; NVLink on a multi-GPU node) and the routing kernel stores each
+    key straight into its owner's buffer at the slot reserved for this
+    source -- the transfer overlaps the hashing key by key instead of
+    following it as a separate NCCL all-to-all.  Only the W x W counts and,
+    on growth, the 64-byte IPC handles travel through torch.distributed.
+
+    route() returns torch views of this rank's receive buffer (valid until the
+    next route())."""
+
+    def __init__(self, device=None):
+        import torch.distributed as dist
+
+        from . import device as dev
+        from ._kernels import _lib
+
+        self._L = _lib.load_library()
+        self._ctx = dev.ctx()
+        self.device = device
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.cap = 0
+        self.ptrs = None
+
+    def _close(self):
+        from . import device as dev
+
+        if self.ptrs is None:
+            return
+        for r, p in enumerate(self.ptrs):
+            dev.check(self._L.shk_ipc_counter_close(self._ctx, p, 1 if r == self.rank else 0), "ipc close")
+        self.ptrs = None
+        self.cap = 0
+
+    def _ensure(self, need):
+        """Every rank's buffer holds >= need keys (collective)."""
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import device as dev
+
+        t = torch.tensor([int(need)], dtype=torch.int64, device=self.device if self.device is not None else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        need = int(t.item())
+        if self.ptrs is not None and need <= self.cap:
+            return
+        dist.barrier()  # nobody writes into the old buffers any more
+        self._close()
+        cap = int(need * 1.25) + 4096
+        handle = ctypes.create_string_buffer(64)
+        mine = ctypes.c_void_p()
+        dev.check(self._L.shk_ipc_buffer_alloc(self._ctx, cap * 17, handle, ctypes.byref(mine)), "ipc alloc")
+        hs = allgather_arrays(np.frombuffer(handle.raw, dtype=np.uint8).copy(), self.device)
+        ptrs = []
+        for r in range(self.world):
+            if r == self.rank:
+                ptrs.append(mine.value)
+                continue
+            p = ctypes.c_void_p()
+            h = ctypes.create_string_buffer(bytes(hs[r]), 64)
+            dev.check(self._L.shk_ipc_counter_open(self._ctx, h, ctypes.byref(p)), "ipc open")
+            ptrs.append(p.value)
+        self.ptrs, self.cap = ptrs, cap
+
+    def route(self, keys_ptr, aux_ptr, n, kind, nbm, seed, bounds):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import device as dev
+
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        W, rank = self.world, self.rank
+        counts = np.zeros(W, dtype=np.int64)
+        dev.check(self._L.shk_route_count(self._ctx, keys_ptr, int(n), int(kind), int(nbm), int(seed),
+                                          b.ctypes.data, W, counts.ctypes.data), "route count")
+        C = np.stack([np.asarray(x, dtype=np.int64) for x in allgather_arrays(counts, self.device)])  # [src][dst]
+        recv = int(C[:, rank].sum())
+        base = np.ascontiguousarray([int(C[:rank, d].sum()) for d in range(W)], dtype=np.int64)
+        self._ensure(int(C.sum(axis=0).max()))
+        dist.barrier()  # every receiver is done with the previous contents
+        arr = (ctypes.c_void_p * W)(*self.ptrs)
+        dev.check(self._L.shk_route_p2p(self._ctx, keys_ptr, aux_ptr, int(n), int(kind), int(nbm), int(seed),
+                                        b.ctypes.data, W, arr, base.ctypes.data, int(self.cap)), "route p2p")
+        dist.barrier()  # every sender's stores have landed
+        k = _torch_view(self.ptrs[rank], 2 * recv).view(-1, 2) if recv else _torch_view(0, 0).view(-1, 2)
+        a = _torch_view(self.ptrs[rank] + 16 * self.cap, recv, "|u1") if recv else _torch_view(0, 0, "|u1")
+        return k, a
+
+
+_PEER = None
+
+
+def _peer_router(device):
+    global _PEER
+    import torch.distributed as dist
+
+    if _PEER is None or _PEER.world != dist.get_world_size():
+        _PEER = PeerRouter(device)
+    return _PEER

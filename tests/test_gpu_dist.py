@@ -252,14 +252,17 @@ def test_shared_leaf_queue_two_ranks(cfg, L):
             assert out[r][batch][2] == gf[:L].tolist()
 
 
-def _worker_input_sharded(rank, world, port, q, N, b, n, mode):
+def _worker_input_sharded(rank, world, port, q, N, b, n, mode, p2p="1"):
     """Input-sharded build: rank r holds only keys [N r/W, N (r+1)/W); two
-    all-to-alls (keys -> bucket owners, rows -> column owners)."""
+    routings (keys -> bucket owners, rows -> column owners), through peer
+    memory (p2p "1": one kernel stores into the owners' IPC-mapped buffers)
+    or a NCCL/host all-to-all ("0")."""
     import os
 
     import torch.distributed as dist
 
     os.environ["SHK_DEVICE"] = "0"
+    os.environ["SHK_P2P"] = p2p
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         from paper_2308_09561_b200 import dist as shdist
@@ -274,9 +277,9 @@ def _worker_input_sharded(rank, world, port, q, N, b, n, mode):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_input_sharded_build_matches_reference(world):
-    out = _spawn(_worker_input_sharded, world, 100_000, 500, 24, 1)
+@pytest.mark.parametrize("world,p2p", [(2, "1"), (3, "1"), (3, "0")])
+def test_input_sharded_build_matches_reference(world, p2p):
+    out = _spawn(_worker_input_sharded, world, 100_000, 500, 24, 1, p2p)
     assert all(out[r][0] == golden("c2.json")["desc_sha"] for r in range(world))
     assert sum(out[r][1] for r in range(world)) == 100_000
 
