@@ -1376,6 +1376,10 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
       p.slow_wid = (e && e[0] == '0') ? (1 << 30) : (w ? atoi(w) : 0);
       const char* iw = getenv("SHK_TREE_IDLE_WID");
       p.idle_wid = iw ? atoi(iw) : 0;
+      // leaf tail: slow-slot warps take no new leaf once fewer than
+      // tail_reserve leaves remain (-1: one per fast warp)
+      const char* tr = getenv("SHK_TREE_TAIL_RESERVE");
+      p.tail_reserve = tr ? atoll(tr) : 0;
     }
     p.max_seed = max_seed;
     p.seeds = dseeds.as<int64_t>();

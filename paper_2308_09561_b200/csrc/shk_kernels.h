@@ -107,6 +107,7 @@ struct ShkTreeLaunch {
   int64_t nsplit;            // split nodes (size of the split region)
   int slow_wid;              // warps with %warpid >= slow_wid take leaves only; 0 = half the resident warps
   int idle_wid;              // warps with %warpid >= idle_wid take no work; 0 = none (A/B only)
+  int64_t tail_reserve;      // leaf-only warps stop once fewer leaves remain (0 off, -1 auto)
   uint64_t max_seed;
   int64_t* seeds;  // per node
   int mode, cache_k, cache_min_leaf, max_n;

@@ -267,6 +267,10 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
 
 // Cells of one key in the rotation search: OR its two cells into the A or B
 // coverage mask (bit = split bit, 1 = B) and store its packed edge.
+#ifndef SHK_ROT_UNROLL
+#define SHK_ROT_UNROLL 2  // keys per iteration of the rotate filter loop (independent hash chains)
+#endif
+constexpr int kRotUnroll = SHK_ROT_UNROLL;
 template <bool WIDE>
 SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_t& ma0, uint32_t& ma1,
                          uint32_t& mb0, uint32_t& mb1, uint32_t& na, uint16_t* e) {
@@ -324,7 +328,7 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
         const u2 xg = seed_mixer_pre_d(base, TAG_LEAF);
         uint32_t ma0 = 0, ma1 = 0, mb0 = 0, mb1 = 0;
         if (ck == 0) {  // A and B keys share the leaf seed (sa == base)
-#pragma unroll 2
+#pragma unroll kRotUnroll
           for (int i = 0; i < n; ++i) {
             const uint4 k = sm.keys[i];
             const u2 kh{k.x, k.y}, kl{k.z, k.w};

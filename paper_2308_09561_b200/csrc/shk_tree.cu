@@ -52,6 +52,7 @@ struct TreeArgs {
   int64_t nsplit;
   int slow_wid;                // warps with %warpid >= slow_wid take leaves only
   int idle_wid;                // warps with %warpid >= idle_wid take no work (A/B)
+  int64_t tail_reserve;        // leaf-only warps take no leaf once fewer than this remain
   uint64_t max_seed;
   int64_t* seeds;
   int* exhausted;
@@ -103,7 +104,8 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
   // every leaf slot -- is eventually published whatever slots the warps get.
   const bool anchor = blockIdx.x == 0 && w == 0;
   if ((int)wid >= t.idle_wid && !anchor) return;
-  bool splits_done = (int)wid >= t.slow_wid && !anchor;
+  const bool slow = (int)wid >= t.slow_wid && !anchor;
+  bool splits_done = slow;
   for (;;) {
     unsigned long long h = 0;
     if (!splits_done) {
@@ -112,6 +114,14 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       if (h >= (unsigned long long)t.nsplit) splits_done = true;
     }
     if (splits_done) {
+      if (slow && t.tail_reserve > 0) {
+        // the last leaves go to the fast slots: a leaf started late on a
+        // slow slot would end the launch (a top slot runs ~16x slower)
+        unsigned long long hh = 0;
+        if (lane == 0) hh = ld_relaxed_u64(t.head + 1);
+        hh = __shfl_sync(FULL_WARP, hh, 0);
+        if ((int64_t)hh + t.tail_reserve >= t.nnodes) break;
+      }
       if (lane == 0) h = atomicAdd(t.head + 1, 1ull);
       h = __shfl_sync(FULL_WARP, h, 0);
       if (h >= (unsigned long long)t.nnodes) break;
@@ -269,6 +279,8 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   const int sms = p.num_sms > 0 ? p.num_sms : 148;
   t.slow_wid = p.slow_wid > 0 ? p.slow_wid : (occ * 4) / 2;
   t.idle_wid = p.idle_wid > 0 ? p.idle_wid : 1 << 30;
+  // -1: one leaf per fast warp (the slots below slow_wid on every SM)
+  t.tail_reserve = p.tail_reserve >= 0 ? p.tail_reserve : (int64_t)sms * (t.slow_wid < occ * 4 ? t.slow_wid : occ * 4);
   kfn<<<(unsigned)(sms * occ), 128, 0, st>>>(t);
   SHK_LAUNCHED();
   return 0;
