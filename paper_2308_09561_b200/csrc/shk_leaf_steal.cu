@@ -39,7 +39,7 @@ struct StealLeaf {                 // per-leaf global state, zero-initialised
   unsigned long long next_blk;     // next 32-seed block to hand out
   unsigned long long nbest;        // ~(best seed found), 0 = none yet
   int workers;                     // warps on the leaf; joins only while > 0
-  int done;
+  int pad;
 };
 
 template <int MAXE>
@@ -224,10 +224,7 @@ __global__ void __launch_bounds__(128, 8) leaf_steal_kernel(LeafArgs a, StealLea
       if (last) __threadfence();
     }
     if (!__shfl_sync(FULL_WARP, last, 0)) continue;
-    if (lane == 0) {
-      nbest = ldr_u64(&L_.nbest);
-      L_.done = 1;
-    }
+    if (lane == 0) nbest = ldr_u64(&L_.nbest);
     nbest = __shfl_sync(FULL_WARP, nbest, 0);
     const int64_t seed = nbest != 0 ? (int64_t)~nbest : -1;
     if (seed >= 0) {

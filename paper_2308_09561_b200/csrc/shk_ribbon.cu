@@ -520,236 +520,6 @@ __global__ void ribbon_query_kernel(const int64_t* starts, const uint64_t* p0, c
 // Overflow rows of a pass, regrouped by the chunk they reached.  Rows past the
 // local column range [0, M) (a column-sharded solve: they belong to the next
 // rank) are appended to `exp` in global columns (+ c0) instead.
-// ---------------------------------------------------------------------------
-// Elimination in ONE launch ("carry" schedule).  The pass schedule above
-// needs one pass per chunk boundary a row crosses (C4: 12 passes, the last
-// seven moving a few hundred rows one chunk right at ~60-110 us each, plus a
-// regroup of hist + scan + scatter launches per pass).  Here the warp of
-// chunk c inserts its own rows, then CARRIES the rows that walked past the
-// chunk end into chunk c+1 itself, then c+2, ... until none is left.  Every
-// chunk's slot table is guarded by a lock word (0 free and never touched,
-// 1 held, 2 free and touched); a warp holds at most one lock at a time and
-// never waits while holding one, so there is no deadlock whatever the
-// residency of the other chunks' warps, and any insertion order gives the
-// reference's solution.  Carried rows live in a small
-// shared-memory list; if a list fills, the excess spills to a global list
-// (count cnt[0]) that the host re-inserts with another launch.
-constexpr int ESC_CAP = 64;
-
-struct ElimTable {
-  uint64_t q0[CE], q1[CE];
-  uint32_t occ[CE / 32], sb[CE / 32];
-};
-
-SHK_D int lock_chunk(int* lk) {
-  int old;
-  for (;;) {
-    old = atomicExch(lk, 1);
-    if (old != 1) break;
-    __nanosleep(64);
-  }
-  __threadfence();
-  return old;  // 0: the table was never touched (all zero)
-}
-
-SHK_D void unlock_chunk(int* lk) {
-  __threadfence();
-  atomicExch(lk, 2);
-}
-
-// Insert rows into the chunk table `T` (columns [base, base + cols)).
-// Source: the first `nsrc` rows of `src` (global, `from_global`) or of the
-// shared list `lst`.  Rows walking past the chunk go to `out` (capacity
-// ESC_CAP, count *nout), else to the spill list; rows past the last local
-// column M go to the export list (global columns, + c0).
-template <bool FROM_GLOBAL>
-SHK_D void elim_insert(ElimTable& T, const RRow* src, int64_t nsrc, int64_t base, int64_t cols, int64_t M,
-                       RRow* out, int* nout, RRow* spill, int64_t* spill_count, RRow* exp, int64_t* exp_count,
-                       int64_t c0, bool& bad, int lane) {
-  int64_t next = lane;
-  bool active = false;
-  uint64_t a0 = 0, a1 = 0;
-  uint32_t b = 0;
-  int j = 0;
-  RRow pre{0, 0, 0};
-  bool have_pre = false;
-  auto load_pre = [&]() {
-    have_pre = next < nsrc;
-    if (have_pre) {
-      pre = src[next];
-      next += 32;
-    }
-  };
-  auto fetch = [&]() {
-    active = have_pre;
-    if (active) {
-      a0 = pre.p0;
-      a1 = pre.p1;
-      b = (pre.s & RHS_BIT) ? 1u : 0u;
-      j = (int)((pre.s & S_MASK) - base);
-    }
-    load_pre();
-  };
-  load_pre();
-  fetch();
-  while (__any_sync(FULL_WARP, active)) {
-    const bool esc = active && j >= cols;
-    uint32_t w = 0, sw = 0;
-    uint64_t q0 = 0, q1 = 0;
-    if (active && !esc) {
-      w = T.occ[j >> 5];
-      sw = T.sb[j >> 5];
-      q0 = T.q0[j];
-      q1 = T.q1[j];
-    }
-    __syncwarp();
-    if (active) {
-      if (esc) {
-        RRow o;
-        o.p0 = a0;
-        o.p1 = a1;
-        o.s = (base + j) | (b ? RHS_BIT : 0);
-        if (base + j >= M) {  // past this solver's columns: export (global columns)
-          o.s = (base + j + c0) | (b ? RHS_BIT : 0);
-          exp[(int64_t)atomicAdd((unsigned long long*)exp_count, 1ull)] = o;
-        } else {
-          const int k = atomicAdd(nout, 1);
-          if (k < ESC_CAP)
-            out[k] = o;
-          else
-            spill[(int64_t)atomicAdd((unsigned long long*)spill_count, 1ull)] = o;
-        }
-        fetch();
-      } else {
-        const uint32_t bitm = 1u << (j & 31);
-        if (w & bitm) {
-          a0 ^= q0;
-          a1 ^= q1;
-          b ^= (sw >> (j & 31)) & 1u;
-          if ((a0 | a1) == 0) {
-            if (b) bad = true;
-            fetch();
-          } else {
-            int t;
-            if (a0) {
-              t = __ffsll((long long)a0) - 1;
-              a0 = (a0 >> t) | (t ? (a1 << (64 - t)) : 0);
-              a1 >>= t;
-            } else {
-              t = 63 + __ffsll((long long)a1);
-              a0 = a1 >> (t - 64);
-              a1 = 0;
-            }
-            j += t;
-          }
-        } else {
-          const uint32_t old = atomicOr(&T.occ[j >> 5], bitm);
-          if (!(old & bitm)) {
-            T.q0[j] = a0;
-            T.q1[j] = a1;
-            if (b) atomicOr(&T.sb[j >> 5], bitm);
-            fetch();
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-}
-
-SHK_D void table_load(ElimTable& T, bool fresh, const uint64_t* sp0, const uint64_t* sp1, const uint32_t* occ,
-                      const uint32_t* sbit, int64_t base, int64_t cols, int lane) {
-  const int64_t wbase = base / 32;
-  if (fresh) {
-    for (int j = lane; j < CE / 32; j += 32) T.occ[j] = T.sb[j] = 0;
-  } else {
-    for (int j = lane; j < CE; j += 32) {
-      const bool in = j < cols;
-      T.q0[j] = in ? __ldcg(sp0 + base + j) : 0;
-      T.q1[j] = in ? __ldcg(sp1 + base + j) : 0;
-    }
-    for (int j = lane; j < CE / 32; j += 32) {
-      const bool in = (j * 32) < cols;
-      T.occ[j] = in ? __ldcg(occ + wbase + j) : 0;
-      T.sb[j] = in ? __ldcg(sbit + wbase + j) : 0;
-    }
-  }
-  __syncwarp();
-}
-
-SHK_D void table_store(const ElimTable& T, uint64_t* sp0, uint64_t* sp1, uint32_t* occ, uint32_t* sbit, int64_t base,
-                       int64_t cols, int lane) {
-  __syncwarp();
-  const int64_t wbase = base / 32;
-  // slots never claimed keep stale smem contents: only occupied ones matter
-  // (readers test the occupancy bit first), but write all for simplicity
-  for (int jj = lane; jj < cols; jj += 32) {
-    sp0[base + jj] = T.q0[jj];
-    sp1[base + jj] = T.q1[jj];
-  }
-  for (int jj = lane; jj < CE / 32; jj += 32)
-    if ((jj * 32) < cols) {
-      occ[wbase + jj] = T.occ[jj];
-      sbit[wbase + jj] = T.sb[jj];
-    }
-  __threadfence();  // every lane's stores before the unlock (lane 0)
-}
-
-__global__ void __launch_bounds__(32) ribbon_elim_carry_kernel(const RRow* rows, const int64_t* row_off,
-                                                               int64_t nchunks, int64_t M, uint64_t* sp0,
-                                                               uint64_t* sp1, uint32_t* occ, uint32_t* sbit,
-                                                               int* locks, RRow* spill, int64_t* spill_count,
-                                                               RRow* exp, int64_t* exp_count, int64_t c0,
-                                                               int* inconsistent, int64_t stride) {
-  __shared__ ElimTable T;
-  __shared__ RRow lst[2][ESC_CAP];
-  __shared__ int nl[2];
-  // Blocks visit the chunks in a strided order (stride coprime to the chunk
-  // count, ~0.62 of it): the warps resident at the same time own chunks far
-  // apart, so the chunk right of a finished one is almost never being
-  // searched at that moment and its lock is free (in block order, every
-  // carry would wait for the neighbour's own insertion).
-  const int64_t c = (int64_t)(((unsigned long long)blockIdx.x * (unsigned long long)stride) % (unsigned long long)nchunks);
-  if (c >= nchunks) return;
-  const int64_t r0 = row_off[c], r1 = row_off[c + 1];
-  if (r0 == r1) return;
-  const int lane = threadIdx.x;
-  bool bad = false;
-  int cur = 0;
-  if (lane == 0) nl[0] = nl[1] = 0;
-  int64_t d = c;
-  {
-    const int64_t base = d * CE, cols = (M - base < CE) ? (M - base) : CE;
-    int old = 0;
-    if (lane == 0) old = lock_chunk(locks + d);
-    old = __shfl_sync(FULL_WARP, old, 0);
-    table_load(T, old == 0, sp0, sp1, occ, sbit, base, cols, lane);
-    elim_insert<true>(T, rows + r0, r1 - r0, base, cols, M, lst[cur], &nl[cur], spill, spill_count, exp, exp_count,
-                      c0, bad, lane);
-    table_store(T, sp0, sp1, occ, sbit, base, cols, lane);
-    __syncwarp();
-    if (lane == 0) unlock_chunk(locks + d);
-  }
-  for (;;) {
-    __syncwarp();
-    const int n = min(nl[cur], ESC_CAP);
-    if (n == 0 || ++d >= nchunks) break;  // (rows past M were exported on the way)
-    const int64_t base = d * CE, cols = (M - base < CE) ? (M - base) : CE;
-    if (lane == 0) nl[cur ^ 1] = 0;
-    int old = 0;
-    if (lane == 0) old = lock_chunk(locks + d);
-    old = __shfl_sync(FULL_WARP, old, 0);
-    table_load(T, old == 0, sp0, sp1, occ, sbit, base, cols, lane);
-    elim_insert<false>(T, lst[cur], n, base, cols, M, lst[cur ^ 1], &nl[cur ^ 1], spill, spill_count, exp, exp_count,
-                       c0, bad, lane);
-    table_store(T, sp0, sp1, occ, sbit, base, cols, lane);
-    __syncwarp();
-    if (lane == 0) unlock_chunk(locks + d);
-    cur ^= 1;
-  }
-  if (__any_sync(FULL_WARP, bad) && lane == 0) atomicOr(inconsistent, 1);
-}
-
 __global__ void ribbon_ovf_hist_kernel(const RRow* o, const int64_t* np, int64_t* hist, int64_t M) {
   const int64_t n = *np;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -789,7 +559,7 @@ using namespace shk;
 // Byte offsets of the solver's buffers inside ShkRibbon::buf.
 struct RibLayout {
   size_t off_rows, off_rows2, off_ovf, off_exp, off_hist, off_rowoff, off_cursor, off_sp0, off_sp1, off_occ, off_sb,
-      off_forms, off_coef, off_y, off_yio, off_ymap, off_cnt, off_scan, off_lock, total;
+      off_forms, off_coef, off_y, off_yio, off_ymap, off_cnt, off_scan, total;
 };
 
 struct ShkRibbon {
@@ -859,8 +629,6 @@ RibLayout layout(int64_t N, int64_t m) {
   o += 256;
   L.off_scan = o;
   o += al(shk_scan_scratch(nch));
-  L.off_lock = o;
-  o += al((size_t)(nch + 1) * 4);
   L.total = o;
   return L;
 }
@@ -889,7 +657,6 @@ struct RibBufs {
   uint64_t *sp0, *sp1;
   uint32_t *occ, *sb;
   uint4 *forms, *coef, *yb, *yio, *ymap;
-  int* locks;
   void* scan;
   RibBufs(ShkRibbon* R, const RibLayout& L) {
     char* B = (char*)R->buf;
@@ -911,7 +678,6 @@ struct RibBufs {
     yio = (uint4*)(B + L.off_yio);
     ymap = (uint4*)(B + L.off_ymap);
     scan = B + L.off_scan;
-    locks = (int*)(B + L.off_lock);
   }
 };
 
@@ -924,7 +690,6 @@ int rib_clear(ShkRibbon* R, const RibLayout& L, int64_t M, cudaStream_t st) {
   SHK_CUDA(cudaMemsetAsync(b.occ, 0, (size_t)nw32 * 4, st));
   SHK_CUDA(cudaMemsetAsync(b.sb, 0, (size_t)nw32 * 4, st));
   SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 256, st));
-  SHK_CUDA(cudaMemsetAsync(b.locks, 0, (size_t)((M + CE - 1) / CE + 1) * 4, st));
   return 0;
 }
 
@@ -975,58 +740,8 @@ int rib_span(int pass) {
 // Passes run in batches without host round trips (every count stays on the
 // device; a pass with nothing pending costs one near-empty launch); the host
 // checks for completion once per batch.
-// The carry schedule (ribbon_elim_carry_kernel): one launch, plus one more
-// per round of spilled rows (a chunk that carried more than ESC_CAP rows).
-int rib_carry(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c0, int* bad_out, cudaStream_t st) {
-  RibBufs b(R, L);
-  const int64_t nch = (M + CE - 1) / CE;
-  int* bad = (int*)(b.cnt + 1);
-  *bad_out = 0;
-  int64_t stride = (int64_t)(0.618034 * (double)nch) | 1;
-  auto gcd = [](int64_t a, int64_t b2) {
-    while (b2) {
-      const int64_t t = a % b2;
-      a = b2;
-      b2 = t;
-    }
-    return a;
-  };
-  while (nch > 1 && gcd(stride, nch) != 1) stride += 2;
-  if (nch <= 1) stride = 1;
-  for (int round = 0;; ++round) {
-    SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 8, st));
-    ribbon_elim_carry_kernel<<<(unsigned)nch, 32, 0, st>>>(cur, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.locks,
-                                                           b.ovf, b.cnt, b.exp, b.cnt + 2, c0, bad, stride);
-    SHK_LAUNCHED();
-    int64_t h[2];
-    SHK_CUDA(cudaMemcpyAsync(h, b.cnt, 16, cudaMemcpyDeviceToHost, st));
-    SHK_CUDA(cudaStreamSynchronize(st));
-    if ((int)h[1]) {
-      *bad_out = 1;
-      return 0;
-    }
-    if (!h[0]) return 0;
-    if (round > 1000) {
-      shk_set_error("ribbon elimination did not converge");
-      return -1;
-    }
-    int rc = rib_regroup(b, b.ovf, b.cnt, M, c0, st);  // the spilled rows, grouped by chunk
-    if (rc) return rc;
-    cur = b.rows2;
-  }
-}
-
 int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c0, int first, int* bad_out,
                cudaStream_t st) {
-  // A/B (SHK_RIBBON_CARRY=1): the carry schedule measured 2.0 ms + a 0.58 ms
-  // spill round at C4 against 2.1 ms for the passes (warps wait on their
-  // right neighbour's lock, and 12.9 KB of shared memory per warp halves the
-  // resident warps), so the passes stay the default
-  static const bool carry = [] {
-    const char* e = getenv("SHK_RIBBON_CARRY");
-    return e && e[0] == '1';
-  }();
-  if (carry) return rib_carry(R, L, cur, M, c0, bad_out, st);
   RibBufs b(R, L);
   const int64_t nch = (M + CE - 1) / CE;
   int* bad = (int*)(b.cnt + 1);
