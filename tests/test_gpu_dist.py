@@ -293,3 +293,33 @@ def test_input_sharded_small_matches_single_gpu():
     ref = hashlib.sha256(recsplit.build(keys, 300, 20, 2).serialize()).hexdigest()
     out = _spawn(_worker_input_sharded, 4, 3000, 300, 20, 2)
     assert all(out[r][0] == ref for r in range(4))
+
+
+def _worker_nccl_input(rank, world, port, q, p2p):
+    """The input-sharded build over NCCL (device tensors for every
+    collective, all_to_all_single when p2p is "0")."""
+    import os
+
+    os.environ["SHK_DEVICE"] = "0"
+    os.environ["SHK_P2P"] = p2p
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        from paper_2308_09561_b200 import dist as shdist
+        from paper_2308_09561_b200 import workloads as W
+
+        keys = W.build_keys(2)
+        blob = np.frombuffer(np.ascontiguousarray(keys, dtype="<u8").tobytes(), dtype=np.uint8)
+        desc, _ = shdist.build_blob_sharded_input(blob, 8, len(keys), 500, 24, 1, device=torch.device("cuda", 0))
+        q.put((rank, hashlib.sha256(desc.serialize()).hexdigest()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_nccl_input_sharded_matches_reference(p2p):
+    out = _spawn(_worker_nccl_input, 1, p2p)
+    assert out[0] == golden("c2.json")["desc_sha"]
