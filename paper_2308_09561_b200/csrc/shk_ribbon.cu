@@ -282,14 +282,26 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
 // ---------------------------------------------------------------------------
 // Symbolic back substitution (affine forms), one CTA of 4 warps per
 // back-chunk.  Warp q, lane L owns unknown u = 4L + q (u = 127 is the
-// constant term) and keeps W_u: a 128-bit window whose bit k is the
+// constant term) and tracks W_u: a 128-bit window whose bit k is the
 // coefficient of u in sol[c + 1 + k].  forms_out[chunk][u] = W_u after the
 // chunk's first column.  Every column's own affine form is also written
 // (coef[col], word q = ballot of warp q's new bits: bit L = coefficient of
 // unknown 4L + q), so the final pass is a parallel map instead of a second
-// sequential walk.  The CTA stages 256-column tiles of pivot patterns as
-// (p >> 1) in four words, zero for free columns, so the per-column loop of a
-// warp is branch-free: LDS.128, 4 AND/XOR, POPC, ballot, window shift.
+// sequential walk.
+//
+// The window is not shifted per column.  Columns go in aligned groups of 32
+// (right to left); within a group the window at the column k steps below
+// the group's top is (Wg << k) | N, Wg = the window at the group's top and
+// N = the k bits produced since.  So parity(W & p) = parity(Wg & (p >> k))
+// ^ parity(N & low_k(p)): the CTA stages each column's pattern pre-shifted
+// by its k (k = 31 - col % 32, fixed per staging thread) plus its low k bits,
+// and a warp's per-column step is LDS.128 + LDS, 5 AND/XOR, POPC, ballot and
+// N = 2N + bit; the 4-word window moves once per group (a word rename).
+// Window bit 127 (sol[c + 128], never used by a 127-bit pattern) is pinned to
+// 1 for the constant term and 0 for the unknowns, and the staged pattern
+// carries the column's rhs in that bit, so the constant lane's parity picks up
+// the rhs with no branch (the pre-shifted pattern is zero in bits 127-k..126,
+// which pair with the bits of Wg that have left the window).
 __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
                                                            const uint64_t* sp1, const uint32_t* occ,
                                                            const uint32_t* sbit, uint4* forms, uint4* coef) {
@@ -297,6 +309,7 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
   // thread's global loads for tile k+1 are in flight, and the finished
   // coefficients of tile k-1 are written out; one barrier per tile
   __shared__ uint4 tpw[2][256];
+  __shared__ uint32_t tlo[2][256];
   __shared__ uint32_t tcoef[2][256][4];
   const int64_t c = blockIdx.x;
   if (c >= nbchunks) return;
@@ -304,20 +317,23 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
   const int u = 4 * lane + q;
   const int64_t s0 = c * CB;
   const int64_t e = (s0 + CB < m) ? s0 + CB : m;
-  // Window bit 127 (sol[c + 128], never used by a 127-bit pattern) is pinned
-  // to 1 for the constant term and 0 for the unknowns, and the staged
-  // pattern carries the column's rhs in that bit, so the constant lane's
-  // parity picks up the rhs with no branch or extra load: W = e_u initially
-  // is exactly that for u = 127.
-  uint32_t W0 = 0, W1 = 0, W2 = 0, W3 = 0;
-  {
-    const uint32_t b = 1u << (u & 31);
-    W0 = (u >> 5) == 0 ? b : 0u;
-    W1 = (u >> 5) == 1 ? b : 0u;
-    W2 = (u >> 5) == 2 ? b : 0u;
-    W3 = (u >> 5) == 3 ? b : 0u;
-  }
   const uint32_t kmask = (u == 127) ? 0x80000000u : 0u;
+  // initial window e_u (bit 127 = kmask) split at the top column's group
+  // offset k0 (tiles and groups are 32-aligned; k0 > 0 only at the system end)
+  const int k0 = 31 - (int)((e - 1) & 31);
+  uint32_t W0 = 0, W1 = 0, W2 = 0, W3 = kmask, N = 0;
+  if (u < 127) {
+    if (u < k0) {
+      N = 1u << u;
+    } else {
+      const int v = u - k0;
+      const uint32_t b = 1u << (v & 31);
+      W0 = (v >> 5) == 0 ? b : 0u;
+      W1 = (v >> 5) == 1 ? b : 0u;
+      W2 = (v >> 5) == 2 ? b : 0u;
+      W3 |= (v >> 5) == 3 ? b : 0u;
+    }
+  }
   // tiles from the top: tile 0 is [tstart(e-1), e), tile k+1 ends where tile k starts
   auto tile_start = [&](int64_t col) { return (col / 256) * 256 > s0 ? (col / 256) * 256 : s0; };
   // per-thread prefetch registers: columns tid and tid + 128 of a tile
@@ -339,19 +355,37 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
       }
     }
   };
+  const int ks = 31 - lane;  // group offset of this thread's staged columns (tid and tid + 128)
   auto stash = [&](int buf, int nt) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int j = tid + 128 * h;
       if (j < nt) {
         const uint64_t a0 = pa0[h], a1 = pa1[h];
-        // p >> 1 as four 32-bit words; bit 127 = the column's rhs
-        tpw[buf][j] = make_uint4((uint32_t)(a0 >> 1) | ((uint32_t)(a0 >> 32) << 31),
-                                 (uint32_t)(a0 >> 33) | ((uint32_t)a1 << 31),
-                                 (uint32_t)(a1 >> 1) | ((uint32_t)(a1 >> 32) << 31),
-                                 (uint32_t)(a1 >> 33) | (prhs[h] << 31));
+        // p >> 1 as four 32-bit words (127 bits)
+        const uint32_t x = (uint32_t)(a0 >> 1) | ((uint32_t)(a0 >> 32) << 31);
+        const uint32_t y = (uint32_t)(a0 >> 33) | ((uint32_t)a1 << 31);
+        const uint32_t z = (uint32_t)(a1 >> 1) | ((uint32_t)(a1 >> 32) << 31);
+        const uint32_t w = (uint32_t)(a1 >> 33);
+        tpw[buf][j] = make_uint4(__funnelshift_r(x, y, ks), __funnelshift_r(y, z, ks), __funnelshift_r(z, w, ks),
+                                 (w >> ks) | (prhs[h] << 31));
+        tlo[buf][j] = x & ((1u << ks) - 1u);
       }
     }
+  };
+  auto step = [&](int buf, int j) {
+    const uint4 p = tpw[buf][j];
+    const uint32_t nb = __popc((W0 & p.x) ^ (W1 & p.y) ^ (W2 & p.z) ^ (W3 & p.w) ^ (N & tlo[buf][j])) & 1u;
+    const uint32_t bal = __ballot_sync(FULL_WARP, nb);
+    if (lane == 0) tcoef[buf][j][q] = bal;
+    N = 2u * N + nb;
+  };
+  auto next_group = [&]() {
+    W3 = (W2 & 0x7FFFFFFFu) | kmask;
+    W2 = W1;
+    W1 = W0;
+    W0 = N;
+    N = 0;
   };
   int64_t col = e - 1;
   int64_t ts = tile_start(col);
@@ -366,15 +400,16 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
     const int64_t nts = ts - 1 >= s0 ? tile_start(ts - 1) : -1;
     const int nnt = nts >= 0 ? (int)(ts - nts) : 0;
     if (nnt) prefetch(nts, nnt);
-    for (int j = nt - 1; j >= 0; --j) {
-      const uint4 p = tpw[buf][j];
-      const uint32_t nb = __popc((W0 & p.x) ^ (W1 & p.y) ^ (W2 & p.z) ^ (W3 & p.w)) & 1u;
-      const uint32_t bal = __ballot_sync(FULL_WARP, nb);
-      if (lane == 0) tcoef[buf][j][q] = bal;
-      W3 = (__funnelshift_l(W2, W3, 1) & 0x7FFFFFFFu) | kmask;
-      W2 = __funnelshift_l(W1, W2, 1);
-      W1 = __funnelshift_l(W0, W1, 1);
-      W0 = (W0 << 1) | nb;
+    int j = nt - 1;
+    while ((j & 31) != 31) {  // partial top group (the system's last columns only)
+      step(buf, j);
+      if ((j & 31) == 0) next_group();
+      --j;
+    }
+    for (; j >= 0; j -= 32) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) step(buf, j - t);
+      next_group();
     }
     if (nnt) stash(buf ^ 1, nnt);
     // coefficients of the previous tile (complete since the last barrier)
