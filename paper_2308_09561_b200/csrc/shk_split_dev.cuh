@@ -16,6 +16,23 @@ namespace shk {
 // partition stores.
 SHK_D ulonglong2 load_key(const ulonglong2* p) { return *p; }
 
+// (analysis builds, -DSHK_SPLIT_WORK) lane-key evaluations the fast split
+// searches issue: [0] keys x 32 lanes per seed block, [1] seed blocks
+#ifdef SHK_SPLIT_WORK
+__device__ unsigned long long g_split_work[2];
+#define SHK_SPLIT_WORK_ADD(keys)                                     \
+  do {                                                               \
+    if (lane == 0) {                                                 \
+      atomicAdd(&g_split_work[0], 32ull * (unsigned long long)(keys)); \
+      atomicAdd(&g_split_work[1], 1ull);                             \
+    }                                                                \
+  } while (0)
+#else
+#define SHK_SPLIT_WORK_ADD(keys) \
+  do {                           \
+  } while (0)
+#endif
+
 // Part index of split hash value r against cumulative bounds (up to 4 parts).
 SHK_D uint32_t part_of(uint32_t r, uint32_t b0, uint32_t b1, uint32_t b2) {
   return (uint32_t)(r >= b0) + (uint32_t)(r >= b1) + (uint32_t)(r >= b2);
@@ -154,6 +171,7 @@ SHK_D int64_t split_search_fast(const ulonglong2* kp, const ShkSplitTask& task, 
       if (F == 4) ovf |= (g1 - g2 > s1) | (g2 - g3 > s2) | (g3 > s3);
       fail |= ovf;
     }
+    SHK_SPLIT_WORK_ADD(all_failed ? i + 8 : m);
     const unsigned ab = __ballot_sync(FULL_WARP, !fail);
     if (ab) return (int64_t)(R + (uint64_t)(__ffs(ab) - 1));
   }
@@ -231,6 +249,7 @@ SHK_D int64_t split_search_equal(const ulonglong2* kp, const ShkSplitTask& task,
       }
       fail |= over(m);
     }
+    SHK_SPLIT_WORK_ADD(all_failed ? i + 8 : m);
     const unsigned ab = __ballot_sync(FULL_WARP, !fail);
     if (ab) return (int64_t)(R + (uint64_t)(__ffs(ab) - 1));
   }

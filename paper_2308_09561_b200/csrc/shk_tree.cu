@@ -298,3 +298,13 @@ extern "C" int shk_debug_tree_trace_m(unsigned int* out, int64_t n) {
   return 0;
 }
 #endif
+#ifdef SHK_SPLIT_WORK
+extern "C" int shk_debug_split_work(unsigned long long* out, int reset) {
+  SHK_CUDA(cudaMemcpyFromSymbol(out, g_split_work, 16));
+  if (reset) {
+    const unsigned long long z[2] = {0, 0};
+    SHK_CUDA(cudaMemcpyToSymbol(g_split_work, z, 16));
+  }
+  return 0;
+}
+#endif
