@@ -26,6 +26,7 @@
 //      chunk's boundary), a fully parallel map (step 3 stored the forms).
 #include <cuda_pipeline.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -147,7 +148,7 @@ __global__ void ribbon_rows_scatter_kernel(const int64_t* starts, const uint64_t
 // insertion order yields the same final solution.
 // S: elimination chunks merged per warp (1 for the first pass; later passes
 // take S consecutive chunks so a row can walk S chunks in one pass).
-template <int S>
+template <int S, bool RING>
 __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const int64_t* row_off, int64_t nchunks,
                                                          int64_t m, uint64_t* sp0, uint64_t* sp1, uint32_t* occ,
                                                          uint32_t* sbit, RRow* ovf, int64_t* ovf_count,
@@ -179,35 +180,61 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
     }
   }
   __syncwarp();
-  int64_t next = lane;
   bool active = false, bad = false;
   uint64_t a0 = 0, a1 = 0;
   uint32_t b = 0;
   int j = 0;
-  // Each lane keeps its following row in registers: the global load is
-  // issued when the current row starts and consumed when it finishes, so its
-  // latency hides behind the current row's elimination steps.
-  RRow pre{0, 0, 0};
-  bool have_pre = false;
-  auto load_pre = [&]() {
-    have_pre = next < nrows;
-    if (have_pre) {
-      pre = rows[r0 + next];
-      next += 32;
+  // RING (the first pass: ~490 rows per chunk): rows are handed out in order
+  // from a 64-row shared ring -- the lanes whose row finished take the next
+  // ones at the top of an iteration (ballot rank) -- refilled 32 rows at a
+  // time from a register stage whose global loads were issued one refill
+  // earlier, so no lane waits on a global load for its next row (with one
+  // row prefetched per lane, a lane whose rows claim a slot at once -- the
+  // first rows of a chunk -- stalled the warp for a global round trip almost
+  // every iteration: C4 pass 0 0.95 -> 0.66 ms, C2 0.23 -> 0.13 ms).  The
+  // later passes hold a few rows per warp that walk long; there lane i takes
+  // rows i, i + 32, ... with one row prefetched (the ring's per-iteration
+  // bookkeeping sits on their walk's critical path).
+  __shared__ RRow ring[RING ? 64 : 1];
+  const unsigned lt = (1u << lane) - 1u;
+  int64_t head = 0, filled = 0;  // RING, warp-uniform: rows handed out / stored in the ring
+  RRow stage{0, 0, 0};
+  int64_t next = lane;  // !RING: this lane's next row
+  if (lane < nrows) stage = rows[r0 + lane];
+  if (!RING) next += 32;
+  auto refill = [&]() {
+    const int64_t k = nrows - filled < 32 ? nrows - filled : 32;
+    if (lane < k) ring[(filled + lane) & 63] = stage;
+    filled += k;
+    if (filled + lane < nrows) stage = rows[r0 + filled + lane];
+    __syncwarp();
+  };
+  auto start = [&](const RRow& r) {
+    active = true;
+    a0 = r.p0;
+    a1 = r.p1;
+    b = (r.s & RHS_BIT) ? 1u : 0u;
+    j = (int)((r.s & S_MASK) - base);
+  };
+  auto take = [&]() {
+    if constexpr (RING) {
+      if (filled - head < 32 && filled < nrows) refill();
+      const unsigned need = __ballot_sync(FULL_WARP, !active);
+      if (!active) {
+        const int64_t idx = head + __popc(need & lt);
+        if (idx < filled) start(ring[idx & 63]);
+      }
+      head += __popc(need);
+      if (head > filled) head = filled;
+    } else {
+      if (!active && next - 32 < nrows) {
+        start(stage);
+        if (next < nrows) stage = rows[r0 + next];
+        next += 32;
+      }
     }
   };
-  auto fetch = [&]() {
-    active = have_pre;
-    if (active) {
-      a0 = pre.p0;
-      a1 = pre.p1;
-      b = (pre.s & RHS_BIT) ? 1u : 0u;
-      j = (int)((pre.s & S_MASK) - base);
-    }
-    load_pre();
-  };
-  load_pre();
-  fetch();
+  take();
   while (__any_sync(FULL_WARP, active)) {
     // phase A: read the slot at the current pivot
     const bool esc = active && j >= CEs;
@@ -229,7 +256,7 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
         o.p1 = a1;
         o.s = (base + j) | (b ? RHS_BIT : 0);
         ovf[kk] = o;
-        fetch();
+        active = false;
       } else {
         const uint32_t bitm = 1u << (j & 31);
         if (w & bitm) {
@@ -238,7 +265,7 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
           b ^= (sw >> (j & 31)) & 1u;
           if ((a0 | a1) == 0) {
             if (b) bad = true;
-            fetch();
+            active = false;
           } else {
             int t;
             if (a0) {
@@ -258,12 +285,13 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
             q0s[j] = a0;
             q1s[j] = a1;
             if (b) atomicOr(&sbs[j >> 5], bitm);
-            fetch();
+            active = false;
           }
         }
       }
     }
     __syncwarp();
+    take();
   }
   if (__any_sync(FULL_WARP, bad) && lane == 0) atomicOr(inconsistent, 1);
   __syncwarp();
@@ -302,7 +330,7 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
 // carries the column's rhs in that bit, so the constant lane's parity picks up
 // the rhs with no branch (the pre-shifted pattern is zero in bits 127-k..126,
 // which pair with the bits of Wg that have left the window).
-__global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nbchunks, const uint64_t* sp0,
+__global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nbchunks, int cb, const uint64_t* sp0,
                                                            const uint64_t* sp1, const uint32_t* occ,
                                                            const uint32_t* sbit, uint4* forms, uint4* coef) {
   // double-buffered 256-column tiles: while the warps walk tile k, each
@@ -315,8 +343,8 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
   if (c >= nbchunks) return;
   const int tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
   const int u = 4 * lane + q;
-  const int64_t s0 = c * CB;
-  const int64_t e = (s0 + CB < m) ? s0 + CB : m;
+  const int64_t s0 = c * cb;
+  const int64_t e = (s0 + cb < m) ? s0 + cb : m;
   const uint32_t kmask = (u == 127) ? 0x80000000u : 0u;
   // initial window e_u (bit 127 = kmask) split at the top column's group
   // offset k0 (tiles and groups are 32-aligned; k0 > 0 only at the system end)
@@ -510,7 +538,7 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
 
 // Final back substitution, a parallel map: sol[col] = parity(coef[col] &
 // ysel[chunk]); one warp per 64-bit solution word (two ballots).
-__global__ void ribbon_final_kernel(int64_t m, int64_t nwords, const uint4* __restrict__ coef,
+__global__ void ribbon_final_kernel(int64_t m, int64_t nwords, int cb, const uint4* __restrict__ coef,
                                     const uint4* __restrict__ ysel, uint64_t* words) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -522,7 +550,7 @@ __global__ void ribbon_final_kernel(int64_t m, int64_t nwords, const uint4* __re
       uint32_t bit = 0;
       if (cc < m) {
         const uint4 a = __ldcs(coef + cc);
-        const uint4 y = __ldg(ysel + cc / CB);
+        const uint4 y = __ldg(ysel + cc / cb);
         bit = __popc((a.x & y.x) ^ (a.y & y.y) ^ (a.z & y.z) ^ (a.w & y.w)) & 1u;
       }
       bits[h] = __ballot_sync(FULL_WARP, bit);
@@ -622,10 +650,21 @@ namespace {
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Back-substitution chunk for M columns: the forms pass costs ~cb column
+// steps on one CTA (latency-bound when there are few chunks) and the chain
+// ~M / cb sequential mat-vecs, so small systems take short chunks (a power
+// of two in [256, CB], ~sqrt(11.5 M)); large ones CB (throughput-bound).
+int rib_cb(int64_t M) {
+  const double want = sqrt((double)M * 11.5);
+  int cb = 256;
+  while (cb < want && cb < CB) cb <<= 1;
+  return cb;
+}
+
 RibLayout layout(int64_t N, int64_t m) {
   RibLayout L;
   int64_t nch = (m + CE - 1) / CE;
-  int64_t nbc = (m + CB - 1) / CB;
+  int64_t nbc = (m + rib_cb(m) - 1) / rib_cb(m);
   int64_t nw32 = (m + 31) / 32 + CE / 32;
   size_t o = 0;
   L.off_rows = o;
@@ -800,12 +839,18 @@ int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c
       RRow* src = pass == 0 ? cur : b.rows2;
       const int fp = (first && pass == 0) ? 1 : 0;
       const unsigned g = (unsigned)((nch + S - 1) / S);
-      if (S == 1)
-        ribbon_elim_kernel<1><<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+      if (S == 1 && pass == 0)
+        ribbon_elim_kernel<1, true>
+            <<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+      else if (S == 1)
+        ribbon_elim_kernel<1, false>
+            <<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
       else if (S == 2)
-        ribbon_elim_kernel<2><<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+        ribbon_elim_kernel<2, false>
+            <<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
       else
-        ribbon_elim_kernel<4><<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+        ribbon_elim_kernel<4, false>
+            <<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
       SHK_LAUNCHED();
       if (trace) {
         cudaEventRecord(e1, st);
@@ -841,8 +886,9 @@ int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c
 // bits; words_out (device) gets ceil(M/64) solution words.
 int rib_forms(ShkRibbon* R, const RibLayout& L, int64_t M, cudaStream_t st) {
   RibBufs b(R, L);
-  const int64_t nbc = (M + CB - 1) / CB;
-  ribbon_forms_kernel<<<(unsigned)nbc, 128, 0, st>>>(M, nbc, b.sp0, b.sp1, b.occ, b.sb, b.forms, b.coef);
+  const int cb = rib_cb(M);
+  const int64_t nbc = (M + cb - 1) / cb;
+  ribbon_forms_kernel<<<(unsigned)nbc, 128, 0, st>>>(M, nbc, cb, b.sp0, b.sp1, b.occ, b.sb, b.forms, b.coef);
   SHK_LAUNCHED();
   return 0;
 }
@@ -851,7 +897,8 @@ int rib_forms(ShkRibbon* R, const RibLayout& L, int64_t M, cudaStream_t st) {
 int rib_chain_final(ShkRibbon* R, const RibLayout& L, int64_t M, const uint32_t* y_in, uint32_t* y_out,
                     uint64_t* words_out, cudaStream_t st) {
   RibBufs b(R, L);
-  const int64_t nbc = (M + CB - 1) / CB;
+  const int cb = rib_cb(M);
+  const int64_t nbc = (M + cb - 1) / cb;
   const uint4 y0 = y_in ? make_uint4(y_in[0], y_in[1], y_in[2], y_in[3]) : make_uint4(0, 0, 0, 0);
   SHK_CUDA(cudaMemcpyAsync(b.yio, &y0, 16, cudaMemcpyHostToDevice, st));
   ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, b.forms, b.yb, b.yio);
@@ -859,7 +906,7 @@ int rib_chain_final(ShkRibbon* R, const RibLayout& L, int64_t M, const uint32_t*
   const int64_t nwords = (M + 63) / 64;
   int64_t fb = (nwords + 7) / 8;
   if (fb > 148 * 8) fb = 148 * 8;
-  ribbon_final_kernel<<<(unsigned)fb, 256, 0, st>>>(M, nwords, b.coef, b.yb, words_out);
+  ribbon_final_kernel<<<(unsigned)fb, 256, 0, st>>>(M, nwords, cb, b.coef, b.yb, words_out);
   SHK_LAUNCHED();
   if (y_out) {
     SHK_CUDA(cudaMemcpyAsync(y_out, b.yio, 16, cudaMemcpyDeviceToHost, st));
@@ -1019,7 +1066,7 @@ int shk_ribbon_dist_map(ShkRibbon* R, uint32_t* map_out, cudaStream_t st) {
   RibBufs b(R, R->dL);
   int rc = rib_forms(R, R->dL, R->dM, st);
   if (rc) return rc;
-  const int64_t nbc = (R->dM + CB - 1) / CB;
+  const int64_t nbc = (R->dM + rib_cb(R->dM) - 1) / rib_cb(R->dM);
   ribbon_chain_kernel<<<128, 32, 0, st>>>(nbc, b.forms, nullptr, b.ymap);
   SHK_LAUNCHED();
   SHK_CUDA(cudaMemcpyAsync(map_out, b.ymap, 128 * 16, cudaMemcpyDeviceToHost, st));
