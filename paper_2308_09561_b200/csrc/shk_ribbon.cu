@@ -313,9 +313,11 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
 // constant term) and tracks W_u: a 128-bit window whose bit k is the
 // coefficient of u in sol[c + 1 + k].  forms_out[chunk][u] = W_u after the
 // chunk's first column.  Every column's own affine form is also written
-// (coef[col], word q = ballot of warp q's new bits: bit L = coefficient of
-// unknown 4L + q), so the final pass is a parallel map instead of a second
-// sequential walk.
+// (coef[col], word q bit L = coefficient of unknown 4L + q, i.e. warp q's
+// new bits of that column across its lanes), so the final pass is a
+// parallel map instead of a second sequential walk.  A lane collects its own
+// bits of a 32-column group in N anyway, so the words come from one 32 x 32
+// bit transpose per group (no per-column ballot or store).
 //
 // The window is not shifted per column.  Columns go in aligned groups of 32
 // (right to left); within a group the window at the column k steps below
@@ -404,9 +406,23 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
   auto step = [&](int buf, int j) {
     const uint4 p = tpw[buf][j];
     const uint32_t nb = __popc((W0 & p.x) ^ (W1 & p.y) ^ (W2 & p.z) ^ (W3 & p.w) ^ (N & tlo[buf][j])) & 1u;
-    const uint32_t bal = __ballot_sync(FULL_WARP, nb);
-    if (lane == 0) tcoef[buf][j][q] = bal;
     N = 2u * N + nb;
+  };
+  // End of a group whose lowest column is tile index gb and which made cnt
+  // columns: bit t of N (t < cnt) is this lane's unknown's coefficient in
+  // column gb + t.  A 32 x 32 bit transpose across the warp (5 shuffle
+  // stages) gives lane t the column's word (bit L = unknown 4L + q), stored
+  // once per group instead of a ballot and a store per column.
+  auto flush = [&](int buf, int gb, int cnt) {
+    uint32_t x = N;
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+      const uint32_t M = sft == 16 ? 0x0000FFFFu : sft == 8 ? 0x00FF00FFu : sft == 4 ? 0x0F0F0F0Fu
+                         : sft == 2 ? 0x33333333u : 0x55555555u;
+      const uint32_t y = __shfl_xor_sync(FULL_WARP, x, sft);
+      x = (lane & sft) ? ((x & ~M) | ((y >> sft) & M)) : ((x & M) | ((y << sft) & ~M));
+    }
+    if (lane < cnt) tcoef[buf][gb + lane][q] = x;
   };
   auto next_group = [&]() {
     W3 = (W2 & 0x7FFFFFFFu) | kmask;
@@ -429,14 +445,16 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
     const int nnt = nts >= 0 ? (int)(ts - nts) : 0;
     if (nnt) prefetch(nts, nnt);
     int j = nt - 1;
-    while ((j & 31) != 31) {  // partial top group (the system's last columns only)
-      step(buf, j);
-      if ((j & 31) == 0) next_group();
-      --j;
+    if ((j & 31) != 31) {  // partial top group (the system's last columns only)
+      const int gb = j & ~31, cnt = j - gb + 1;
+      for (; j >= gb; --j) step(buf, j);
+      flush(buf, gb, cnt);
+      next_group();
     }
     for (; j >= 0; j -= 32) {
 #pragma unroll
       for (int t = 0; t < 32; ++t) step(buf, j - t);
+      flush(buf, j - 31, 32);
       next_group();
     }
     if (nnt) stash(buf ^ 1, nnt);

@@ -199,45 +199,65 @@ SHK_D bool equal_split_ok(int F, int m) {
   return F != 4 || m < 172;
 }
 
+#ifndef SHK_SPLIT_EQ_BLOCK
+#define SHK_SPLIT_EQ_BLOCK 8  // keys between overflow checks of the equal-part search
+#endif
+#ifndef SHK_SPLIT_EQ_SEEDS
+#define SHK_SPLIT_EQ_SEEDS 1  // seeds per lane (S > 1: lane tests R + lane + 32 j, j < S, per key load)
+#endif
 template <int F>
 SHK_D int64_t split_search_equal(const ulonglong2* kp, const ShkSplitTask& task, uint64_t max_seed, int lane) {
+  constexpr int U = SHK_SPLIT_EQ_BLOCK, S = SHK_SPLIT_EQ_SEEDS;
   const int m = task.m;
   const int sz = m / F;
   const uint32_t K4 = (uint32_t)(127 - sz) * 0x01010101u;  // byte b > sz <=> bit 7 of (b + 127 - sz)
-  for (uint64_t R = 0; R < max_seed; R += 32) {
-    const uint64_t s = R + lane;
-    const u2 x = seed_mixer_pre_d(s, TAG_SPLIT);
-    uint32_t a = 0, b = 0;
-    bool fail = !(s < max_seed);
+  for (uint64_t R = 0; R < max_seed; R += 32 * S) {
+    u2 x[S];
+    uint32_t a[S], b[S];
+    bool fail[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const uint64_t s = R + lane + 32 * j;
+      x[j] = seed_mixer_pre_d(s, TAG_SPLIT);
+      a[j] = 0;
+      b[j] = 0;
+      fail[j] = !(s < max_seed);
+    }
     bool all_failed = false;
     int i = 0;
-    auto count = [&](uint32_t vh) {
+    auto count = [&](int j, uint32_t vh) {
       if (F == 2) {
-        a += vh >> 31;
+        a[j] += vh >> 31;
       } else if (F == 3) {
         const uint32_t p = __umulhi(vh, 3u);
-        a += p;
-        b += p >> 1;
+        a[j] += p;
+        b[j] += p >> 1;
       } else {
-        a += 1u << ((vh >> 27) & 24u);
+        a[j] += 1u << ((vh >> 27) & 24u);
       }
     };
-    auto over = [&](int done) -> bool {
-      if (F == 2) return (done - (int)a > sz) || ((int)a > sz);
+    auto over = [&](int j, int done) -> bool {
+      if (F == 2) return (done - (int)a[j] > sz) || ((int)a[j] > sz);
       if (F == 3) {
-        const int c2 = (int)b, c1 = (int)a - 2 * c2;
+        const int c2 = (int)b[j], c1 = (int)a[j] - 2 * c2;
         return (done - c1 - c2 > sz) || (c1 > sz) || (c2 > sz);
       }
-      return ((a + K4) & 0x80808080u) != 0u;
+      return ((a[j] + K4) & 0x80808080u) != 0u;
     };
-    for (; i + 8 <= m; i += 8) {
+    for (; i + U <= m; i += U) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const ulonglong2 k = load_key(kp + i + u);
-        count(remix_hi_pre_d(split64(k.x), split64(k.y), x));
+#pragma unroll
+        for (int j = 0; j < S; ++j) count(j, remix_hi_pre_d(split64(k.x), split64(k.y), x[j]));
       }
-      fail |= over(i + 8);
-      if (__all_sync(FULL_WARP, fail)) {
+      bool af = true;
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        fail[j] |= over(j, i + U);
+        af &= fail[j];
+      }
+      if (__all_sync(FULL_WARP, af)) {
         all_failed = true;
         break;
       }
@@ -245,13 +265,18 @@ SHK_D int64_t split_search_equal(const ulonglong2* kp, const ShkSplitTask& task,
     if (!all_failed) {
       for (; i < m; ++i) {
         const ulonglong2 k = load_key(kp + i);
-        count(remix_hi_pre_d(split64(k.x), split64(k.y), x));
+#pragma unroll
+        for (int j = 0; j < S; ++j) count(j, remix_hi_pre_d(split64(k.x), split64(k.y), x[j]));
       }
-      fail |= over(m);
+#pragma unroll
+      for (int j = 0; j < S; ++j) fail[j] |= over(j, m);
     }
-    SHK_SPLIT_WORK_ADD(all_failed ? i + 8 : m);
-    const unsigned ab = __ballot_sync(FULL_WARP, !fail);
-    if (ab) return (int64_t)(R + (uint64_t)(__ffs(ab) - 1));
+    SHK_SPLIT_WORK_ADD(S * (all_failed ? i + U : m));
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const unsigned ab = __ballot_sync(FULL_WARP, !fail[j]);
+      if (ab) return (int64_t)(R + 32 * j + (uint64_t)(__ffs(ab) - 1));
+    }
   }
   return -1;
 }
