@@ -61,7 +61,7 @@ __global__ void orient_kernel(const uint8_t* eu, const uint8_t* ev, const int64_
 using namespace shk;
 
 int shk_launch_leaf_search(const ShkLeafLaunch& p, cudaStream_t st) {
-  LeafArgs a;
+  LeafArgs a{};
   a.hi = p.hi;
   a.lo = p.lo;
   a.off = p.off;

@@ -48,7 +48,10 @@ constexpr int CE = SHK_RIBBON_CE;
 #define SHK_RIBBON_CB 8192
 #endif
 constexpr int CB = SHK_RIBBON_CB;
-#define RIB_SPAN_DEFAULT "1,2"  // back-substitution chunk (columns), multiple of CE and 64
+#define RIB_SPAN_DEFAULT "1,2"
+// Rows per chunk bin of the emitted rows (a 512-column chunk gets ~488 rows
+// on average at eps = 0.05, sd ~22; a full bin spills to the overflow list).
+constexpr int64_t RIB_BIN_CAP = 576;  // back-substitution chunk (columns), multiple of CE and 64
 
 struct RRow {
   uint64_t p0, p1;
@@ -115,6 +118,35 @@ __global__ void ribbon_keyrows_scatter_kernel(const ulonglong2* keys, const uint
   }
 }
 
+// Rows from keys straight into per-chunk bins of `cap` rows (no histogram
+// pass): a row's slot is one atomicAdd on its chunk's count; rows past a full
+// bin go to the overflow list, which the second elimination pass takes with
+// the first pass's own overflow (single-GPU solve over all columns).
+__global__ void ribbon_keyrows_bins_kernel(const ulonglong2* keys, const uint8_t* rhs, int64_t N, int64_t m,
+                                           uint64_t seed, unsigned long long* bcnt, int64_t cap, RRow* bins,
+                                           RRow* ovf, unsigned long long* ovf_cnt) {
+  const u2 xs = split64(seed_mixer(seed, TAG_RSTART));
+  const u2 x0 = split64(seed_mixer(seed, TAG_RPAT0));
+  const u2 x1 = split64(seed_mixer(seed, TAG_RPAT1));
+  const uint64_t span = (uint64_t)(m - RIBBON_W + 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 k = keys[i];
+    u2 kh = split64(k.x), kl = split64(k.y);
+    u2 v = remix_d(kh, kl, xs);
+    const int64_t s = (int64_t)(((uint64_t)v.hi * span) >> 32);
+    const int64_t ch = s / CE;
+    const unsigned long long pos = atomicAdd(bcnt + ch, 1ull);
+    u2 a = remix_d(kh, kl, x0);
+    u2 b = remix_d(kh, kl, x1);
+    RRow r;
+    r.p0 = join64(a.lo | 1u, a.hi);
+    r.p1 = join64(b.lo, b.hi);
+    r.s = s | ((rhs[i] & 1) ? RHS_BIT : 0);
+    RRow* dst = pos < (unsigned long long)cap ? bins + ch * cap + (int64_t)pos : ovf + atomicAdd(ovf_cnt, 1ull);
+    *dst = r;
+  }
+}
+
 // Explicit rows (ribbon_solve seam).
 __global__ void ribbon_rows_hist_kernel(const int64_t* starts, int64_t N, int64_t* hist) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
@@ -148,8 +180,12 @@ __global__ void ribbon_rows_scatter_kernel(const int64_t* starts, const uint64_t
 // insertion order yields the same final solution.
 // S: elimination chunks merged per warp (1 for the first pass; later passes
 // take S consecutive chunks so a row can walk S chunks in one pass).
+// Bin mode (bcnt != nullptr, S = 1): chunk c's rows are rows[c cap, c cap +
+// min(bcnt[c], cap)) (rows emitted by the construction kernel) instead of the
+// CSR range row_off[c], row_off[c + 1].
 template <int S, bool RING>
-__global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const int64_t* row_off, int64_t nchunks,
+__global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const int64_t* row_off,
+                                                         const unsigned long long* bcnt, int64_t cap, int64_t nchunks,
                                                          int64_t m, uint64_t* sp0, uint64_t* sp1, uint32_t* occ,
                                                          uint32_t* sbit, RRow* ovf, int64_t* ovf_count,
                                                          int* inconsistent, int first_pass) {
@@ -158,7 +194,15 @@ __global__ void __launch_bounds__(32) ribbon_elim_kernel(const RRow* rows, const
   __shared__ uint32_t occs[CEs / 32], sbs[CEs / 32];
   const int64_t c = blockIdx.x;
   if (c * S >= nchunks) return;
-  const int64_t r0 = row_off[c * S], r1 = row_off[(c + 1) * S < nchunks ? (c + 1) * S : nchunks];
+  int64_t r0, r1;
+  if (bcnt) {
+    r0 = c * cap;
+    const unsigned long long k = bcnt[c];
+    r1 = r0 + (k < (unsigned long long)cap ? (int64_t)k : cap);
+  } else {
+    r0 = row_off[c * S];
+    r1 = row_off[(c + 1) * S < nchunks ? (c + 1) * S : nchunks];
+  }
   if (r0 == r1) return;
   const int lane = threadIdx.x;
   const int64_t base = c * CEs;
@@ -477,35 +521,51 @@ __global__ void __launch_bounds__(128) ribbon_forms_kernel(int64_t m, int64_t nb
 }
 
 // Right-to-left chain over back-chunks: y = first 127 solution bits of chunk
-// c + 1 (right boundary of chunk c).  One warp; the next chunk's forms are
-// loaded while the current one is evaluated.  ysel[c] is the boundary in the
-// coef layout (word q bit L = y bit 4L + q; bit 127 = 1 for the constant).
-// y_io (device, one uint4): in = the 127 solution bits right of the last chunk
-// (zero at the end of the system; the right neighbour's first bits in a
-// column-sharded solve), out = the first 127 solution bits of chunk 0.
-// Map mode (ysel == nullptr, one block per basis vector): block j < 127 runs
-// the chain from y = e_j, block 127 from y = 0, and writes its result to
-// y_io[j]: the range's first 127 bits as an affine function of the 127 bits
-// right of it (the column-sharded solve composes these maps across ranks).
-__global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, const uint4* forms, uint4* ysel,
-                                                          uint4* y_io) {
+// c + 1 (right boundary of chunk c); chunk c's forms map it to chunk c's
+// first bits (an affine GF(2) map: sum of the forms of the set bits of y plus
+// the constant's form).  One warp per chain; the next chunk's forms are
+// loaded while the current one is evaluated.  The chunks are cut in groups
+// of G consecutive chunks (group g = chunks [gG, gG + G)) so the serial
+// chain is two-level (rib_chain_final): the groups' maps in parallel, then a
+// short chain over the group maps, then every group's own chain in parallel.
+//   RUN mode (lin < 0): block g runs group g from y = ybound[g] (or *y_io when
+//     ybound is null); ysel[c] (may be null) gets chunk c's right boundary in
+//     the coef layout (word q bit L = y bit 4L + q; bit 127 = 1 for the
+//     constant), yplain[c] (may be null) the same boundary as plain bits;
+//     with ybound null, *y_io gets the final y (chunk c_lo's first bits).
+//   MAP mode (lin >= 0): block (j, g) runs group g from y = e_j (j < 127) or
+//     y = 0 (j = 127) and writes y_io[128 g + j].  lin = 0: images of the basis
+//     (the affine map as the column-sharded solve composes it); lin = 1: the
+//     constant is left out of the chains of j < 127, giving the linear part
+//     L e_j and, at j = 127, the constant -- the same layout as a chunk's
+//     forms, so the group maps chain with this kernel too.
+__global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, int64_t G, const uint4* forms,
+                                                          uint4* ysel, uint4* yplain, uint4* y_io,
+                                                          const uint4* ybound, int lin) {
   // D-deep cp.async ring: the forms of chunk c - D are in flight while chunk
   // c is evaluated (each lane copies and later reads only its own 64 bytes).
   constexpr int D = 8;
   __shared__ uint4 ring[D][128];
   const int lane = threadIdx.x;
-  const int j = blockIdx.x;
+  const bool map = lin >= 0;
+  const int j = map ? (int)blockIdx.x : 0;
+  const int64_t g = map ? (int64_t)blockIdx.y : (int64_t)blockIdx.x;
+  const int64_t c_lo = g * G;
+  const int64_t c_hi = (c_lo + G < nbchunks) ? c_lo + G : nbchunks;
+  if (c_lo >= c_hi) return;
   uint4 y;
-  if (ysel) {
-    y = *y_io;
+  uint32_t cst = 1u;
+  if (!map) {
+    y = ybound ? ybound[g] : *y_io;
   } else {
     const uint32_t b = (j < 127) ? 1u << (j & 31) : 0u;
     y = make_uint4((j >> 5) == 0 ? b : 0u, (j >> 5) == 1 ? b : 0u, (j >> 5) == 2 ? b : 0u, (j >> 5) == 3 ? b : 0u);
+    if (lin > 0 && j < 127) cst = 0u;
   }
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    const int64_t cc = nbchunks - 1 - k;
-    if (cc >= 0) {
+    const int64_t cc = c_hi - 1 - k;
+    if (cc >= c_lo) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         __pipeline_memcpy_async(&ring[k][4 * lane + q], forms + cc * 128 + 4 * lane + q, sizeof(uint4));
@@ -513,7 +573,7 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
     __pipeline_commit();
   }
   int slot = 0;
-  for (int64_t c = nbchunks - 1; c >= 0; --c) {
+  for (int64_t c = c_hi - 1; c >= c_lo; --c) {
     __pipeline_wait_prior(D - 1);
     uint4 w[4];
 #pragma unroll
@@ -524,7 +584,7 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
     for (int q = 0; q < 4; ++q) {
       const int u = 4 * lane + q;
       uint32_t yw = (u >> 5) == 0 ? y.x : (u >> 5) == 1 ? y.y : (u >> 5) == 2 ? y.z : y.w;
-      sel[q] = (u == 127) ? 1u : ((yw >> (u & 31)) & 1u);
+      sel[q] = (u == 127) ? cst : ((yw >> (u & 31)) & 1u);
       const uint32_t msk = 0u - sel[q];
       acc0 ^= w[q].x & msk;
       acc1 ^= w[q].y & msk;
@@ -532,16 +592,19 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
       acc3 ^= w[q].w & msk;
     }
     // refill the slot just consumed (after its values were used)
-    if (c - D >= 0) {
+    if (c - D >= c_lo) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         __pipeline_memcpy_async(&ring[slot][4 * lane + q], forms + (c - D) * 128 + 4 * lane + q, sizeof(uint4));
     }
     __pipeline_commit();
     slot = (slot + 1 == D) ? 0 : slot + 1;
-    const uint32_t s0 = __ballot_sync(FULL_WARP, sel[0]), s1 = __ballot_sync(FULL_WARP, sel[1]);
-    const uint32_t s2 = __ballot_sync(FULL_WARP, sel[2]), s3 = __ballot_sync(FULL_WARP, sel[3]);
-    if (lane == 0 && ysel) ysel[c] = make_uint4(s0, s1, s2, s3);
+    if (ysel) {
+      const uint32_t s0 = __ballot_sync(FULL_WARP, sel[0]), s1 = __ballot_sync(FULL_WARP, sel[1]);
+      const uint32_t s2 = __ballot_sync(FULL_WARP, sel[2]), s3 = __ballot_sync(FULL_WARP, sel[3]);
+      if (lane == 0) ysel[c] = make_uint4(s0, s1, s2, s3);
+    }
+    if (yplain && lane == 0) yplain[c] = y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       acc0 ^= __shfl_xor_sync(FULL_WARP, acc0, o);
@@ -551,7 +614,12 @@ __global__ void __launch_bounds__(32) ribbon_chain_kernel(int64_t nbchunks, cons
     }
     y = make_uint4(acc0, acc1, acc2, acc3 & 0x7FFFFFFFu);  // 127 bits
   }
-  if (lane == 0) y_io[ysel ? 0 : j] = y;
+  if (lane == 0) {
+    if (map)
+      y_io[g * 128 + j] = y;
+    else if (!ybound)
+      *y_io = y;
+  }
 }
 
 // Final back substitution, a parallel map: sol[col] = parity(coef[col] &
@@ -640,7 +708,8 @@ using namespace shk;
 // Byte offsets of the solver's buffers inside ShkRibbon::buf.
 struct RibLayout {
   size_t off_rows, off_rows2, off_ovf, off_exp, off_hist, off_rowoff, off_cursor, off_sp0, off_sp1, off_occ, off_sb,
-      off_forms, off_coef, off_y, off_yio, off_ymap, off_cnt, off_scan, total;
+      off_forms, off_coef, off_y, off_yio, off_ymap, off_gmap, off_ygrp, off_cnt, off_scan, off_bins, off_bcnt,
+      total;
 };
 
 struct ShkRibbon {
@@ -679,7 +748,21 @@ int rib_cb(int64_t M) {
   return cb;
 }
 
-RibLayout layout(int64_t N, int64_t m) {
+// Two-level chain over nbc back-chunks: groups of G ~ sqrt(nbc) chunks
+// (ribbon_chain_kernel); short systems keep the single chain.
+constexpr int64_t CHAIN_FLAT = 48;
+int64_t chain_group(int64_t nbc) {
+  int64_t G = 1;
+  while (G * G < nbc) ++G;
+  return G;
+}
+int64_t chain_groups(int64_t nbc) {
+  if (nbc <= CHAIN_FLAT) return 1;
+  const int64_t G = chain_group(nbc);
+  return (nbc + G - 1) / G;
+}
+
+RibLayout layout(int64_t N, int64_t m, bool bins = false) {
   RibLayout L;
   int64_t nch = (m + CE - 1) / CE;
   int64_t nbc = (m + rib_cb(m) - 1) / rib_cb(m);
@@ -717,10 +800,24 @@ RibLayout layout(int64_t N, int64_t m) {
   o += 256;
   L.off_ymap = o;
   o += 128 * 16;
+  {
+    const int64_t ng = chain_groups(nbc);
+    L.off_gmap = o;
+    o += al((size_t)ng * 128 * 16);
+    L.off_ygrp = o;
+    o += al((size_t)ng * 16);
+  }
   L.off_cnt = o;
   o += 256;
   L.off_scan = o;
   o += al(shk_scan_scratch(nch));
+  L.off_bins = L.off_bcnt = 0;
+  if (bins) {  // rows emitted by the construction kernel
+    L.off_bins = o;
+    o += al((size_t)nch * RIB_BIN_CAP * sizeof(RRow));
+    L.off_bcnt = o;
+    o += al((size_t)nch * 8);
+  }
   L.total = o;
   return L;
 }
@@ -748,7 +845,7 @@ struct RibBufs {
   int64_t *hist, *rowoff, *cursor, *cnt;  // cnt: [0] ovf count, [1] inconsistent flag (int), [2] export count
   uint64_t *sp0, *sp1;
   uint32_t *occ, *sb;
-  uint4 *forms, *coef, *yb, *yio, *ymap;
+  uint4 *forms, *coef, *yb, *yio, *ymap, *gmap, *ygrp;
   void* scan;
   RibBufs(ShkRibbon* R, const RibLayout& L) {
     char* B = (char*)R->buf;
@@ -769,6 +866,8 @@ struct RibBufs {
     yb = (uint4*)(B + L.off_y);
     yio = (uint4*)(B + L.off_yio);
     ymap = (uint4*)(B + L.off_ymap);
+    gmap = (uint4*)(B + L.off_gmap);
+    ygrp = (uint4*)(B + L.off_ygrp);
     scan = B + L.off_scan;
   }
 };
@@ -833,7 +932,7 @@ int rib_span(int pass) {
 // device; a pass with nothing pending costs one near-empty launch); the host
 // checks for completion once per batch.
 int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c0, int first, int* bad_out,
-               cudaStream_t st) {
+               cudaStream_t st, const unsigned long long* bins_cnt = nullptr) {
   RibBufs b(R, L);
   const int64_t nch = (M + CE - 1) / CE;
   int* bad = (int*)(b.cnt + 1);
@@ -841,7 +940,10 @@ int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c
   constexpr int BATCH = 4;
   for (int pass = 0;;) {
     for (int k = 0; k < BATCH; ++k, ++pass) {
-      SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 8, st));
+      // bin mode: the first pass's overflow list already holds the rows that
+      // did not fit their bins (its count is cnt[0])
+      const unsigned long long* bc = pass == 0 ? bins_cnt : nullptr;
+      if (!bc) SHK_CUDA(cudaMemsetAsync(b.cnt, 0, 8, st));
       static const bool trace = getenv("SHK_RIBBON_TRACE") != nullptr;  // analysis: per-pass counts + times
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (trace) {
@@ -853,22 +955,22 @@ int rib_passes(ShkRibbon* R, const RibLayout& L, RRow* cur, int64_t M, int64_t c
       // later passes: 4 chunks per warp (few chunks hold rows, and a row may
       // walk 4 chunks before it overflows: ~3 passes after the first instead
       // of ~11)
-      const int S = rib_span(pass);
+      const int S = bc ? 1 : rib_span(pass);
       RRow* src = pass == 0 ? cur : b.rows2;
       const int fp = (first && pass == 0) ? 1 : 0;
       const unsigned g = (unsigned)((nch + S - 1) / S);
       if (S == 1 && pass == 0)
         ribbon_elim_kernel<1, true>
-            <<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+            <<<g, 32, 0, st>>>(src, b.rowoff, bc, RIB_BIN_CAP, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
       else if (S == 1)
         ribbon_elim_kernel<1, false>
-            <<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+            <<<g, 32, 0, st>>>(src, b.rowoff, bc, RIB_BIN_CAP, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
       else if (S == 2)
         ribbon_elim_kernel<2, false>
-            <<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+            <<<g, 32, 0, st>>>(src, b.rowoff, bc, RIB_BIN_CAP, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
       else
         ribbon_elim_kernel<4, false>
-            <<<g, 32, 0, st>>>(src, b.rowoff, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
+            <<<g, 32, 0, st>>>(src, b.rowoff, bc, RIB_BIN_CAP, nch, M, b.sp0, b.sp1, b.occ, b.sb, b.ovf, b.cnt, bad, fp);
       SHK_LAUNCHED();
       if (trace) {
         cudaEventRecord(e1, st);
@@ -919,8 +1021,21 @@ int rib_chain_final(ShkRibbon* R, const RibLayout& L, int64_t M, const uint32_t*
   const int64_t nbc = (M + cb - 1) / cb;
   const uint4 y0 = y_in ? make_uint4(y_in[0], y_in[1], y_in[2], y_in[3]) : make_uint4(0, 0, 0, 0);
   SHK_CUDA(cudaMemcpyAsync(b.yio, &y0, 16, cudaMemcpyHostToDevice, st));
-  ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, b.forms, b.yb, b.yio);
-  SHK_LAUNCHED();
+  if (nbc <= CHAIN_FLAT) {
+    ribbon_chain_kernel<<<1, 32, 0, st>>>(nbc, nbc, b.forms, b.yb, nullptr, b.yio, nullptr, -1);
+    SHK_LAUNCHED();
+  } else {
+    // group maps (linear part + constant) in parallel, the chain over the
+    // group maps (each group's right boundary), then every group's chain
+    const int64_t G = chain_group(nbc), ng = chain_groups(nbc);
+    ribbon_chain_kernel<<<dim3(128, (unsigned)ng), 32, 0, st>>>(nbc, G, b.forms, nullptr, nullptr, b.gmap, nullptr,
+                                                                1);
+    SHK_LAUNCHED();
+    ribbon_chain_kernel<<<1, 32, 0, st>>>(ng, ng, b.gmap, nullptr, b.ygrp, b.yio, nullptr, -1);
+    SHK_LAUNCHED();
+    ribbon_chain_kernel<<<(unsigned)ng, 32, 0, st>>>(nbc, G, b.forms, b.yb, nullptr, nullptr, b.ygrp, -1);
+    SHK_LAUNCHED();
+  }
   const int64_t nwords = (M + 63) / 64;
   int64_t fb = (nwords + 7) / 8;
   if (fb > 148 * 8) fb = 148 * 8;
@@ -992,12 +1107,43 @@ int shk_ribbon_solve_keys(ShkRibbon* R, const uint64_t* keys_u64, const uint8_t*
     shk_set_error("ribbon needs m >= 128");
     return 3;
   }
-  RibLayout L = layout(N, m);
+  static const bool csr = [] {
+    const char* e = getenv("SHK_RIBBON_BINS");  // A/B: 0 = histogram + scan + CSR scatter
+    return e && e[0] == '0';
+  }();
+  if (csr) {
+    RibLayout L = layout(N, m);
+    int rc = ensure(R, L.total);
+    if (rc) return rc;
+    rc = gen_keyrows(R, L, keys, rhs, N, m, seed, 0, m, st);
+    if (rc) return rc;
+    return solve_sorted(R, L, N, m, words_out, consistent, st);
+  }
+  RibLayout L = layout(N, m, true);
   int rc = ensure(R, L.total);
   if (rc) return rc;
-  rc = gen_keyrows(R, L, keys, rhs, N, m, seed, 0, m, st);
+  rc = rib_clear(R, L, m, st);  // also zeroes the overflow count cnt[0]
   if (rc) return rc;
-  return solve_sorted(R, L, N, m, words_out, consistent, st);
+  RibBufs b(R, L);
+  char* B = (char*)R->buf;
+  const int64_t nch = (m + CE - 1) / CE;
+  unsigned long long* bcnt = (unsigned long long*)(B + L.off_bcnt);
+  RRow* bins = (RRow*)(B + L.off_bins);
+  SHK_CUDA(cudaMemsetAsync(bcnt, 0, (size_t)nch * 8, st));
+  if (N > 0) {
+    ribbon_keyrows_bins_kernel<<<grid_for(N), 256, 0, st>>>(keys, rhs, N, m, seed, bcnt, RIB_BIN_CAP, bins, b.ovf,
+                                                            (unsigned long long*)b.cnt);
+    SHK_LAUNCHED();
+  }
+  int bad = 0;
+  rc = rib_passes(R, L, bins, m, 0, 1, &bad, st, bcnt);
+  if (rc) return rc;
+  if (bad) {
+    *consistent = 0;
+    return 0;
+  }
+  *consistent = 1;
+  return rib_backsub(R, L, m, nullptr, nullptr, words_out, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1085,7 +1231,15 @@ int shk_ribbon_dist_map(ShkRibbon* R, uint32_t* map_out, cudaStream_t st) {
   int rc = rib_forms(R, R->dL, R->dM, st);
   if (rc) return rc;
   const int64_t nbc = (R->dM + rib_cb(R->dM) - 1) / rib_cb(R->dM);
-  ribbon_chain_kernel<<<128, 32, 0, st>>>(nbc, b.forms, nullptr, b.ymap);
+  if (nbc <= CHAIN_FLAT) {
+    ribbon_chain_kernel<<<dim3(128, 1), 32, 0, st>>>(nbc, nbc, b.forms, nullptr, nullptr, b.ymap, nullptr, 0);
+  } else {  // the range's map composed from its group maps
+    const int64_t G = chain_group(nbc), ng = chain_groups(nbc);
+    ribbon_chain_kernel<<<dim3(128, (unsigned)ng), 32, 0, st>>>(nbc, G, b.forms, nullptr, nullptr, b.gmap, nullptr,
+                                                                1);
+    SHK_LAUNCHED();
+    ribbon_chain_kernel<<<dim3(128, 1), 32, 0, st>>>(ng, ng, b.gmap, nullptr, nullptr, b.ymap, nullptr, 0);
+  }
   SHK_LAUNCHED();
   SHK_CUDA(cudaMemcpyAsync(map_out, b.ymap, 128 * 16, cudaMemcpyDeviceToHost, st));
   SHK_CUDA(cudaStreamSynchronize(st));

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 for v in "$@"; do
   SHK_LIB_PATH=$PWD/paper_2308_09561_b200/_lib/variants/libshockhash_b200_$v.so \
-    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --queries 0 --leaf-configs "" --no-check \
+    python bench.py --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline --queries 0 --leaf-configs "" --no-check \
     > gpurun_out/ab_$v.json 2> gpurun_out/ab_$v.err
   python - "$v" <<'PY'
 import json, sys
