@@ -14,9 +14,28 @@
 #include <unordered_map>
 #include <vector>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "../../include/shockhash_b200.h"
 #include "shk_common.cuh"
 #include "shk_kernels.h"
+
+// (analysis) SHK_HOST_TRACE=1: host timestamps of the build's stages, us
+// since the build object was created, on stderr
+static double host_now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static bool host_trace_on() {
+  static const bool on = getenv("SHK_HOST_TRACE") != nullptr;
+  return on;
+}
+static double g_host_t0 = 0;
+#define HOST_TRACE(tag) \
+  do { \
+    if (host_trace_on()) fprintf(stderr, "host %-24s %9.1f us\n", tag, host_now_us() - g_host_t0); \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // errors / launch counting
@@ -60,7 +79,11 @@ struct shk_ctx {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int64_t opt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // shk_ctx_set_option
   int* shared_leaf_counter = nullptr;  // shk_ctx_set_leaf_counter (cross-GPU leaf queue)
+  struct PlanCache* plans = nullptr;   // the last build's plan tables, host and device (plan_cache)
+  void* h_stage = nullptr;             // pinned staging for the per-build tables (one H2D copy)
+  size_t h_stage_cap = 0;
 };
+static void plan_cache_free(shk_ctx* c);
 
 static size_t round_up(size_t b) {
   if (b < 256) return 256;
@@ -222,6 +245,8 @@ int shk_ctx_destroy(shk_ctx* c) {
   for (auto& kv : c->free_blocks) cudaFree(kv.second);
   for (auto& kv : c->live) cudaFree(kv.first);
   shk_ribbon_destroy(c->rib);
+  plan_cache_free(c);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   cudaFree(c->d_counter);
   if (c->h_flags) cudaFreeHost(c->h_flags);
   cudaEventDestroy(c->t0);
@@ -997,6 +1022,113 @@ static int load_plans(const shk_plans* P, PlanSet& S) {
   return 0;
 }
 
+// The plan tables of repeated builds over one key set (or any sets with the
+// same bucket sizes) are identical: the context keeps the last PlanSet and its
+// device copy, reused when the incoming arrays are equal (a content compare,
+// ~1 MB at C4, instead of parsing 18k nodes into freshly faulted pages and
+// re-uploading them: ~0.25 ms of host time before the first search).
+struct PlanCache {
+  std::vector<int64_t> src;  // the input arrays the tables were built from
+  PlanSet S;
+  ShkPlanNode* d_nodes = nullptr;
+  int64_t* d_off = nullptr;
+  size_t d_nodes_n = 0, d_off_n = 0;
+  bool valid = false;
+};
+
+static void plan_cache_free(shk_ctx* c) {
+  if (!c->plans) return;
+  cudaFree(c->plans->d_nodes);
+  cudaFree(c->plans->d_off);
+  delete c->plans;
+  c->plans = nullptr;
+}
+
+// Walk the input arrays in a fixed order: fn(ptr, count) per array.
+template <class F>
+static void plans_arrays(const shk_plans* P, F&& fn) {
+  const int64_t np = P->nplans;
+  const int64_t total = np > 0 ? P->plan_off[np] : 0;
+  int64_t flat = 0;  // sizes_flat entries read by load_plans
+  for (int64_t p = 0; p < np; ++p)
+    for (int64_t j = P->plan_off[p]; j < P->plan_off[p + 1]; ++j)
+      if (P->kind[j] == 0) {
+        const int64_t need = P->sizes_base[p] + P->sizes_off[j] + P->fanout[j];
+        if (need > flat) flat = need;
+      }
+  fn(&np, 1);
+  fn(P->plan_m, np);
+  fn(P->plan_off, np + 1);
+  fn(P->sizes_base, np);
+  fn(P->kind, total);
+  fn(P->g, total);
+  fn(P->fanout, total);
+  fn(P->sizes_off, total);
+  fn(P->subtree, total);
+  fn(P->m_node, total);
+  fn(&flat, 1);
+  fn(P->sizes_flat, flat);
+}
+
+static int plan_cache_get(shk_ctx* c, const shk_plans* P, const PlanSet** out) {
+  if (!P || P->nplans < 0) {
+    shk_set_error("missing plan tables");
+    return SHK_INVALID;
+  }
+  if (!c->plans) c->plans = new PlanCache();
+  PlanCache& pc = *c->plans;
+  if (pc.valid) {
+    bool same = true;
+    size_t o = 0;
+    plans_arrays(P, [&](const int64_t* a, int64_t n) {
+      if (!same) return;
+      if (o + (size_t)n > pc.src.size() || (n && memcmp(pc.src.data() + o, a, (size_t)n * 8) != 0)) same = false;
+      o += (size_t)n;
+    });
+    if (same && o == pc.src.size()) {
+      *out = &pc.S;
+      return 0;
+    }
+  }
+  pc.valid = false;
+  pc.S = PlanSet();
+  RC(load_plans(P, pc.S));
+  pc.src.clear();
+  plans_arrays(P, [&](const int64_t* a, int64_t n) { pc.src.insert(pc.src.end(), a, a + n); });
+  const size_t nn = pc.S.nodes.size() + 1, no = pc.S.plan_off.size() + 1;
+  if (pc.d_nodes_n < nn) {
+    cudaFree(pc.d_nodes);
+    pc.d_nodes = nullptr;
+    SHK_CUDA(cudaMalloc(&pc.d_nodes, nn * sizeof(ShkPlanNode)));
+    pc.d_nodes_n = nn;
+  }
+  if (pc.d_off_n < no) {
+    cudaFree(pc.d_off);
+    pc.d_off = nullptr;
+    SHK_CUDA(cudaMalloc(&pc.d_off, no * 8));
+    pc.d_off_n = no;
+  }
+  SHK_CUDA(cudaMemcpy(pc.d_nodes, pc.S.nodes.data(), pc.S.nodes.size() * sizeof(ShkPlanNode), cudaMemcpyHostToDevice));
+  SHK_CUDA(cudaMemcpy(pc.d_off, pc.S.plan_off.data(), pc.S.plan_off.size() * 8, cudaMemcpyHostToDevice));
+  pc.valid = true;
+  *out = &pc.S;
+  return 0;
+}
+
+// Pinned host staging of `bytes` (grown on demand; the previous contents
+// must have been consumed: every build syncs before it returns).
+static int host_stage(shk_ctx* c, size_t bytes, void** out) {
+  if (c->h_stage_cap < bytes) {
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    c->h_stage = nullptr;
+    c->h_stage_cap = 0;
+    SHK_CUDA(cudaMallocHost(&c->h_stage, bytes));
+    c->h_stage_cap = bytes;
+  }
+  *out = c->h_stage;
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // Build object.
 
@@ -1103,6 +1235,8 @@ int shk_build_create(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
     shk_set_error("build needs N >= 1 and nbuckets >= 1");
     return SHK_INVALID;
   }
+  g_host_t0 = host_now_us();
+  HOST_TRACE("create");
   shk_build* b = new shk_build(c);
   b->N = N;
   b->nb = nbuckets;
@@ -1126,6 +1260,7 @@ int shk_build_create(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
                             b->prefix.as<uint64_t>(), ddup, scratch.p, ss, &b->max_bucket, c->stream,
                             async ? b->h_prefix.data() : nullptr)))
       break;
+    HOST_TRACE("bucketize enqueued");
     if (async) {
       // the prefix is on the host already; the scatter and the sort are
       // still running: the duplicate flag follows them into pinned memory
@@ -1152,6 +1287,7 @@ int shk_build_create(shk_ctx* c, const uint64_t* hi, const uint64_t* lo, int64_t
     return rc;
   }
   *out = b;
+  HOST_TRACE("create return");
   return 0;
 }
 
@@ -1183,8 +1319,11 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     shk_set_error("invalid bucket range or mode");
     return SHK_INVALID;
   }
-  PlanSet S;
-  RC(load_plans(plans, S));
+  HOST_TRACE("run");
+  const PlanSet* SP = nullptr;
+  RC(plan_cache_get(c, plans, &SP));
+  const PlanSet& S = *SP;
+  HOST_TRACE("plans loaded");
   const int64_t nbr = b1 - b0;
   // ---- per-bucket plan ids and global node numbering
   std::vector<int64_t> node_base((size_t)nbr + 1);
@@ -1291,6 +1430,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     leaf_off.push_back((int64_t)b->h_prefix[b1]);  // leaves are contiguous: CSR end = range end
   }
   int64_t L = use_tree ? 0 : (int64_t)leaf_slot.size();
+  HOST_TRACE("node numbering");
   // ---- device tables
   DBuf dseeds(c), dg(c), dkind(c), dtasks(c), dloff(c), dlslot(c), dlen(c), dpos(c), dnb(c), dbo(c), dacc(c),
       dscan(c);
@@ -1324,40 +1464,47 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   b->mark(2);
   b->level_reset();
   // an asynchronous bucketize is checked here, after the host-side
-  // preparation (which overlapped the sort) and before the first search
-  if (b->take_dup()) {
+  // preparation (which overlapped the sort) and before the first search --
+  // by the construction kernel itself on the persistent schedule (it reads
+  // the sort's device flag and does nothing when it is set; the host checks
+  // once the kernel is done), so the launch is enqueued while the sort runs
+  HOST_TRACE("tables");
+  if (!use_tree && b->take_dup()) {
     shk_set_error("equal 128-bit codes in the input");
     return SHK_DUPLICATE;
   }
+  HOST_TRACE("dup flag");
   // the seed searches take pre-mixed key high words (shk_hash.cuh premix_hi);
   // undone right after the leaves
   RC(shk_launch_premix(b->keys.as<uint64_t>(), b->N, 0, c->stream));
-  DBuf dnodes(c), dqueue(c), dqctl(c), dpn(c), dpoff(c), dbp(c), dnbase(c), dks(c), droot(c);
+  DBuf dnodes(c), dqueue(c), dtab(c);
   if (use_tree && nn > 0) {
-    // ---- node table expanded on the device from the (small) plan tables
+    // ---- node table expanded on the device from the (small) plan tables:
+    // the plan nodes are the cached device copy; the per-bucket tables and
+    // the queue counters go up in ONE copy from pinned staging
     RC(dnodes.alloc((size_t)nn * sizeof(ShkTreeNode)));
     RC(dqueue.alloc((size_t)nn * 8));
-    RC(dqctl.alloc(256));
-    RC(dpn.alloc(S.nodes.size() * sizeof(PlanNode) + 16));
-    RC(dpoff.alloc(S.plan_off.size() * 8 + 8));
-    RC(dbp.alloc((size_t)nbr * 4 + 4));
-    RC(dnbase.alloc((size_t)nbr * 8 + 8));
-    RC(dks.alloc((size_t)nbr * 8 + 8));
-    RC(droot.alloc((size_t)nbr * 8 + 8));
-    RC(h2d(c, dpn.p, S.nodes.data(), S.nodes.size() * sizeof(PlanNode)));
-    RC(h2d(c, dpoff.p, S.plan_off.data(), S.plan_off.size() * 8));
-    RC(h2d(c, dbp.p, bplan.data(), (size_t)nbr * 4));
-    RC(h2d(c, dnbase.p, node_base.data(), (size_t)nbr * 8));
-    RC(h2d(c, dks.p, kstart_v.data(), (size_t)nbr * 8));
-    RC(h2d(c, droot.p, root_pos.data(), (size_t)nbr * 8));
-    SHK_CUDA(cudaMemsetAsync(dqueue.p, 0xFF, (size_t)nn * 8, c->stream));
+    const size_t o_qc = 0, o_nb = 32, o_ks = o_nb + (size_t)(nbr + 1) * 8, o_rp = o_ks + (size_t)(nbr + 1) * 8,
+                 o_bp = o_rp + (size_t)(nbr + 1) * 8, tab_bytes = o_bp + (size_t)(nbr + 1) * 4;
+    RC(dtab.alloc(tab_bytes));
+    void* hs = nullptr;
+    RC(host_stage(c, tab_bytes, &hs));
+    char* H = (char*)hs;
     // split head, leaf head, split tail, leaf tail
-    unsigned long long qc[4] = {0ull, (unsigned long long)nsplit, (unsigned long long)nroots_split,
-                                (unsigned long long)(nsplit + nroots_leaf)};
-    RC(h2d(c, dqctl.p, qc, 32));
-    RC(shk_launch_expand_nodes(dpn.as<PlanNode>(), dpoff.as<int64_t>(), dbp.as<int32_t>(), dnbase.as<int64_t>(),
-                               dks.as<int64_t>(), droot.as<int64_t>(), nbr, dnodes.as<ShkTreeNode>(), dg.as<int32_t>(),
-                               dkind.as<uint8_t>(), dqueue.as<int64_t>(), c->stream));
+    const unsigned long long qc[4] = {0ull, (unsigned long long)nsplit, (unsigned long long)nroots_split,
+                                      (unsigned long long)(nsplit + nroots_leaf)};
+    memcpy(H + o_qc, qc, 32);
+    memcpy(H + o_nb, node_base.data(), (size_t)(nbr + 1) * 8);
+    memcpy(H + o_ks, kstart_v.data(), (size_t)nbr * 8);
+    memcpy(H + o_rp, root_pos.data(), (size_t)nbr * 8);
+    memcpy(H + o_bp, bplan.data(), (size_t)nbr * 4);
+    RC(h2d(c, dtab.p, hs, tab_bytes));
+    char* D = dtab.as<char>();
+    SHK_CUDA(cudaMemsetAsync(dqueue.p, 0xFF, (size_t)nn * 8, c->stream));
+    RC(shk_launch_expand_nodes(c->plans->d_nodes, c->plans->d_off, (const int32_t*)(D + o_bp),
+                               (const int64_t*)(D + o_nb), (const int64_t*)(D + o_ks), (const int64_t*)(D + o_rp), nbr,
+                               dnodes.as<ShkTreeNode>(), dg.as<int32_t>(), dkind.as<uint8_t>(), dqueue.as<int64_t>(),
+                               c->stream));
     // ---- one persistent launch for every split node and leaf (shk_tree.cu)
     ShkTreeLaunch p{};
     p.keys = b->keys.as<uint64_t>();
@@ -1365,8 +1512,9 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     p.nodes = dnodes.as<ShkTreeNode>();
     p.nnodes = nn;
     p.queue = dqueue.as<int64_t>();
-    p.head = dqctl.as<unsigned long long>();
-    p.tail = dqctl.as<unsigned long long>() + 2;
+    p.head = (unsigned long long*)(D + o_qc);
+    p.tail = (unsigned long long*)(D + o_qc) + 2;
+    p.dup_flag = b->dup_pending ? c->d_counter + 3 : nullptr;
     p.nsplit = nsplit;
     {
       // A/B of the slot-aware schedule: SHK_TREE_SLOT_AWARE=0 lets every warp
@@ -1396,6 +1544,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     p.exhausted = exh;
     p.num_sms = c->num_sms;
     RC(shk_launch_tree(p, c->stream));
+    HOST_TRACE("tree launched");
     b->mark(3);
   }
   // ---- splits, level by level (every node of one depth in one launch)
@@ -1458,14 +1607,12 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   }
   RC(shk_launch_premix(b->keys.as<uint64_t>(), b->N, 1, c->stream));
   b->mark(4);
+  // ---- Rice stream: lengths -> scan -> scatter.  The lengths are computed
+  // before the host has seen the exhaustion flag (one round trip instead of
+  // two): with an exhausted search they are garbage and the flag, read with
+  // the total, stops the build before anything is sized from them.
   int hex = 0;
   RC(d2h(c, &hex, exh, 4));
-  RC(csync(c));
-  if (hex) {
-    shk_set_error("seed search exhausted (max_seed %llu)", (unsigned long long)max_seed);
-    return SHK_EXHAUSTED;
-  }
-  // ---- Rice stream: lengths -> scan -> scatter
   RC(dlen.alloc((size_t)(nn + 1) * 8));
   RC(dpos.alloc((size_t)(nn + 2) * 8));
   RC(shk_rice_lengths(dseeds.as<int64_t>(), dg.as<int32_t>(), nn, dlen.as<int64_t>(), c->stream));
@@ -1478,6 +1625,15 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   int64_t total_bits = 0;
   RC(d2h(c, &total_bits, dpos.as<int64_t>() + nn, 8));
   RC(csync(c));
+  HOST_TRACE("tree done + rice length");
+  if (b->take_dup()) {  // the persistent schedule checks the flag on the device (above)
+    shk_set_error("equal 128-bit codes in the input");
+    return SHK_DUPLICATE;
+  }
+  if (hex) {
+    shk_set_error("seed search exhausted (max_seed %llu)", (unsigned long long)max_seed);
+    return SHK_EXHAUSTED;
+  }
   b->bit_len = total_bits;
   b->nwords = (total_bits + 63) / 64;
   RC(b->words.alloc((size_t)(b->nwords + 1) * 8));
@@ -1485,11 +1641,16 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   RC(shk_rice_scatter(dseeds.as<int64_t>(), dg.as<int32_t>(), dpos.as<int64_t>(), nn, b->words.as<uint64_t>(),
                       c->stream));
   // per-bucket bit offsets: pos[node_base[i]]
-  RC(dnb.alloc((size_t)(nbr + 1) * 8));
+  // (the persistent schedule's device copy of node_base is still in dtab)
+  const int64_t* d_nb = dtab.p ? (const int64_t*)(dtab.as<char>() + 32) : nullptr;
+  if (!d_nb) {
+    RC(dnb.alloc((size_t)(nbr + 1) * 8));
+    RC(h2d(c, dnb.p, node_base.data(), (size_t)(nbr + 1) * 8));
+    d_nb = dnb.as<int64_t>();
+  }
   RC(dbo.alloc((size_t)(nbr + 1) * 8));
-  RC(h2d(c, dnb.p, node_base.data(), (size_t)(nbr + 1) * 8));
-  gather_bitoff_kernel<<<(unsigned)((nbr + 256) / 256), 256, 0, c->stream>>>(dpos.as<int64_t>(), dnb.as<int64_t>(),
-                                                                              nbr, dbo.as<uint64_t>());
+  gather_bitoff_kernel<<<(unsigned)((nbr + 256) / 256), 256, 0, c->stream>>>(dpos.as<int64_t>(), d_nb, nbr,
+                                                                              dbo.as<uint64_t>());
   SHK_LAUNCHED();
   b->bit_off.resize((size_t)nbr + 1);
   RC(d2h(c, b->bit_off.data(), dbo.p, (size_t)(nbr + 1) * 8));
@@ -1513,6 +1674,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   b->b0 = b0;
   b->b1 = b1;
   b->ran = true;
+  HOST_TRACE("run return");
   return 0;
 }
 
@@ -1669,6 +1831,7 @@ int shk_build_choice(shk_build* b, uint8_t* choice) {
 int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int64_t m, int max_tries,
                      uint64_t* seed_out, uint64_t* words_out) {
   shk_ctx* c = b->c;
+  HOST_TRACE("ribbon");
   if (m < 128) {
     shk_set_error("ribbon needs m >= 128");
     return SHK_INVALID;
@@ -1694,7 +1857,9 @@ int shk_build_ribbon(shk_build* b, const uint8_t* choice, int choice_flags, int6
     rkeys = b->sorted.as<uint64_t>();
   }
   b->mark(6);
+  HOST_TRACE("ribbon start");
   RC(ribbon_seed_loop(c, rkeys, drhs, b->N, m, max_tries, seed_out, tw.as<uint64_t>()));
+  HOST_TRACE("ribbon solved");
   b->mark(7);
   RC(d2h(c, words_out, tw.p, (size_t)nw * 8));
   RC(csync(c));

@@ -116,6 +116,7 @@ struct ShkTreeLaunch {
   unsigned long long* stats_acc;
   int* exhausted;
   int num_sms;
+  const int* dup_flag;  // optional: the bucket sort's duplicate flag (nonzero: the kernel does nothing)
 };
 int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st);
 

@@ -56,6 +56,7 @@ struct TreeArgs {
   uint64_t max_seed;
   int64_t* seeds;
   int* exhausted;
+  const int* dup_flag;         // nonzero: equal codes in the input, every warp exits (the host raises)
   LeafArgs leaf;
 };
 
@@ -104,6 +105,9 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
   // every leaf slot -- is eventually published whatever slots the warps get.
   const bool anchor = blockIdx.x == 0 && w == 0;
   if ((int)wid >= t.idle_wid && !anchor) return;
+  // the bucket sort's duplicate flag is checked here rather than by the host
+  // before the launch, so the host enqueues the launch while the sort runs
+  if (t.dup_flag && *(volatile const int*)t.dup_flag) return;
   const bool slow = (int)wid >= t.slow_wid && !anchor;
   bool splits_done = slow;
   for (;;) {
@@ -244,6 +248,7 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   t.max_seed = p.max_seed;
   t.seeds = p.seeds;
   t.exhausted = p.exhausted;
+  t.dup_flag = p.dup_flag;
   LeafArgs& a = t.leaf;
   a = LeafArgs{};
   a.hi = p.keys;
