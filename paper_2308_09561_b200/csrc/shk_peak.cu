@@ -11,6 +11,11 @@
 //   kind 2: LOP3 + IMAD, 1:1  (both pipes: the ideal split of the searches)
 //   kind 3: SHF + LOP3 + IMAD, 2:1:1 (the remix's own mix: xor-shifts on
 //           SHF/LOP3, multiplies on IMAD)
+// Pipe costs of the multiply forms the hash uses (analysis, tools/int_peak.py;
+// two ops per chain step each):
+//   kind 4: IMAD.WIDE only   kind 5: IMAD.HI only
+//   kind 6: IMAD.WIDE + LOP3 1:1   kind 7: IMAD.HI + LOP3 1:1
+//   kind 8: IMAD by a power of two (a shift on the FMA pipe) + LOP3 1:1
 // ops = threads x iters x 8 chains x ops per chain step; the grid fills every
 // SM with 64 warps.
 #include "shk_common.cuh"
@@ -36,6 +41,27 @@ __global__ void __launch_bounds__(256) int_peak_kernel(uint32_t* sink, int iters
       } else if (KIND == 2) {
         asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[j]) : "r"(y), "r"(z));
         asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[j]) : "r"(z), "r"(y));
+      } else if (KIND == 4 || KIND == 6) {
+        uint32_t lo, hi;
+        asm volatile("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %2, %3;\n\tmov.b64 {%0, %1}, w;\n\t}"
+                     : "=r"(lo), "=r"(hi)
+                     : "r"(x[j]), "r"(y));
+        if (KIND == 4) {
+          asm volatile("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %2, %3;\n\tmov.b64 {%0, %1}, w;\n\t}"
+                       : "=r"(x[j]), "=r"(hi)
+                       : "r"(lo), "r"(z));
+        } else {
+          asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(x[j]) : "r"(lo), "r"(hi), "r"(z));
+        }
+      } else if (KIND == 5 || KIND == 7) {
+        asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x[j]) : "r"(y));
+        if (KIND == 5)
+          asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x[j]) : "r"(z));
+        else
+          asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[j]) : "r"(z), "r"(y));
+      } else if (KIND == 8) {
+        asm volatile("mad.lo.u32 %0, %0, 8192, %1;" : "+r"(x[j]) : "r"(y));
+        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[j]) : "r"(z), "r"(y));
       } else {
         uint32_t t;
         asm volatile("shf.r.wrap.b32 %0, %1, %1, 13;" : "=r"(t) : "r"(x[j]));
@@ -65,7 +91,12 @@ int shk_launch_int_peak(int kind, int iters, int num_sms, uint32_t* sink, int64_
     case 1: int_peak_kernel<1><<<blocks, 256, 0, st>>>(sink, iters, 0x1234567u); break;
     case 2: int_peak_kernel<2><<<blocks, 256, 0, st>>>(sink, iters, 0x1234567u); break;
     case 3: int_peak_kernel<3><<<blocks, 256, 0, st>>>(sink, iters, 0x1234567u); break;
-    default: shk_set_error("int peak kind must be 0..3"); return 3;
+    case 4: int_peak_kernel<4><<<blocks, 256, 0, st>>>(sink, iters, 0x1234567u); break;
+    case 5: int_peak_kernel<5><<<blocks, 256, 0, st>>>(sink, iters, 0x1234567u); break;
+    case 6: int_peak_kernel<6><<<blocks, 256, 0, st>>>(sink, iters, 0x1234567u); break;
+    case 7: int_peak_kernel<7><<<blocks, 256, 0, st>>>(sink, iters, 0x1234567u); break;
+    case 8: int_peak_kernel<8><<<blocks, 256, 0, st>>>(sink, iters, 0x1234567u); break;
+    default: shk_set_error("int peak kind must be 0..8"); return 3;
   }
   SHK_LAUNCHED();
   return 0;

@@ -114,6 +114,9 @@ def set_option(opt: int, value: int):
 
 
 INT_PEAK_KINDS = {0: "LOP3", 1: "IMAD", 2: "LOP3+IMAD 1:1", 3: "SHF+LOP3+IMAD 2:1:1"}
+# analysis only (tools/int_peak.py): pipe cost of the hash's multiply forms
+INT_PEAK_KINDS_EXTRA = {4: "IMAD.WIDE", 5: "IMAD.HI", 6: "IMAD.WIDE+LOP3 1:1", 7: "IMAD.HI+LOP3 1:1",
+                        8: "IMAD(2^k)+LOP3 1:1"}
 
 
 def int_peak(kind: int, iters: int = 4096):

@@ -10,6 +10,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2308_09561_b200 import device as dev
 
-for kind, name in dev.INT_PEAK_KINDS.items():
+for kind, name in {**dev.INT_PEAK_KINDS, **dev.INT_PEAK_KINDS_EXTRA}.items():
     ms, ops = dev.int_peak(kind, 16384)
     print(f"{name}: {ops / (ms * 1e-3) / 1e12:.2f} Tops/s ({ms:.3f} ms)")
