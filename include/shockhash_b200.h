@@ -120,6 +120,11 @@ int shk_dev_free(shk_ctx* ctx, void* p);
 int shk_memcpy(shk_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /*0 H2D 1 D2H 2 D2D*/);
 /* Stream-ordered byte fill of device memory (value & 0xFF). */
 int shk_memset(shk_ctx* ctx, void* dst, int value, size_t bytes);
+/* Exclusive prefix sum of n int64 device values into out[0..n] (out[n] = the
+ * total), stream-ordered, synchronous on return: the scan every build stage
+ * uses (recsplit.py:485 key_prefix = cumsum(counts), the Rice code offsets,
+ * the ribbon's chunk offsets). */
+int shk_exclusive_scan(shk_ctx* ctx, const int64_t* in, int64_t* out, int64_t n);
 /* Events on the context stream: elapsed milliseconds between two records. */
 int shk_timer_start(shk_ctx* ctx);
 int shk_timer_stop(shk_ctx* ctx, float* ms);

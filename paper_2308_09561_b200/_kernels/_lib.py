@@ -77,6 +77,7 @@ _SIGS = {
     "shk_host_free": (_I, [_P, _P]),
     "shk_memcpy": (_I, [_P, _P, _P, ctypes.c_size_t, _I]),
     "shk_memset": (_I, [_P, _P, _I, ctypes.c_size_t]),
+    "shk_exclusive_scan": (_I, [_P, _P, _P, _I64]),
     "shk_timer_start": (_I, [_P]),
     "shk_timer_stop": (_I, [_P, _P]),
     "shk_launch_count": (_I64, [_P]),

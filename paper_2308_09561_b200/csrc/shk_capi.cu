@@ -298,6 +298,19 @@ int shk_memset(shk_ctx* c, void* dst, int value, size_t bytes) {
   SHK_CUDA(cudaMemsetAsync(dst, value, bytes, c->stream));
   return 0;
 }
+int shk_exclusive_scan(shk_ctx* c, const int64_t* in, int64_t* out, int64_t n) {
+  if (n < 0) {
+    shk_set_error("scan length must be >= 0");
+    return SHK_INVALID;
+  }
+  const size_t ss = shk_scan_scratch(n);
+  void* scratch = nullptr;
+  RC(pool_alloc(c, ss, &scratch));
+  const int rc = shk_exclusive_scan_i64(in, out, n, scratch, ss, c->stream);
+  const int rs = csync(c);
+  pool_free(c, scratch);
+  return rc ? rc : rs;
+}
 int shk_timer_start(shk_ctx* c) {
   SHK_CUDA(cudaEventRecord(c->t0, c->stream));
   return 0;

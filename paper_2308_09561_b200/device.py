@@ -84,6 +84,11 @@ def memset_device(ptr: int, value: int, nbytes: int):
     check(_lib.load_library().shk_memset(ctx(), ptr, int(value), int(nbytes)), "memset")
 
 
+def exclusive_scan_device(d_in: "DeviceBuffer", d_out: "DeviceBuffer", n: int):
+    """out[0..n] = exclusive prefix sum of n int64 values (out[n] = total), on the device."""
+    check(_lib.load_library().shk_exclusive_scan(ctx(), d_in.ptr, d_out.ptr, int(n)), "scan")
+
+
 def sync():
     check(_lib.load_library().shk_ctx_sync(ctx()), "sync")
 

@@ -161,3 +161,20 @@ def test_steal_kernel_exhaustion_and_single_leaf():
     assert int(s1[0]) == ref[0]
     e = oracle.edges_plain(hi[:n], lo[:n], ref[0], n)
     assert int(f1[0]) == oracle.orient(e, n)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 255, 2047, 2048, 2049, 100_000, 1_482_000, 4096 * 2048 + 3])
+def test_exclusive_scan_lengths(n):
+    """The device scan every build stage uses (shk_exclusive_scan): one tile,
+    tile edges, the per-tile carry loop and (past 4096 tiles) the recursive
+    scan of the tile totals, against numpy's cumsum (recsplit.py:485)."""
+    from paper_2308_09561_b200 import device as dev
+
+    rng = np.random.default_rng(n + 1)
+    a = rng.integers(0, 1 << 40, size=max(n, 1), dtype=np.int64)[:n]
+    d_in = dev.DeviceBuffer.from_host(a if n else np.zeros(1, dtype=np.int64))
+    d_out = dev.DeviceBuffer(8 * (n + 1))
+    dev.exclusive_scan_device(d_in, d_out, n)
+    got = d_out.download(np.int64, n + 1)
+    want = np.concatenate([[0], np.cumsum(a)]).astype(np.int64)
+    assert np.array_equal(got, want)
