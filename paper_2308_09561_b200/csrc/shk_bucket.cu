@@ -12,6 +12,7 @@
 // resolved on lo, which is astronomically rare but exact), gathers, writes
 // the interleaved sorted keys and flags adjacent duplicates.
 #include <cstdlib>
+#include <cstring>
 
 #include <cooperative_groups.h>
 
@@ -691,27 +692,44 @@ static int bucketize_smem(const uint64_t* hi, const uint64_t* lo, int64_t N, int
   bk_prefix_kernel<<<(unsigned)((nb + 256) / 256 < 148 ? (nb + 256) / 256 : 148), 256, 0, st>>>(Moff, BK_G, nb,
                                                                                                  prefix, maxv);
   SHK_LAUNCHED();
-  int64_t maxb = 0;
-  if (h_prefix) {
-    SHK_CUDA(cudaMemcpyAsync(h_prefix, prefix, (size_t)(nb + 1) * 8, cudaMemcpyDeviceToHost, st));
+  // The key prefix and the largest bucket come back through pinned memory
+  // behind an event; the super-bucket scatter is queued before the host
+  // waits (it does not depend on the largest bucket, which only picks the
+  // sort kernel), so the device goes from the scan straight into the scatter.
+  static thread_local int64_t* hp = nullptr;
+  static thread_local size_t hp_cap = 0;
+  static thread_local cudaEvent_t ev = nullptr;
+  if (hp_cap < (size_t)(nb + 2)) {
+    if (hp) cudaFreeHost(hp);
+    hp = nullptr;
+    hp_cap = 0;
+    SHK_CUDA(cudaMallocHost(&hp, (size_t)(nb + 2) * 8));
+    hp_cap = (size_t)(nb + 2);
   }
-  SHK_CUDA(cudaMemcpyAsync(&maxb, maxv, 8, cudaMemcpyDeviceToHost, st));
-  // the largest bucket picks the sort kernel; the caller's host work overlaps
-  // the scatter and the sort (only the histogram and the scan are waited for)
-  SHK_CUDA(cudaStreamSynchronize(st));
-  if (max_bucket_out) *max_bucket_out = maxb;
+  if (!ev) SHK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  if (h_prefix) SHK_CUDA(cudaMemcpyAsync(hp, prefix, (size_t)(nb + 1) * 8, cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaMemcpyAsync(hp + nb + 1, maxv, 8, cudaMemcpyDeviceToHost, st));
+  SHK_CUDA(cudaEventRecord(ev, st));
   static const bool use_cluster = [] {
     const char* e = getenv("SHK_BUCKET_CLUSTER");
     return !(e && e[0] == '0');
   }();
-  const int64_t cap = maxb;
-  const size_t csm = (size_t)cap * 16 + (size_t)((cap + 7) & ~7) * 2 + BK_CBINS * 4;
-  if (use_cluster && csm <= 200 * 1024) {
+  if (use_cluster) {
     // super-bucket scatter (coalesced runs), then one 16-CTA cluster per super-bucket
     const size_t l1sm = (size_t)BK_TILE * 18 + (size_t)(3 * nsb + 1) * 4;
     SHK_CUDA(cudaFuncSetAttribute(bk_l1_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l1sm));
     bk_l1_scatter_kernel<<<BK_G, 512, l1sm, st>>>(hi, lo, N, (uint32_t)nb, Msboff, unsorted);
     SHK_LAUNCHED();
+  }
+  // the largest bucket picks the sort kernel; the caller's host work overlaps
+  // the scatter and the sort (only the histogram and the scan are waited for)
+  SHK_CUDA(cudaEventSynchronize(ev));
+  const int64_t maxb = hp[nb + 1];
+  if (h_prefix) memcpy(h_prefix, hp, (size_t)(nb + 1) * 8);
+  if (max_bucket_out) *max_bucket_out = maxb;
+  const int64_t cap = maxb;
+  const size_t csm = (size_t)cap * 16 + (size_t)((cap + 7) & ~7) * 2 + BK_CBINS * 4;
+  if (use_cluster && csm <= 200 * 1024) {
     SHK_CUDA(cudaFuncSetAttribute(bk_cluster_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
     SHK_CUDA(cudaFuncSetAttribute(bk_cluster_sort_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
