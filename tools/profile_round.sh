@@ -17,4 +17,6 @@ ncu --set full --import-source on --clock-control none -k regex:tree_kernel -s 2
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --leaf-configs "" --queries 0 > gpurun_out/ncu_tree_$TAG.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"ribbon_(elim|forms)" -s 40 -c 2 -o gpurun_out/ribbon_$TAG \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --leaf-configs "" --queries 0 > gpurun_out/ncu_ribbon_$TAG.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"bk_l1_scatter|bk_cluster_sort|ribbon_keyrows_bins" -s 6 -c 3 -o gpurun_out/bucket_$TAG \
+  python bench.py --steps 1 --warmup 3 --no-cpu-baseline --leaf-configs "" --queries 0 > gpurun_out/ncu_bucket_$TAG.log 2>&1
 echo done
