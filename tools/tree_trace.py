@@ -90,3 +90,10 @@ for w_ in range(int(wid.max()) + 1):
     if m_.any():
         d40 = dur[m_ & f40]
         print(f"  {w_:3d}: {m_.sum():7d} {dur[m_].mean()*1e3:9.0f} {d40.mean()*1e3 if len(d40) else 0:9.0f}")
+# the tail: the nodes still running in the last 3 ms of the launch
+tail_t = span - 3.0
+late = np.nonzero(en > tail_t)[0]
+print(f"nodes running after {tail_t:.2f} ms: {len(late)} "
+      f"(leaves {np.count_nonzero((info[late] & 255) == 0)}, splits {np.count_nonzero((info[late] & 255) != 0)})")
+for i in late[np.argsort(-en[late])][:24]:
+    print(f"  m={info[i] >> 8} fanout={info[i] & 255} warpid={wid[i]}: start {st[i]:7.2f} end {en[i]:7.2f} ms, {dur[i]:.2f} ms")
