@@ -268,7 +268,7 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
 // Cells of one key in the rotation search: OR its two cells into the A or B
 // coverage mask (bit = split bit, 1 = B) and store its packed edge.
 #ifndef SHK_ROT_UNROLL
-#define SHK_ROT_UNROLL 4  // keys per iteration of the rotate filter loop (independent hash chains)
+#define SHK_ROT_UNROLL 3  // keys per iteration of the rotate filter loop (independent hash chains); 3 vs 4: -0.2 ms (C4, 4 A/B pairs)
 #endif
 constexpr int kRotUnroll = SHK_ROT_UNROLL;
 template <bool WIDE>
