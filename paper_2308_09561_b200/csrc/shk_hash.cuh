@@ -235,17 +235,20 @@ SHK_D u2 remix_pre_d(u2 kp, u2 k_lo, u2 xp) {
   return xs_sel<31, AM, 4>(z);
 }
 
+// AM bit i: xor-shift i (27, 31, 30, 27) takes its high-word shift on the
+// ALU pipe (SHF) instead of the FMA pipe (IMAD.HI, two FMA issue slots).
+template <int AM = 0>
 SHK_D uint32_t remix_top_pre_d(u2 kp, u2 k_lo, u2 xp) {
   u2 z;
   z.lo = kp.lo ^ xp.lo;
   z.hi = kp.hi ^ xp.hi;
   z = mulc<MUL1>(z);
-  z = mulc<MUL2>(xorshr<27>(z));
-  z = xorshr<31>(z);
+  z = mulc<MUL2>(xs_sel<27, AM, 0>(z));
+  z = xs_sel<31, AM, 1>(z);
   z.lo ^= k_lo.lo;
   z.hi ^= k_lo.hi;
-  z = mulc<MUL1>(xorshr<30>(z));
-  return mulc_hi<MUL2>(xorshr<27>(z)) >> 31;
+  z = mulc<MUL1>(xs_sel<30, AM, 2>(z));
+  return mulc_hi<MUL2>(xs_sel<27, AM, 3>(z)) >> 31;
 }
 
 

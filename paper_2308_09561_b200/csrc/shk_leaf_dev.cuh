@@ -267,6 +267,18 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
 
 // Cells of one key in the rotation search: OR its two cells into the A or B
 // coverage mask (bit = split bit, 1 = B) and store its packed edge.
+// High-word shift placement of the rotation search's two remixes per key
+// (bit i: xor-shift i on the ALU pipe, else IMAD.HI on the FMA pipe; see
+// remix_pre_d / remix_top_pre_d).  IMAD.HI takes two FMA issue slots
+// (tools/int_peak.py), which made the rotation loop FMA-bound: all nine shifts
+// on the ALU pipe measured C4 99.06 -> 98.17 ms (20-step A/Bs; one, two, five
+// and four of them in between).
+#ifndef SHK_ROT_SHIFT_MASK
+#define SHK_ROT_SHIFT_MASK 0x1F
+#endif
+#ifndef SHK_ROT_TOP_SHIFT_MASK
+#define SHK_ROT_TOP_SHIFT_MASK 0xF
+#endif
 #ifndef SHK_ROT_UNROLL
 #define SHK_ROT_UNROLL 3  // keys per iteration of the rotate filter loop (independent hash chains); 3 vs 4: -0.2 ms (C4, 4 A/B pairs)
 #endif
@@ -332,8 +344,9 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
           for (int i = 0; i < n; ++i) {
             const uint4 k = sm.keys[i];
             const u2 kh{k.x, k.y}, kl{k.z, k.w};
-            const uint32_t bit = remix_top_pre_d(kh, kl, xb);
-            rot_key_cells<WIDE>(remix_pre_d(kh, kl, xg), un, unm1, bit, ma0, ma1, mb0, mb1, na, e + i * 32);
+            const uint32_t bit = remix_top_pre_d<SHK_ROT_TOP_SHIFT_MASK>(kh, kl, xb);
+            rot_key_cells<WIDE>(remix_pre_d<SHK_ROT_SHIFT_MASK>(kh, kl, xg), un, unm1, bit, ma0, ma1, mb0, mb1, na,
+                                e + i * 32);
           }
         } else {
           const u2 xa = seed_mixer_pre_d(sa, TAG_LEAF);

@@ -54,6 +54,13 @@ __global__ void node_index_kernel(ShkQueryDesc d, uint64_t* node_val, int32_t* b
   }
 }
 
+// High-word shift placement of the query's full remixes (ribbon patterns,
+// leaf cells, split bit): 0 = IMAD.HI on the FMA pipe (two issue slots).
+#ifndef SHK_QUERY_SHIFTS_ALU
+#define SHK_QUERY_SHIFTS_ALU 1  // all on the ALU pipe: 1e8 queries 3.838 -> 3.826 ms (3 A/B pairs)
+#endif
+constexpr int QAM = SHK_QUERY_SHIFTS_ALU ? 0x1F : 0, QTM = SHK_QUERY_SHIFTS_ALU ? 0xF : 0;
+
 // Pre-mixed per-descriptor mixers of the query (constant over a launch).
 struct QueryMixers {
   u2 bucket, rstart, rpat0, rpat1;
@@ -63,8 +70,8 @@ SHK_D uint64_t rib_choice(const ShkQueryDesc& d, const QueryMixers& mx, u2 kp, u
   if (!d.rib_m) return 0;
   const uint64_t span = (uint64_t)(d.rib_m - RIBBON_W + 1);
   const int64_t s = (int64_t)(((uint64_t)remix_hi_pre_d(kp, kl, mx.rstart) * span) >> 32);
-  const u2 a = remix_pre_d(kp, kl, mx.rpat0);
-  const u2 b = remix_pre_d(kp, kl, mx.rpat1);
+  const u2 a = remix_pre_d<QAM>(kp, kl, mx.rpat0);
+  const u2 b = remix_pre_d<QAM>(kp, kl, mx.rpat1);
   const uint64_t pat0 = join64(a.lo | 1u, a.hi), pat1 = join64(b.lo, b.hi);
   const int64_t wi = s >> 6;
   const int sh = (int)(s & 63);
@@ -95,7 +102,7 @@ SHK_D uint32_t leaf_cell_pre(u2 kp, u2 kl, uint64_t q, uint32_t n, int mode, int
   if (n <= 1) return 0;  // leaf_pair gives (0, 0)
   uint32_t h0, h1;
   if (mode == 0) {
-    leaf_pair_d(remix_pre_d(kp, kl, seed_mixer_pre_d(q, TAG_LEAF)), n, n - 1, h0, h1);
+    leaf_pair_d(remix_pre_d<QAM>(kp, kl, seed_mixer_pre_d(q, TAG_LEAF)), n, n - 1, h0, h1);
     return choice ? h1 : h0;
   }
   uint64_t base = q >> 6, r = q & 63;  // node_index_kernel's packing
@@ -105,11 +112,11 @@ SHK_D uint32_t leaf_cell_pre(u2 kp, u2 kl, uint64_t q, uint32_t n, int mode, int
     r = q - base * n;
   }
   const uint64_t sa = (mode == 2 && cache_k && n > 32) ? base - base % (uint64_t)cache_k : base;
-  if (remix_top_pre_d(kp, kl, seed_mixer_pre_d(sa, TAG_SPLITBIT)) == 0) {
-    leaf_pair_d(remix_pre_d(kp, kl, seed_mixer_pre_d(sa, TAG_LEAF)), n, n - 1, h0, h1);
+  if (remix_top_pre_d<QTM>(kp, kl, seed_mixer_pre_d(sa, TAG_SPLITBIT)) == 0) {
+    leaf_pair_d(remix_pre_d<QAM>(kp, kl, seed_mixer_pre_d(sa, TAG_LEAF)), n, n - 1, h0, h1);
     return choice ? h1 : h0;
   }
-  leaf_pair_d(remix_pre_d(kp, kl, seed_mixer_pre_d(base, TAG_LEAF)), n, n - 1, h0, h1);
+  leaf_pair_d(remix_pre_d<QAM>(kp, kl, seed_mixer_pre_d(base, TAG_LEAF)), n, n - 1, h0, h1);
   uint32_t h = (choice ? h1 : h0) + (uint32_t)r;  // < 2n
   return h >= n ? h - n : h;
 }
