@@ -272,9 +272,11 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
 // remix_pre_d / remix_top_pre_d).  IMAD.HI takes two FMA issue slots
 // (tools/int_peak.py), which made the rotation loop FMA-bound: all nine shifts
 // on the ALU pipe measured C4 99.06 -> 98.17 ms (20-step A/Bs; one, two, five
-// and four of them in between).
+// and four of them in between), and eight of them (the cells remix's first
+// shift back on IMAD.HI) 98.31 -> 98.11 ms over 4 pairs; other single or
+// double moves back measured equal or slower.
 #ifndef SHK_ROT_SHIFT_MASK
-#define SHK_ROT_SHIFT_MASK 0x1F
+#define SHK_ROT_SHIFT_MASK 0x1E
 #endif
 #ifndef SHK_ROT_TOP_SHIFT_MASK
 #define SHK_ROT_TOP_SHIFT_MASK 0xF
