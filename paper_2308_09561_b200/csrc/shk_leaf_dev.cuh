@@ -153,8 +153,10 @@ SHK_D void plain_fill_edges(const uint4* keys, int n, uint64_t s, unsigned lanes
 // loop is FMA-pipe bound with every high-word shift on IMAD.HI (ncu: C3
 // fmaheavy 83% / ALU 63%, C5 fmaheavy 85% / ALU 63%), so all five shifts go
 // to the ALU pipe (tools/ab_leaf.sh: C3 26.0 -> 25.5 ms; C5 13.03-13.08 ->
-// 12.82-12.92 s).  The rotate search in the build keeps the FMA placement:
-// the tree kernel is ALU-heavier (split hashes), ncu ALU 72% / fmaheavy 65%.
+// 12.82-12.92 s).  The rotate search in the build was left on the FMA
+// placement in round 1 (the tree kernel is ALU-heavier overall); measured
+// again once IMAD.HI was known to take two FMA issue slots, it is faster with
+// the shifts on the ALU pipe too (SHK_ROT_SHIFT_MASK below).
 // Re-swept for the stealing kernel (ncu C3: ALU 76%, fmaheavy 64%): C3 best
 // with shift 4 on the FMA pipe (0x0F: 23.62 vs 23.93 ms), C5 with shifts 1
 // and 3 there (0x15: 11.20 vs 11.41 s); all-FMA (0x00) is the slowest.
