@@ -58,6 +58,7 @@ struct LeafSmem {
   uint64_t slot_aev_le[2][TW];
   uint64_t slot_aev[2][TW];
   uint8_t eu[MAXE], ev[MAXE];
+  uint2 onehot[64];               // (rotation search, 64-bit masks) 1 << h as (lo, hi) words
   uint64_t inc[MAXE];
   WarpChk chk[TW];                // per-warp scratch of the exact check
   int64_t leaf;
@@ -288,14 +289,24 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
 #endif
 constexpr int kRotUnroll = SHK_ROT_UNROLL;
 template <bool WIDE>
+// SHK_ROT_ONEHOT_LDS: the 64-bit one-hots of the two cells come from a
+// shared-memory table (two LDS.64 on the LSU pipe) instead of four shifts and
+// two XORs on the ALU pipe, which the rotation loop saturates.
+#ifndef SHK_ROT_ONEHOT_LDS
+#define SHK_ROT_ONEHOT_LDS 1
+#endif
 SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_t& ma0, uint32_t& ma1,
-                         uint32_t& mb0, uint32_t& mb1, uint32_t& na, uint16_t* e) {
+                         uint32_t& mb0, uint32_t& mb1, uint32_t& na, uint16_t* e, const uint2* onehot = nullptr) {
   uint32_t h0, h1;
   leaf_pair_d(v, un, unm1, h0, h1);
   const uint32_t sel = 0u - bit;  // all ones for B
   uint32_t c0, c1 = 0;
   if (!WIDE) {
     c0 = (1u << h0) | (1u << h1);
+  } else if (SHK_ROT_ONEHOT_LDS && onehot) {
+    const uint2 t0 = onehot[h0], t1 = onehot[h1];
+    c0 = t0.x | t1.x;
+    c1 = t0.y | t1.y;
   } else {
     // 64-bit one-hots: low word clamps to 0 for h >= 32, and the wrapped
     // shift (h mod 32) differs from it exactly when h >= 32
@@ -318,6 +329,9 @@ template <int TW, bool WIDE, class SM>
 SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafOut& o, int team,
                         int warp, int lane, int tt) {
   load_leaf_keys<TW>(a, sm, k0, n, tt);
+  if (WIDE && SHK_ROT_ONEHOT_LDS) {
+    for (int h = tt; h < 64; h += TW * 32) sm.onehot[h] = make_uint2(h < 32 ? 1u << h : 0u, h < 32 ? 0u : 1u << (h - 32));
+  }
   team_sync<TW>(team);
   uint16_t* e = &sm.edges[warp][lane];
   const int64_t ck = (n > a.cache_min_leaf) ? a.cache_k : 0;
@@ -350,7 +364,7 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
             const u2 kh{k.x, k.y}, kl{k.z, k.w};
             const uint32_t bit = remix_top_pre_d<SHK_ROT_TOP_SHIFT_MASK>(kh, kl, xb);
             rot_key_cells<WIDE>(remix_pre_d<SHK_ROT_SHIFT_MASK>(kh, kl, xg), un, unm1, bit, ma0, ma1, mb0, mb1, na,
-                                e + i * 32);
+                                e + i * 32, sm.onehot);
           }
         } else {
           const u2 xa = seed_mixer_pre_d(sa, TAG_LEAF);
