@@ -205,11 +205,22 @@ SHK_D bool equal_split_ok(int F, int m) {
 #ifndef SHK_SPLIT_EQ_SEEDS
 #define SHK_SPLIT_EQ_SEEDS 1  // seeds per lane (S > 1: lane tests R + lane + 32 j, j < S, per key load)
 #endif
+// SHK_SPLIT_CNT_LDS: the F = 4 byte counter's increment 1 << 8 part comes from
+// a 4-entry shared-memory table (one LDS on the LSU pipe) instead of a mask
+// and a variable shift on the ALU pipe, which the construction kernel saturates.
+#ifndef SHK_SPLIT_CNT_LDS
+#define SHK_SPLIT_CNT_LDS 1
+#endif
 template <int F>
 SHK_D int64_t split_search_equal(const ulonglong2* kp, const ShkSplitTask& task, uint64_t max_seed, int lane) {
   constexpr int U = SHK_SPLIT_EQ_BLOCK, S = SHK_SPLIT_EQ_SEEDS;
   const int m = task.m;
   const int sz = m / F;
+  __shared__ uint32_t cnt_tab[4];  // 1 << 8 p (written by every warp before its search: same values)
+  if (F == 4 && SHK_SPLIT_CNT_LDS) {
+    if (lane < 4) cnt_tab[lane] = 1u << (8 * lane);
+    __syncwarp();
+  }
   const uint32_t K4 = (uint32_t)(127 - sz) * 0x01010101u;  // byte b > sz <=> bit 7 of (b + 127 - sz)
   for (uint64_t R = 0; R < max_seed; R += 32 * S) {
     u2 x[S];
@@ -232,6 +243,8 @@ SHK_D int64_t split_search_equal(const ulonglong2* kp, const ShkSplitTask& task,
         const uint32_t p = __umulhi(vh, 3u);
         a[j] += p;
         b[j] += p >> 1;
+      } else if (SHK_SPLIT_CNT_LDS) {
+        a[j] += cnt_tab[vh >> 30];
       } else {
         a[j] += 1u << ((vh >> 27) & 24u);
       }
