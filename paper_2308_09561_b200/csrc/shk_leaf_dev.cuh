@@ -295,6 +295,13 @@ template <bool WIDE>
 #ifndef SHK_ROT_ONEHOT_LDS
 #define SHK_ROT_ONEHOT_LDS 1
 #endif
+// SHK_ROT_MASK_LDS: further, the table is indexed by (split bit, cell) and
+// holds the one-hot already placed in the A or the B half of a 4-word
+// (ma0, ma1, mb0, mb1) record, so a key's cells OR straight into the masks
+// (two LDS.128, four 3-input ORs; no select).  One table per CTA.
+#ifndef SHK_ROT_MASK_LDS
+#define SHK_ROT_MASK_LDS 1
+#endif
 SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_t& ma0, uint32_t& ma1,
                          uint32_t& mb0, uint32_t& mb1, uint32_t& na, uint16_t* e, const uint2* onehot = nullptr) {
   uint32_t h0, h1;
@@ -303,6 +310,16 @@ SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_
   uint32_t c0, c1 = 0;
   if (!WIDE) {
     c0 = (1u << h0) | (1u << h1);
+  } else if (SHK_ROT_MASK_LDS && onehot) {
+    const uint4* t4 = reinterpret_cast<const uint4*>(onehot) + (bit << 6);
+    const uint4 t0 = t4[h0], t1 = t4[h1];
+    ma0 |= t0.x | t1.x;
+    ma1 |= t0.y | t1.y;
+    mb0 |= t0.z | t1.z;
+    mb1 |= t0.w | t1.w;
+    na += bit ^ 1u;
+    *e = (uint16_t)(h0 | (h1 << 8) | (bit << 15));
+    return;
   } else if (SHK_ROT_ONEHOT_LDS && onehot) {
     const uint2 t0 = onehot[h0], t1 = onehot[h1];
     c0 = t0.x | t1.x;
@@ -329,7 +346,17 @@ template <int TW, bool WIDE, class SM>
 SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafOut& o, int team,
                         int warp, int lane, int tt) {
   load_leaf_keys<TW>(a, sm, k0, n, tt);
-  if (WIDE && SHK_ROT_ONEHOT_LDS) {
+  __shared__ uint4 rot_tab[128];  // SHK_ROT_MASK_LDS: (bit << 6 | h) -> (ma0, ma1, mb0, mb1) one-hot, per CTA
+  const uint2* onehot_tab = sm.onehot;
+  if (WIDE && SHK_ROT_MASK_LDS) {
+    // every team writes the same values (benign) before its search
+    for (int k = tt; k < 128; k += TW * 32) {
+      const int h = k & 63;
+      const uint32_t lo = h < 32 ? 1u << h : 0u, hi = h < 32 ? 0u : 1u << (h - 32);
+      rot_tab[k] = (k >> 6) ? make_uint4(0u, 0u, lo, hi) : make_uint4(lo, hi, 0u, 0u);
+    }
+    onehot_tab = reinterpret_cast<const uint2*>(rot_tab);
+  } else if (WIDE && SHK_ROT_ONEHOT_LDS) {
     for (int h = tt; h < 64; h += TW * 32) sm.onehot[h] = make_uint2(h < 32 ? 1u << h : 0u, h < 32 ? 0u : 1u << (h - 32));
   }
   team_sync<TW>(team);
@@ -364,7 +391,7 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
             const u2 kh{k.x, k.y}, kl{k.z, k.w};
             const uint32_t bit = remix_top_pre_d<SHK_ROT_TOP_SHIFT_MASK>(kh, kl, xb);
             rot_key_cells<WIDE>(remix_pre_d<SHK_ROT_SHIFT_MASK>(kh, kl, xg), un, unm1, bit, ma0, ma1, mb0, mb1, na,
-                                e + i * 32, sm.onehot);
+                                e + i * 32, onehot_tab);
           }
         } else {
           const u2 xa = seed_mixer_pre_d(sa, TAG_LEAF);
