@@ -167,8 +167,20 @@ SHK_D void plain_fill_edges(const uint4* keys, int n, uint64_t s, unsigned lanes
 #ifndef SHK_PLAIN_SHIFT_MASK_WIDE
 #define SHK_PLAIN_SHIFT_MASK_WIDE 0x15
 #endif
+// SHK_PLAIN_ONEHOT_LDS: the cells' one-hots come from a 64-entry (lo, hi)
+// shared-memory table `tab` (LSU) instead of shifts on the ALU pipe (as in the
+// rotation search); tab == nullptr keeps the shifts.
+#ifndef SHK_PLAIN_ONEHOT_LDS
+#define SHK_PLAIN_ONEHOT_LDS 1
+#endif
+// Fill a 64-entry one-hot table (the calling warp's lanes; same values from
+// every warp of the CTA, so concurrent fills are benign).
+SHK_D void fill_onehot_tab(uint2* tab, int lane) {
+  for (int h = lane; h < 64; h += 32) tab[h] = make_uint2(h < 32 ? 1u << h : 0u, h < 32 ? 0u : 1u << (h - 32));
+  __syncwarp();
+}
 template <bool WIDE, bool STORE = true>
-SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
+SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e, const uint2* tab = nullptr) {
   u2 x = seed_mixer_pre_d(s, TAG_LEAF);
   const uint32_t un = (uint32_t)n, unm1 = (uint32_t)(n - 1);
   uint32_t m0 = 0, m1 = 0;
@@ -178,7 +190,11 @@ SHK_D bool plain_mask_full(const uint4* keys, int n, uint64_t s, uint16_t* e) {
     u2 v = remix_pre_d<WIDE ? SHK_PLAIN_SHIFT_MASK_WIDE : SHK_PLAIN_SHIFT_MASK>(u2{k.x, k.y}, u2{k.z, k.w}, x);
     uint32_t h0, h1;
     leaf_pair_d(v, un, unm1, h0, h1);
-    if (!WIDE) {
+    if (SHK_PLAIN_ONEHOT_LDS && tab) {
+      const uint2 t0 = tab[h0], t1 = tab[h1];
+      m0 |= t0.x | t1.x;
+      if (WIDE) m1 |= t0.y | t1.y;
+    } else if (!WIDE) {
       m0 |= (1u << h0) | (1u << h1);
     } else {
       m0 |= shl_clamp(1u, h0) | shl_clamp(1u, h1);
@@ -211,12 +227,14 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
     seed = 0;
     passes = 1;
   } else {
+    __shared__ uint2 plain_tab[64];  // SHK_PLAIN_ONEHOT_LDS (one per CTA)
+    if (SHK_PLAIN_ONEHOT_LDS) fill_onehot_tab(plain_tab, lane);
     // Rounds of TW*32 consecutive seeds; warp w owns [R + 32w, R + 32w + 32).
     int par = 0;
     for (uint64_t R = 0; R < a.max_seed; R += (uint64_t)TW * 32, par ^= 1) {
       const uint64_t s = R + (uint64_t)warp * 32 + lane;
       const bool valid = s < a.max_seed;
-      bool full = valid && plain_mask_full<WIDE, false>(sm.keys, n, s, e);
+      bool full = valid && plain_mask_full<WIDE, false>(sm.keys, n, s, e, SHK_PLAIN_ONEHOT_LDS ? plain_tab : nullptr);
       unsigned pb = __ballot_sync(FULL_WARP, full);
       if (pb) plain_fill_edges(sm.keys, n, s, pb, sm.edges[warp], lane);
       const bool acc = warp_first_accept(sm.edges[warp], full ? 1ull : 0ull, n, lane, sm.chk[warp]) == 0;

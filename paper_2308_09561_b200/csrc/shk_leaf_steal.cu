@@ -96,9 +96,11 @@ template <bool WIDE, int MAXE>
 __global__ void __launch_bounds__(128, 8) leaf_steal_kernel(LeafArgs a, StealLeaf* st, long long* active,
                                                              int* leaf_counter) {
   __shared__ StealSmem<MAXE> sm_all[4];
+  __shared__ uint2 onehot_tab[64];  // SHK_PLAIN_ONEHOT_LDS
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   StealSmem<MAXE>& sm = sm_all[w];
+  if (SHK_PLAIN_ONEHOT_LDS) fill_onehot_tab(onehot_tab, lane);
   const int gw = blockIdx.x * 4 + w;
   const int nw = gridDim.x * 4;
   bool tail = false;
@@ -201,7 +203,8 @@ __global__ void __launch_bounds__(128, 8) leaf_steal_kernel(LeafArgs a, StealLea
       blk = __shfl_sync(FULL_WARP, blk, 0);
       const uint64_t s0 = (uint64_t)blk * 32ull;
       const uint64_t s = s0 + lane;
-      const bool full = s < a.max_seed && plain_mask_full<WIDE, false>(sm.keys, n, s, nullptr);
+      const bool full = s < a.max_seed &&
+                        plain_mask_full<WIDE, false>(sm.keys, n, s, nullptr, SHK_PLAIN_ONEHOT_LDS ? onehot_tab : nullptr);
       const unsigned pb = __ballot_sync(FULL_WARP, full);
       if (pb) {
         const int win = plain_first_accept(sm, n, s0, pb, lane);
