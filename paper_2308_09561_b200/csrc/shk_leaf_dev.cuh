@@ -58,7 +58,6 @@ struct LeafSmem {
   uint64_t slot_aev_le[2][TW];
   uint64_t slot_aev[2][TW];
   uint8_t eu[MAXE], ev[MAXE];
-  uint2 onehot[64];               // (rotation search, 64-bit masks) 1 << h as (lo, hi) words
   uint64_t inc[MAXE];
   WarpChk chk[TW];                // per-warp scratch of the exact check
   int64_t leaf;
@@ -307,16 +306,13 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
 #endif
 constexpr int kRotUnroll = SHK_ROT_UNROLL;
 template <bool WIDE>
-// SHK_ROT_ONEHOT_LDS: the 64-bit one-hots of the two cells come from a
-// shared-memory table (two LDS.64 on the LSU pipe) instead of four shifts and
-// two XORs on the ALU pipe, which the rotation loop saturates.
-#ifndef SHK_ROT_ONEHOT_LDS
-#define SHK_ROT_ONEHOT_LDS 1
-#endif
-// SHK_ROT_MASK_LDS: further, the table is indexed by (split bit, cell) and
-// holds the one-hot already placed in the A or the B half of a 4-word
-// (ma0, ma1, mb0, mb1) record, so a key's cells OR straight into the masks
-// (two LDS.128, four 3-input ORs; no select).  One table per CTA.
+// SHK_ROT_MASK_LDS: the 64-bit one-hots of the two cells come from a
+// shared-memory table (LSU pipe) instead of shifts and XORs on the ALU pipe,
+// which the rotation loop saturates.  The table is indexed by (split bit,
+// cell) and holds the one-hot already placed in the A or the B half of a
+// 4-word (ma0, ma1, mb0, mb1) record, so a key's cells OR straight into the
+// masks (two LDS.128, four 3-input ORs; no select).  One table per CTA.
+// (A (lo, hi) one-hot table with the A/B select kept measured half the gain.)
 #ifndef SHK_ROT_MASK_LDS
 #define SHK_ROT_MASK_LDS 1
 #endif
@@ -338,10 +334,6 @@ SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_
     na += bit ^ 1u;
     *e = (uint16_t)(h0 | (h1 << 8) | (bit << 15));
     return;
-  } else if (SHK_ROT_ONEHOT_LDS && onehot) {
-    const uint2 t0 = onehot[h0], t1 = onehot[h1];
-    c0 = t0.x | t1.x;
-    c1 = t0.y | t1.y;
   } else {
     // 64-bit one-hots: low word clamps to 0 for h >= 32, and the wrapped
     // shift (h mod 32) differs from it exactly when h >= 32
@@ -365,7 +357,7 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
                         int warp, int lane, int tt) {
   load_leaf_keys<TW>(a, sm, k0, n, tt);
   __shared__ uint4 rot_tab[128];  // SHK_ROT_MASK_LDS: (bit << 6 | h) -> (ma0, ma1, mb0, mb1) one-hot, per CTA
-  const uint2* onehot_tab = sm.onehot;
+  const uint2* onehot_tab = nullptr;
   if (WIDE && SHK_ROT_MASK_LDS) {
     // every team writes the same values (benign) before its search
     for (int k = tt; k < 128; k += TW * 32) {
@@ -374,8 +366,6 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
       rot_tab[k] = (k >> 6) ? make_uint4(0u, 0u, lo, hi) : make_uint4(lo, hi, 0u, 0u);
     }
     onehot_tab = reinterpret_cast<const uint2*>(rot_tab);
-  } else if (WIDE && SHK_ROT_ONEHOT_LDS) {
-    for (int h = tt; h < 64; h += TW * 32) sm.onehot[h] = make_uint2(h < 32 ? 1u << h : 0u, h < 32 ? 0u : 1u << (h - 32));
   }
   team_sync<TW>(team);
   uint16_t* e = &sm.edges[warp][lane];
