@@ -305,7 +305,6 @@ SHK_D void solve_plain(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafO
 #define SHK_ROT_UNROLL 3  // keys per iteration of the rotate filter loop (independent hash chains); 3 vs 4: -0.2 ms (C4, 4 A/B pairs)
 #endif
 constexpr int kRotUnroll = SHK_ROT_UNROLL;
-template <bool WIDE>
 // SHK_ROT_MASK_LDS: the 64-bit one-hots of the two cells come from a
 // shared-memory table (LSU pipe) instead of shifts and XORs on the ALU pipe,
 // which the rotation loop saturates.  The table is indexed by (split bit,
@@ -316,6 +315,16 @@ template <bool WIDE>
 #ifndef SHK_ROT_MASK_LDS
 #define SHK_ROT_MASK_LDS 1
 #endif
+#ifndef SHK_ROT_FMA_BOOK
+#define SHK_ROT_FMA_BOOK 1
+#endif
+// a * b + c as one IMAD (written in PTX so it stays on the FMA pipe)
+SHK_D uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+template <bool WIDE>
 SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_t& ma0, uint32_t& ma1,
                          uint32_t& mb0, uint32_t& mb1, uint32_t& na, uint16_t* e, const uint2* onehot = nullptr) {
   uint32_t h0, h1;
@@ -331,8 +340,16 @@ SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_
     ma1 |= t0.y | t1.y;
     mb0 |= t0.z | t1.z;
     mb1 |= t0.w | t1.w;
+#if SHK_ROT_FMA_BOOK
+    // (table path) na counts the B keys here (the caller turns it into the A
+    // count after the loop) and the edge is packed with multiply-adds: the
+    // bookkeeping runs on the FMA pipe, the ALU pipe being the bound
+    na = imad_u32(bit, 1u, na);
+    *e = (uint16_t)imad_u32(bit, 0x8000u, imad_u32(h1, 0x100u, h0));
+#else
     na += bit ^ 1u;
     *e = (uint16_t)(h0 | (h1 << 8) | (bit << 15));
+#endif
     return;
   } else {
     // 64-bit one-hots: low word clamps to 0 for h >= 32, and the wrapped
@@ -401,6 +418,7 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
             rot_key_cells<WIDE>(remix_pre_d<SHK_ROT_SHIFT_MASK>(kh, kl, xg), un, unm1, bit, ma0, ma1, mb0, mb1, na,
                                 e + i * 32, onehot_tab);
           }
+          if (SHK_ROT_FMA_BOOK && WIDE && SHK_ROT_MASK_LDS) na = (uint32_t)n - na;  // B count -> A count
         } else {
           const u2 xa = seed_mixer_pre_d(sa, TAG_LEAF);
 #pragma unroll 2
