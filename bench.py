@@ -258,7 +258,10 @@ def roofline_numbers(prof, hash_evals, n, clock_mhz, sms, int_peak=None):
     peak = INT_OPS_PER_CLK_SM * sms * MAX_MHZ * 1e6 / 1e12  # Tops/s at max clock
     if ph["leaf_search"] < 0.05 * ph["split_search"]:
         # persistent schedule: split and leaf searches share one kernel launch
-        kern = {"tree_kernel(split+leaf search)": (leaf_ops + split_ops, ph["split_search"] + ph["leaf_search"])}
+        # (and its tail: tree_resume_kernel, the leaves handed off when the
+        # queue ran dry -- both inside the timed phase)
+        kern = {"tree_kernel+tree_resume_kernel(split+leaf search)": (leaf_ops + split_ops,
+                                                                      ph["split_search"] + ph["leaf_search"])}
     else:
         kern = {
             "leaf_search": (leaf_ops, ph["leaf_search"]),

@@ -238,8 +238,10 @@ typedef struct shk_plans {
  *   and the Rice stream for buckets [b0, b1) (recsplit.py:499-521).
  * ribbon: retrieval over ALL keys with the choice bits (recsplit.py:523);
  *   choice (nullable, host or device per flags) overrides the build's own.
- * stats_out[7] of run: hash_evals, filter_passes, exact_checks, a_evals,
- *   leaf_seed_bits, split_seed_bits, leaf_count (recsplit.py:539-547). */
+ * stats_out[8] of run: hash_evals, filter_passes, exact_checks, a_evals,
+ *   leaf_seed_bits, split_seed_bits, leaf_count (recsplit.py:539-547), and
+ *   the number of leaves the persistent kernel handed to the resume teams
+ *   at its tail (rotate modes; SHK_TREE_HANDOFF_TW, diagnostic only). */
 int shk_build_create(shk_ctx* ctx, const uint64_t* hi, const uint64_t* lo, int64_t N, int64_t nbuckets, int flags,
                      shk_build** out, int* dup, int64_t* max_bucket);
 int shk_build_duplicate(shk_build* b, int* dup /* 0 or 1; waits for the sort */);

@@ -1490,23 +1490,27 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
   // the seed searches take pre-mixed key high words (shk_hash.cuh premix_hi);
   // undone right after the leaves
   RC(shk_launch_premix(b->keys.as<uint64_t>(), b->N, 0, c->stream));
-  DBuf dnodes(c), dqueue(c), dtab(c);
+  // dtab: queue counters + hand-off words (64 B), then node_base, key starts,
+  // root slots and bucket plans
+  constexpr size_t kTabNodeBase = 64;
+  DBuf dnodes(c), dqueue(c), dtab(c), dhand(c);
   if (use_tree && nn > 0) {
     // ---- node table expanded on the device from the (small) plan tables:
     // the plan nodes are the cached device copy; the per-bucket tables and
     // the queue counters go up in ONE copy from pinned staging
     RC(dnodes.alloc((size_t)nn * sizeof(ShkTreeNode)));
     RC(dqueue.alloc((size_t)nn * 8));
-    const size_t o_qc = 0, o_nb = 32, o_ks = o_nb + (size_t)(nbr + 1) * 8, o_rp = o_ks + (size_t)(nbr + 1) * 8,
+    const size_t o_qc = 0, o_nb = kTabNodeBase, o_ks = o_nb + (size_t)(nbr + 1) * 8, o_rp = o_ks + (size_t)(nbr + 1) * 8,
                  o_bp = o_rp + (size_t)(nbr + 1) * 8, tab_bytes = o_bp + (size_t)(nbr + 1) * 4;
     RC(dtab.alloc(tab_bytes));
     void* hs = nullptr;
     RC(host_stage(c, tab_bytes, &hs));
     char* H = (char*)hs;
     // split head, leaf head, split tail, leaf tail
-    const unsigned long long qc[4] = {0ull, (unsigned long long)nsplit, (unsigned long long)nroots_split,
-                                      (unsigned long long)(nsplit + nroots_leaf)};
-    memcpy(H + o_qc, qc, 32);
+    // then the hand-off flag, records written, resume fetch counter
+    const unsigned long long qc[8] = {0ull, (unsigned long long)nsplit, (unsigned long long)nroots_split,
+                                      (unsigned long long)(nsplit + nroots_leaf), 0ull, 0ull, 0ull, 0ull};
+    memcpy(H + o_qc, qc, 64);
     memcpy(H + o_nb, node_base.data(), (size_t)(nbr + 1) * 8);
     memcpy(H + o_ks, kstart_v.data(), (size_t)nbr * 8);
     memcpy(H + o_rp, root_pos.data(), (size_t)nbr * 8);
@@ -1556,6 +1560,18 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     p.stats_acc = dacc.as<unsigned long long>();
     p.exhausted = exh;
     p.num_sms = c->num_sms;
+    // rotate tail hand-off (shk_tree.cu): SHK_TREE_HANDOFF_TW = warps per
+    // resume team (0 = off: the flag is never raised)
+    if (mode != 0) {
+      const char* ht = getenv("SHK_TREE_HANDOFF_TW");
+      p.handoff_tw = ht ? atoi(ht) : 8;
+      p.handoff_cap = (int64_t)(c->num_sms > 0 ? c->num_sms : 148) * 64;
+      RC(dhand.alloc((size_t)p.handoff_cap * 56));
+      p.handoff = dhand.p;
+      p.abort_flag = (int*)(D + o_qc + 32);
+      p.handoff_count = dacc.as<unsigned long long>() + 7;  // read back with the stats
+      p.handoff_next = (unsigned long long*)(D + o_qc + 40);
+    }
     RC(shk_launch_tree(p, c->stream));
     HOST_TRACE("tree launched");
     b->mark(3);
@@ -1655,7 +1671,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
                       c->stream));
   // per-bucket bit offsets: pos[node_base[i]]
   // (the persistent schedule's device copy of node_base is still in dtab)
-  const int64_t* d_nb = dtab.p ? (const int64_t*)(dtab.as<char>() + 32) : nullptr;
+  const int64_t* d_nb = dtab.p ? (const int64_t*)(dtab.as<char>() + kTabNodeBase) : nullptr;
   if (!d_nb) {
     RC(dnb.alloc((size_t)(nbr + 1) * 8));
     RC(h2d(c, dnb.p, node_base.data(), (size_t)(nbr + 1) * 8));
@@ -1683,6 +1699,7 @@ int shk_build_run(shk_build* b, const shk_plans* plans, int mode, int cache_k, i
     stats_out[4] = (int64_t)acc[4];  // leaf seed bits
     stats_out[5] = (int64_t)acc[5];  // split seed bits
     stats_out[6] = n_leaves;
+    stats_out[7] = (int64_t)acc[7];  // leaves the tree kernel handed off to the resume teams
   }
   b->b0 = b0;
   b->b1 = b1;

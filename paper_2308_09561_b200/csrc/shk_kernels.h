@@ -117,6 +117,17 @@ struct ShkTreeLaunch {
   int* exhausted;
   int num_sms;
   const int* dup_flag;  // optional: the bucket sort's duplicate flag (nonzero: the kernel does nothing)
+  // rotate search tail hand-off (required when mode != 0): the flag the kernel
+  // raises once every leaf is handed out, a buffer of handoff_cap 56-byte
+  // records (>= the resident warps), the count of records written and the
+  // resume kernel's fetch counter (all zeroed by the caller); handoff_tw:
+  // warps per resume team, 0 = no hand-off
+  int* abort_flag;
+  void* handoff;
+  int64_t handoff_cap;
+  unsigned long long* handoff_count;
+  unsigned long long* handoff_next;
+  int handoff_tw;
 };
 int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st);
 

@@ -20,6 +20,8 @@
 
 namespace shk {
 
+struct ShkHandoff;
+
 struct LeafArgs {
   const uint64_t* hi;
   const uint64_t* lo;
@@ -41,6 +43,24 @@ struct LeafArgs {
   int* exhausted;       // optional: set if a leaf has no seed below max_seed
   int64_t* place_out;   // optional [N]: global slot of each key (leaf start + its cell)
   int pre;              // hi words are already premix_hi'ed (build path)
+  // Tail hand-off of the persistent construction kernel (shk_tree.cu), rotate
+  // search with one-warp teams only: once abort_flag is set, a warp ends its
+  // leaf after the current round and records where the search stands; the
+  // resume kernel finishes the recorded leaves with multi-warp teams.
+  const int* abort_flag;               // optional
+  ShkHandoff* handoff;                 // [capacity]
+  unsigned long long* handoff_count;
+};
+
+// A leaf search stopped at a round boundary: every base below `next_base` is
+// searched (no acceptance), the counters cover exactly those bases.
+struct ShkHandoff {
+  int64_t seed_slot;
+  int64_t k0;
+  uint64_t next_base;
+  uint64_t evals, passes, aev;
+  int32_t n;
+  int32_t pad;
 };
 
 // MAXE: most keys per leaf the team's buffers hold (64, or 40 to fit more
@@ -369,9 +389,19 @@ SHK_D void rot_key_cells(u2 v, uint32_t un, uint32_t unm1, uint32_t bit, uint32_
 }
 
 // Rotation fitting of one leaf: lane per base seed.
-template <int TW, bool WIDE, class SM>
+#ifndef SHK_HANDOFF_EVERY
+// rounds between abort-flag checks (power of two; 1 and 4 measured equal at C4,
+// and the flag load placed at the top of a round or folded into the winner's
+// exit measured slower: the hot loop's schedule moves)
+#define SHK_HANDOFF_EVERY 1
+#endif
+// HANDOFF (one-warp teams): check a.abort_flag after every round without an
+// acceptance and hand the leaf off if it is set.  Resume: start at base R0
+// with the counters of the bases below it.
+template <int TW, bool WIDE, bool HANDOFF = false, class SM>
 SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const LeafOut& o, int team,
-                        int warp, int lane, int tt) {
+                        int warp, int lane, int tt, uint64_t R0 = 0, uint64_t ev0 = 0, uint64_t pass0 = 0,
+                        uint64_t aev0 = 0) {
   load_leaf_keys<TW>(a, sm, k0, n, tt);
   __shared__ uint4 rot_tab[128];  // SHK_ROT_MASK_LDS: (bit << 6 | h) -> (ma0, ma1, mb0, mb1) one-hot, per CTA
   const uint2* onehot_tab = nullptr;
@@ -388,7 +418,8 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
   uint16_t* e = &sm.edges[warp][lane];
   const int64_t ck = (n > a.cache_min_leaf) ? a.cache_k : 0;
   int64_t q = -1;
-  uint64_t passes = 0, evals = 0, aev = 0;
+  uint64_t passes = pass0, evals = ev0, aev = aev0;
+  uint64_t stop_at = 0;  // HANDOFF: next base of a search stopped by the abort flag (0: not stopped)
   if (n <= 1) {
     q = 0;
     passes = 1;
@@ -397,7 +428,7 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
     const uint64_t max_base = a.max_seed / (uint64_t)n + 1;
     const uint32_t un = (uint32_t)n, unm1 = (uint32_t)(n - 1);
     int par = 0;
-    for (uint64_t R = 0; R < max_base; R += (uint64_t)TW * 32, par ^= 1) {
+    for (uint64_t R = R0; R < max_base; R += (uint64_t)TW * 32, par ^= 1) {
       const uint64_t base = R + (uint64_t)warp * 32 + lane;
       const bool valid = base < max_base;
       uint64_t passmask = 0;
@@ -504,6 +535,14 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
           q = (qq >= a.max_seed) ? -1 : (int64_t)qq;
           break;
         }
+        if (HANDOFF && (SHK_HANDOFF_EVERY == 1 || ((R >> 5) & (SHK_HANDOFF_EVERY - 1)) == 0)) {
+          int f;  // volatile asm: one relaxed load per round (not hoisted), no memory clobber
+          asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(a.abort_flag));
+          if (__any_sync(FULL_WARP, f != 0)) {
+            stop_at = R + 32;
+            break;
+          }
+        }
         continue;
       }
       if (lane == 0) {
@@ -542,6 +581,22 @@ SHK_D void solve_rotate(const LeafArgs& a, SM& sm, int64_t k0, int n, const Leaf
         break;
       }
     }
+  }
+  if (HANDOFF && stop_at) {
+    if (lane == 0) {
+      ShkHandoff h;
+      h.seed_slot = o.seed_slot;
+      h.k0 = k0;
+      h.next_base = stop_at;
+      h.evals = evals;
+      h.passes = passes;
+      h.aev = aev;
+      h.n = n;
+      h.pad = 0;
+      a.handoff[atomicAdd(a.handoff_count, 1ull)] = h;
+    }
+    __syncwarp();
+    return;
   }
   if (warp == 0) {
     if (q >= 0 && n >= 2) {

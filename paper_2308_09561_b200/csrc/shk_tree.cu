@@ -57,6 +57,7 @@ struct TreeArgs {
   int64_t* seeds;
   int* exhausted;
   const int* dup_flag;         // nonzero: equal codes in the input, every warp exits (the host raises)
+  int set_abort;               // rotate tail hand-off: raise leaf.abort_flag once the leaf queue is empty
   LeafArgs leaf;
 };
 
@@ -128,7 +129,12 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       }
       if (lane == 0) h = atomicAdd(t.head + 1, 1ull);
       h = __shfl_sync(FULL_WARP, h, 0);
-      if (h >= (unsigned long long)t.nnodes) break;
+      if (h >= (unsigned long long)t.nnodes) {
+        // every leaf is handed out: the leaves still searching stop at their
+        // next round boundary and tree_resume_kernel finishes them with teams
+        if (t.set_abort && lane == 0) *(volatile int*)t.leaf.abort_flag = 1;
+        break;
+      }
     }
     int64_t id = -1;
     if (lane == 0) {
@@ -171,7 +177,7 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       if (MODE == 0)
         solve_plain<1, WIDE>(t.leaf, sm, nd.start, nd.m, o, 0, 0, lane, lane);
       else
-        solve_rotate<1, WIDE>(t.leaf, sm, nd.start, nd.m, o, 0, 0, lane, lane);
+        solve_rotate<1, WIDE, true>(t.leaf, sm, nd.start, nd.m, o, 0, 0, lane, lane);
     }
 #ifdef SHK_TREE_TRACE
     if (lane == 0 && id < (1 << 20)) {
@@ -184,6 +190,30 @@ __global__ void __launch_bounds__(128, MINB) tree_kernel(TreeArgs t) {
       g_tree_trace_m[id] = ((unsigned)nd.m << 8) | (nd.kind == 0 ? (unsigned)nd.fanout : 0u) | (wid << 24);
     }
 #endif
+  }
+}
+
+// Tail hand-off, second half: one team of TW warps per CTA takes the leaves
+// the construction kernel stopped (ShkHandoff records) and resumes each at its
+// recorded base with its recorded counters.  A team round covers TW * 32
+// consecutive bases and keeps the lowest accepting (base, r), so the seed,
+// the f bits and the counters are those of the uninterrupted one-warp search.
+// A leaf's heavy seed tail is thus spread over TW warps instead of ending the
+// build on one warp.
+static_assert(sizeof(ShkHandoff) == 56, "hand-off record size is part of the host allocation");
+template <int TW, bool WIDE, int MAXE>
+__global__ void __launch_bounds__(TW * 32) tree_resume_kernel(LeafArgs a, unsigned long long* next) {
+  __shared__ LeafSmem<TW, MAXE> sm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tt = threadIdx.x;
+  const unsigned long long cnt = *(volatile const unsigned long long*)a.handoff_count;
+  for (;;) {
+    if (tt == 0) sm.leaf = (int64_t)atomicAdd(next, 1ull);
+    team_sync<TW>(0);
+    const int64_t i = sm.leaf;
+    if ((unsigned long long)i >= cnt) break;
+    const ShkHandoff h = a.handoff[i];
+    const LeafOut o{h.seed_slot, -1};
+    solve_rotate<TW, WIDE>(a, sm, h.k0, h.n, o, 0, warp, lane, tt, h.next_base, h.evals, h.passes, h.aev);
   }
 }
 
@@ -264,6 +294,10 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   a.stats_acc = p.stats_acc;
   a.exhausted = p.exhausted;
   a.place_out = p.place_out;
+  a.abort_flag = p.abort_flag;
+  a.handoff = reinterpret_cast<ShkHandoff*>(p.handoff);
+  a.handoff_count = p.handoff_count;
+  t.set_abort = p.mode != 0 && p.handoff_tw > 0 && p.abort_flag != nullptr && p.handoff_count && p.handoff_next;
   const bool wide = p.max_n > 32;
   const bool small = p.max_n <= 40;
   void (*kfn)(TreeArgs);
@@ -286,8 +320,36 @@ int shk_launch_tree(const ShkTreeLaunch& p, cudaStream_t st) {
   t.idle_wid = p.idle_wid > 0 ? p.idle_wid : 1 << 30;
   // -1: one leaf per fast warp (the slots below slow_wid on every SM)
   t.tail_reserve = p.tail_reserve >= 0 ? p.tail_reserve : (int64_t)sms * (t.slow_wid < occ * 4 ? t.slow_wid : occ * 4);
+  if (p.mode != 0 && p.abort_flag == nullptr) {
+    shk_set_error("tree launch: the rotate search needs the hand-off flag and buffer");
+    return 3;
+  }
+  if ((int64_t)sms * occ * 4 > p.handoff_cap && p.mode != 0) {
+    shk_set_error("tree launch: hand-off buffer smaller than the resident warps");
+    return 3;
+  }
   kfn<<<(unsigned)(sms * occ), 128, 0, st>>>(t);
   SHK_LAUNCHED();
+  if (t.set_abort) {
+    // resume teams: launched whatever the count (the count is on the device);
+    // with no stopped leaf every CTA exits after one atomic
+    void (*rfn)(LeafArgs, unsigned long long*);
+#define SHK_RESUME_FN(TW) \
+  (small ? (wide ? tree_resume_kernel<TW, true, 40> : tree_resume_kernel<TW, false, 40>) : tree_resume_kernel<TW, true, 64>)
+    switch (p.handoff_tw) {
+      case 1: rfn = SHK_RESUME_FN(1); break;
+      case 2: rfn = SHK_RESUME_FN(2); break;
+      case 4: rfn = SHK_RESUME_FN(4); break;
+      case 8: rfn = SHK_RESUME_FN(8); break;
+      default: shk_set_error("hand-off team size must be 1, 2, 4 or 8"); return 3;
+    }
+#undef SHK_RESUME_FN
+    int rocc = 0;
+    SHK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rocc, rfn, p.handoff_tw * 32, 0));
+    if (rocc < 1) rocc = 1;
+    rfn<<<(unsigned)(sms * rocc), p.handoff_tw * 32, 0, st>>>(a, p.handoff_next);
+    SHK_LAUNCHED();
+  }
   return 0;
 }
 

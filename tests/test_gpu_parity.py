@@ -255,6 +255,10 @@ def test_c2_build_golden():
     {"SHK_TREE_SLOT_AWARE": "0"},          # every warp slot takes split nodes
     {"SHK_TREE_SLOW_WID": "4"},            # splits on the 4 lowest slots only
     {"SHK_TREE_SLOW_WID": "31", "SHK_TREE_IDLE_WID": "24"},
+    {"SHK_TREE_HANDOFF_TW": "0"},          # no tail hand-off
+    {"SHK_TREE_HANDOFF_TW": "1"},          # resume teams of 1, 2, 4 warps
+    {"SHK_TREE_HANDOFF_TW": "2"},
+    {"SHK_TREE_HANDOFF_TW": "4"},
 ])
 def test_c2_build_schedule_independent(monkeypatch, env):
     """The persistent tree kernel's schedule (which warp slots take split nodes
@@ -268,6 +272,42 @@ def test_c2_build_schedule_independent(monkeypatch, env):
     keys = W.keys_as_bytes(W.build_keys(2))
     blob = recsplit.build(keys, 500, 24).serialize()
     assert sha(blob) == golden("c2.json")["desc_sha"]
+
+
+@pytest.mark.parametrize("n,mode", [(24, 1), (40, 2)])
+def test_tree_handoff_exact(monkeypatch, n, mode):
+    """Tail hand-off (shk_tree.cu): once every leaf is handed out, the
+    leaves still searching stop at a round boundary and tree_resume_kernel
+    finishes them with multi-warp teams.  The seeds (Rice stream), the choice
+    bits and every reference counter equal the uninterrupted search's, for the
+    plain rotation and the k-aligned cached rotation."""
+    from paper_2308_09561_b200 import recsplit
+    from paper_2308_09561_b200 import shockhash as leaf_mod
+    from paper_2308_09561_b200 import workloads as W
+    from paper_2308_09561_b200.keys import master_hash_many
+    from paper_2308_09561_b200._kernels import kernels as K
+
+    keys = W.keys_as_bytes(W.build_keys(2))
+    hi, lo = master_hash_many(keys, 0)
+    N, b = len(keys), 500
+    nb = (N + b - 1) // b
+    ck = leaf_mod.DEFAULT_CACHE_K if mode == 2 else 0
+    out = {}
+    for tw in ("0", "8", "2"):
+        monkeypatch.setenv("SHK_TREE_HANDOFF_TW", tw)
+        gb = K.GpuBuild(hi, lo, nb)
+        plans = recsplit.packed_plans_for_prefix(gb.key_prefix(), n, recsplit.leaf_g_table(n))
+        st = gb.run(plans, 1, ck, leaf_mod.CACHE_MIN_LEAF, 0, nb, leaf_mod.MAX_SEED)
+        words, bits, _ = gb.stream()
+        out[tw] = (st, words, bits, gb.choice())
+        gb.close()
+    assert out["0"][0][7] == 0
+    for tw in ("8", "2"):
+        st, words, bits, ch = out[tw]
+        assert st[7] > 0, "no leaf was handed off"
+        assert (st[:7] == out["0"][0][:7]).all()
+        assert bits == out["0"][2] and (words == out["0"][1]).all()
+        assert (ch == out["0"][3]).all()
 
 
 def test_small_builds_golden():

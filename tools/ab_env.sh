@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 i=0
 for e in "$@"; do
   i=$((i+1))
-  env $e python bench.py --steps 5 --warmup 3 --no-cpu-baseline --queries 0 --leaf-configs "" --no-check \
+  env $e python bench.py --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline --queries 0 --leaf-configs "" --no-check \
     > gpurun_out/abenv_$i.json 2> gpurun_out/abenv_$i.err
   python - "$e" "$i" <<'PY'
 import json, sys
