@@ -84,7 +84,14 @@ SHK_D void split_partition(const ulonglong2* kp, ulonglong2* kw, ulonglong2* tmp
 // High word of remix(hi, lo, seed, tag) (all the split hash needs), from a
 // pre-mixed key high word and seed mixer (shk_hash.cuh, premix_hi).
 #ifndef SHK_SPLIT_SHIFT_MASK
-#define SHK_SPLIT_SHIFT_MASK 0  // bit i: xor-shift i of the split hash takes its high-word shift on the FMA pipe
+// bit i: xor-shift i of the split hash takes its high-word shift on the FMA pipe
+// (IMAD.HI, two issue slots) instead of the ALU pipe (SHF).  With the
+// shared-memory tables the construction kernel is ALU-bound (ncu: ALU 75%,
+// FMA-heavy 62%), so two of the four shifts go back to the FMA pipe.  All 16
+// masks measured at C4 (10-step A/Bs, two rounds each, tools/ab_bench.sh):
+// 0: 91.7 ms, single bits 91.4-91.7, 3: 91.1, 12: 91.1, 5: 90.8 (best),
+// three bits 91.3-91.8, 15: 92.0-92.9.
+#define SHK_SPLIT_SHIFT_MASK 5
 #endif
 template <int S, int I>
 SHK_D u2 split_xs(u2 z) {
