@@ -33,6 +33,29 @@ def test_blake2b_vectors(K):
         assert [int(x) for x in lo] == [r["lo"] for r in rows]
 
 
+@pytest.mark.parametrize("key_len", [1, 3, 7, 8, 9, 15, 16, 17, 24, 31, 32, 33, 64, 100, 127, 128])
+def test_blake2b_fixed_lengths(key_len):
+    """Fixed-length fingerprint kernel (one specialisation per message-word
+    count: <= 8, <= 16, <= 32, <= 128 bytes; word and byte loads) against the
+    reference's definition, keys.py:39-58: hashlib.blake2b(key, digest_size=16,
+    salt=pack("<QQ", salt, 0)) unpacked "<QQ" -> (hi, lo)."""
+    import struct
+
+    from paper_2308_09561_b200 import device as dev
+
+    rng = np.random.default_rng(1000 + key_len)
+    N = 777
+    blob = rng.integers(0, 256, N * key_len, dtype=np.uint8)
+    for salt in (0, 5, (1 << 64) - 1):
+        hi, lo = dev.blake2b_fixed_host(blob, key_len, salt)
+        raw = blob.tobytes()
+        for i in range(N):
+            d = hashlib.blake2b(raw[i * key_len : (i + 1) * key_len], digest_size=16,
+                                salt=struct.pack("<QQ", salt, 0)).digest()
+            eh, el = struct.unpack("<QQ", d)
+            assert (int(hi[i]), int(lo[i])) == (eh, el), (key_len, salt, i)
+
+
 @pytest.mark.parametrize("which", ["plain", "rotate", "rotate_cached"])
 def test_leaf_search_golden(K, which):
     recs = golden("leaves.json")
