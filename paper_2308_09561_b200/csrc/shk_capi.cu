@@ -2121,10 +2121,10 @@ int shk_query(shk_qdesc* q, const uint64_t* hi, const uint64_t* lo, int64_t Q, u
 }
 
 // query_many(keys) end to end from a host buffer of fixed-length keys:
-// chunks of the key blob go H2D on the copy stream, are fingerprinted and
-// queried on the context stream, and the outputs come back D2H on a second
-// copy stream, so the PCIe transfers of chunk k+1 (in) and k-1 (out)
-// overlap the kernels of chunk k.  Host-blocking.  (recsplit.py:270-275:
+// chunks of the key blob go H2D on the copy stream, are fingerprinted on the
+// context stream and queried on a third stream, and the outputs come back D2H
+// on a second copy stream, so the PCIe transfers of chunk k+1 (in) and k-1
+// (out) overlap the kernels of chunk k.  Host-blocking.  (recsplit.py:270-275:
 // master_hash_many + query_hashed_many.)
 int shk_query_blob(shk_qdesc* q, const uint8_t* blob, int key_len, int64_t Q, uint64_t salt, uint64_t* out, int clamp) {
   shk_ctx* c = q->c;
@@ -2135,60 +2135,76 @@ int shk_query_blob(shk_qdesc* q, const uint8_t* blob, int key_len, int64_t Q, ui
   }
   const int64_t CH = (int64_t)1 << 22;  // keys per chunk
   const int64_t per = Q < CH ? Q : CH;
-  DBuf kb[2] = {DBuf(c), DBuf(c)}, ob[2] = {DBuf(c), DBuf(c)}, hh(c), ll(c);
+  // Four stages on four streams, every buffer double: H2D (copy stream) ->
+  // fingerprints (context stream) -> query (its own stream) -> D2H (second
+  // copy stream).  The fingerprint kernel is ALU-bound and the query kernel
+  // gather-bound, so chunk k's query runs beside chunk k+1's fingerprints
+  // and the PCIe transfers bound the call (back to back on one stream the two
+  // kernels of a chunk took longer than its H2D).
+  DBuf kb[2] = {DBuf(c), DBuf(c)}, ob[2] = {DBuf(c), DBuf(c)}, hh[2] = {DBuf(c), DBuf(c)}, ll[2] = {DBuf(c), DBuf(c)};
   for (int k = 0; k < 2; ++k) {
     RC(kb[k].alloc((size_t)per * key_len));
     RC(ob[k].alloc((size_t)per * 8));
+    RC(hh[k].alloc((size_t)per * 8));
+    RC(ll[k].alloc((size_t)per * 8));
   }
-  RC(hh.alloc((size_t)per * 8));
-  RC(ll.alloc((size_t)per * 8));
   int* err = c->d_counter + 5;
   SHK_CUDA(cudaMemsetAsync(err, 0, 4, c->stream));
   const int64_t nch = (Q + per - 1) / per;
-  cudaEvent_t in_done[2], comp_done[2], out_done[2];
+  cudaStream_t qs = nullptr;
+  SHK_CUDA(cudaStreamCreateWithFlags(&qs, cudaStreamNonBlocking));
+  cudaEvent_t in_done[2], hash_done[2], query_done[2], out_done[2];
   for (int k = 0; k < 2; ++k) {
     SHK_CUDA(cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming));
-    SHK_CUDA(cudaEventCreateWithFlags(&comp_done[k], cudaEventDisableTiming));
+    SHK_CUDA(cudaEventCreateWithFlags(&hash_done[k], cudaEventDisableTiming));
+    SHK_CUDA(cudaEventCreateWithFlags(&query_done[k], cudaEventDisableTiming));
     SHK_CUDA(cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming));
   }
   int rc = 0;
+  auto ck = [&](cudaError_t e) {
+    if (e != cudaSuccess && !rc) {
+      shk_set_error("query pipeline: %s", cudaGetErrorString(e));
+      rc = -1000 - (int)e;
+    }
+    return e == cudaSuccess;
+  };
   for (int64_t k = 0; k < nch && !rc; ++k) {
     const int s = (int)(k & 1);
     const int64_t a = k * per, n = (a + per < Q) ? per : Q - a;
-    cudaError_t e = cudaSuccess;
-    if (k >= 2) e = cudaStreamWaitEvent(c->copy, comp_done[s], 0);  // the key buffer was consumed
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(kb[s].p, blob + (size_t)a * key_len, (size_t)n * key_len, cudaMemcpyHostToDevice, c->copy);
-    if (e == cudaSuccess) e = cudaEventRecord(in_done[s], c->copy);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, in_done[s], 0);
-    if (e == cudaSuccess && k >= 2) e = cudaStreamWaitEvent(c->stream, out_done[s], 0);  // outputs copied out
-    if (e != cudaSuccess) {
-      shk_set_error("query pipeline: %s", cudaGetErrorString(e));
-      rc = -1000 - (int)e;
+    // H2D: the key buffer is free once chunk k-2 was fingerprinted
+    if (k >= 2 && !ck(cudaStreamWaitEvent(c->copy, hash_done[s], 0))) break;
+    if (!ck(cudaMemcpyAsync(kb[s].p, blob + (size_t)a * key_len, (size_t)n * key_len, cudaMemcpyHostToDevice, c->copy)))
       break;
-    }
-    rc = shk_launch_blake2b_fixed(kb[s].as<uint8_t>(), key_len, n, salt, hh.as<uint64_t>(), ll.as<uint64_t>(),
+    if (!ck(cudaEventRecord(in_done[s], c->copy))) break;
+    // fingerprints: the code buffers are free once chunk k-2 was queried
+    if (!ck(cudaStreamWaitEvent(c->stream, in_done[s], 0))) break;
+    if (k >= 2 && !ck(cudaStreamWaitEvent(c->stream, query_done[s], 0))) break;
+    rc = shk_launch_blake2b_fixed(kb[s].as<uint8_t>(), key_len, n, salt, hh[s].as<uint64_t>(), ll[s].as<uint64_t>(),
                                   c->stream);
-    if (!rc) rc = shk_launch_query(q->d, hh.as<uint64_t>(), ll.as<uint64_t>(), n, ob[s].as<uint64_t>(), err, clamp,
-                                   c->stream);
     if (rc) break;
-    e = cudaEventRecord(comp_done[s], c->stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy_out, comp_done[s], 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(out + a, ob[s].p, (size_t)n * 8, cudaMemcpyDeviceToHost, c->copy_out);
-    if (e == cudaSuccess) e = cudaEventRecord(out_done[s], c->copy_out);
-    if (e != cudaSuccess) {
-      shk_set_error("query pipeline: %s", cudaGetErrorString(e));
-      rc = -1000 - (int)e;
-    }
+    if (!ck(cudaEventRecord(hash_done[s], c->stream))) break;
+    // query: the output buffer is free once chunk k-2 was copied out
+    if (!ck(cudaStreamWaitEvent(qs, hash_done[s], 0))) break;
+    if (k >= 2 && !ck(cudaStreamWaitEvent(qs, out_done[s], 0))) break;
+    rc = shk_launch_query(q->d, hh[s].as<uint64_t>(), ll[s].as<uint64_t>(), n, ob[s].as<uint64_t>(), err, clamp, qs);
+    if (rc) break;
+    if (!ck(cudaEventRecord(query_done[s], qs))) break;
+    // D2H
+    if (!ck(cudaStreamWaitEvent(c->copy_out, query_done[s], 0))) break;
+    if (!ck(cudaMemcpyAsync(out + a, ob[s].p, (size_t)n * 8, cudaMemcpyDeviceToHost, c->copy_out))) break;
+    if (!ck(cudaEventRecord(out_done[s], c->copy_out))) break;
   }
   cudaStreamSynchronize(c->copy);
   cudaStreamSynchronize(c->stream);
+  cudaStreamSynchronize(qs);
   cudaStreamSynchronize(c->copy_out);
   for (int k = 0; k < 2; ++k) {
     cudaEventDestroy(in_done[k]);
-    cudaEventDestroy(comp_done[k]);
+    cudaEventDestroy(hash_done[k]);
+    cudaEventDestroy(query_done[k]);
     cudaEventDestroy(out_done[k]);
   }
+  cudaStreamDestroy(qs);
   if (rc) return rc;
   int herr = 0;
   RC(d2h(c, &herr, err, 4));
